@@ -1,0 +1,181 @@
+/*
+ * b200moe -- C ABI of the B200-native MoE-layer hot path.
+ *
+ * The reference (moefold, /root/reference/pkg/src/moefold) is a pure
+ * Python/numpy simulator: it has no FFI.  Its drop-in boundary is the Python
+ * API re-exported by moefold/__init__.py:7-69; the package
+ * paper_2504_14960_b200 mirrors that API and binds the entry points below with
+ * ctypes.  Each entry point names the reference function
+ * whose arithmetic it replaces.
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless stated otherwise;
+ *   - `stream` is a cudaStream_t passed as void*; nothing here synchronises
+ *     the device or allocates memory (callers pass workspaces);
+ *   - return value: B200MOE_OK or an error code; b200moe_last_error() gives a
+ *     message.  Shape/argument validation happens before any launch.
+ *   - dtype codes: B200MOE_F32 (float32) / B200MOE_BF16 (bfloat16).
+ */
+#ifndef B200MOE_H_
+#define B200MOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define B200MOE_API __attribute__((visibility("default")))
+#else
+#define B200MOE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B200MOE_OK 0
+#define B200MOE_EINVAL 1        /* bad argument / shape (ValidationError) */
+#define B200MOE_ELAUNCH 2       /* CUDA launch or runtime failure        */
+#define B200MOE_EUNSUPPORTED 3  /* configuration not supported by a kernel */
+#define B200MOE_ENODEV 4        /* no sm_100 device                       */
+
+#define B200MOE_F32 0
+#define B200MOE_BF16 1
+
+#define B200MOE_GATE_SOFTMAX 0 /* router.py:146-147 */
+#define B200MOE_GATE_SIGMOID 1 /* router.py:148-149 */
+
+#define B200MOE_ACT_RELU 0   /* experts.py:24-25 */
+#define B200MOE_ACT_GELU 1   /* experts.py:26-28 (tanh approximation) */
+#define B200MOE_ACT_SWIGLU 2 /* builder-defined: silu(x Wg) * (x Wu) */
+
+#define B200MOE_MAJOR_K 0
+#define B200MOE_MAJOR_MN 1
+
+B200MOE_API const char* b200moe_version(void);
+B200MOE_API const char* b200moe_last_error(void);
+/* 0 when the current device is sm_100 (B200); B200MOE_ENODEV otherwise. */
+B200MOE_API int b200moe_device_check(void);
+
+/* ---------------------------------------------------------------- router */
+
+/* logits[T,E] (fp32) = x[T,H] @ w_g[H,E]                -- router.py:145 */
+B200MOE_API int b200moe_router_logits(const void* x, int x_dtype, const float* w_g, int64_t T, int64_t H,
+                          int E, float* logits, void* stream);
+
+/* scores = softmax/sigmoid(logits) (fp64 internally, stored fp32),
+ * topk_idx[T,k] best first with ties to the lower expert id, gates[T,k] raw
+ * or renormalised over the k winners.  gates_f64 (nullable) receives the
+ * float64 gates, used as the probability-priority key.  -- router.py:112-162 */
+B200MOE_API int b200moe_router_topk(const float* logits, int64_t T, int E, int k, int gate_fn, int renorm,
+                        float* scores, int32_t* topk_idx, float* gates, double* gates_f64,
+                        void* stream);
+
+/* Workspace bytes needed by b200moe_dispatch_plan for T tokens, E experts. */
+B200MOE_API size_t b200moe_dispatch_plan_ws(int64_t T, int E);
+
+/* Capacity dropping + dispatch plan as one stable counting sort by expert.
+ *   router.py:165-206 (apply_capacity, position priority) and
+ *   dispatcher.py:96-131 (build_dispatch_plan).
+ * kept_in   [T*k] u8, nullable: pairs with 0 are treated as already dropped.
+ * order     [T] i32, nullable: token admission order for capacity (identity
+ *           when positions are increasing in row order).
+ * cap       per-expert capacity; <= 0 means dropless.
+ * align     row alignment of each expert segment in the padded (GEMM) layout.
+ * Outputs: kept_out[T*k] u8; expert_counts[E] (kept pairs);
+ *   expert_offsets[E+1] (unpadded, send order); padded_offsets[E+1];
+ *   send_row[T*k] (row of the pair in reference permutation order, -1 when
+ *   dropped); gemm_row[T*k] (row in the padded expert-major layout, -1);
+ *   perm[T*k] i64: perm[send_row] = token*k + slot (DispatchPlan.permutation);
+ *   perm_gates[T*k] f32 nullable: gate of each send row (DispatchPlan.gates). */
+B200MOE_API int b200moe_dispatch_plan(const int32_t* topk_idx, const float* gates, const uint8_t* kept_in,
+                          const int32_t* order, int64_t T, int k, int E, int64_t cap, int align,
+                          void* workspace, size_t workspace_bytes, uint8_t* kept_out,
+                          int32_t* expert_counts, int32_t* expert_offsets, int32_t* padded_offsets,
+                          int32_t* send_row, int32_t* gemm_row, int64_t* perm, float* perm_gates,
+                          void* stream);
+
+/* Probability-priority capacity (router.py:195): pair (t,s) of expert e is
+ * kept iff fewer than `cap` pairs of e precede it in (-gate, position, slot)
+ * order.  The pairs are given expert-segmented by a dropless plan
+ * (perm0 / offsets0 from b200moe_dispatch_plan with cap <= 0);
+ * gates_f64 [T*k]; positions[T] i64 nullable (identity). */
+B200MOE_API int b200moe_capacity_by_gate(const int64_t* perm0, const int32_t* offsets0, const double* gates_f64,
+                             const int64_t* positions, int64_t T, int k, int E, int64_t cap,
+                             uint8_t* kept_out, void* stream);
+
+/* dz[T,E] = d(gates)/d(logits)^T dgates                 -- dispatcher.py:470-488 */
+B200MOE_API int b200moe_router_bwd(const float* dgates, const float* scores, const int32_t* topk_idx,
+                       const float* gates, int64_t T, int E, int k, int gate_fn, int renorm,
+                       float* dz, void* stream);
+
+/* dw_g[H,E] (fp32, overwritten) = x^T dz, fixed-order (deterministic)
+ *                                                        -- dispatcher.py:489 */
+B200MOE_API int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz, int64_t T, int64_t H, int E,
+                         float* dw_g, void* stream);
+
+/* ------------------------------------------------------- permute/combine */
+
+/* out[row_of(t,s)] = x[t] (* scale[t,s] when scale != NULL) for every kept
+ * pair (pair_row >= 0).                                 -- dispatcher.py:134-142
+ * When padded_offsets/expert_counts are given, rows
+ * [padded_offsets[e]+expert_counts[e], padded_offsets[e+1]) are zeroed. */
+B200MOE_API int b200moe_permute(const void* x, int dtype, int64_t T, int64_t H, int k, const int32_t* pair_row,
+                    const float* scale, void* out, const int32_t* padded_offsets,
+                    const int32_t* expert_counts, int E, int align, void* stream);
+
+/* Backward dispatch (dispatcher.py:426-428): dy_rows[row] = gate * u[t] and
+ * dgates[t*k+s] = <u[t], y_rows[row]> (0 for dropped pairs). */
+B200MOE_API int b200moe_permute_bwd(const void* u, int dtype, int64_t T, int64_t H, int k,
+                        const int32_t* pair_row, const float* gates, const void* y_rows,
+                        void* dy_rows, float* dgates, const int32_t* padded_offsets,
+                        const int32_t* expert_counts, int E, int align, void* stream);
+
+/* out[t] = sum_s w[t,s] * rows[row_of(t,s)] (+ dz[t] @ w_g^T when dz != NULL)
+ * with w = gates (or 1 when gates == NULL); tokens with no kept pair get 0.
+ * w_gT is the TRANSPOSED gating matrix [E, H] fp32.  accumulate: out += ...
+ *                       -- dispatcher.py:145-157 (fwd), :467-468,490 (bwd) */
+B200MOE_API int b200moe_combine(const void* rows, int dtype, int64_t T, int64_t H, int k,
+                    const int32_t* pair_row, const float* gates, const float* dz,
+                    const float* w_gT, int E, void* out, int out_dtype, int accumulate,
+                    void* stream);
+
+/* ------------------------------------------------------------ expert GEMM */
+
+/* Grouped GEMM, fp32 accumulation:  C_g = A_g · B_g  for g < G.
+ *   A(m,k) = A[(m_base+m)*a_sm + (k_base+k)*a_sk]
+ *   B(k,n) = B[b_group*b_sg + (k_base+k)*b_sk + n*b_sn]
+ *   C(m,n) = C[c_group*c_sg + (m_base+m)*ldc + n]
+ * grouped_dim = 0 ("M"): m_base = group_off[g], M_g = group_off[g+1]-group_off[g],
+ *   k_base = 0, K fixed, b_group = group_expert[g] (identity when NULL), c_group = 0.
+ * grouped_dim = 1 ("K"): k_base = group_off[g], K_g likewise, m_base = 0,
+ *   M fixed, b_group = 0, c_group = g.
+ * group_off is a DEVICE array [G+1]; group sizes never leave the device. */
+typedef struct {
+  int dtype_in;      /* B200MOE_F32 | B200MOE_BF16 (A and B) */
+  int dtype_out;     /* B200MOE_F32 | B200MOE_BF16 */
+  int grouped_dim;   /* 0 = M, 1 = K */
+  int accumulate;    /* C += A·B (fp32 out only) */
+  int G;
+  int64_t M, N, K;   /* the fixed extents (M ignored for grouped M, K for grouped K) */
+  const void* A; int64_t a_sm, a_sk;
+  const void* B; int64_t b_sg, b_sk, b_sn;
+  void* C; int64_t c_sg, ldc;
+  const int32_t* group_off;
+  const int32_t* group_expert;
+  int64_t max_rows;  /* upper bound of group_off[G] (buffer capacity) */
+} b200moe_gemm_args;
+
+/* Portable SIMT implementation (fp32 parity mode and cross-check). */
+B200MOE_API int b200moe_gemm_simt(const b200moe_gemm_args* args, void* stream);
+
+/* Elementwise expert activations in the padded row layout, rows < group_off[G].
+ * SwiGLU layout: pre has 2F columns, 64-column blocks of [32 gate | 32 up]. */
+B200MOE_API int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,
+                    int64_t max_rows, int64_t F, void* h, void* stream);
+B200MOE_API int b200moe_act_bwd(const void* dh, const void* pre, int dtype, int act, const int32_t* group_off,
+                    int G, int64_t max_rows, int64_t F, void* dpre, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200MOE_H_ */

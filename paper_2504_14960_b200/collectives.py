@@ -1,0 +1,389 @@
+"""Rank worlds and the variable-count collectives of the MoE layer.
+
+Mirrors the reference's per-rank API (/root/reference/pkg/src/moefold/
+collectives.py: VarBuffer :42-78, SimWorld.run :128-173, RankContext
+.all_to_all_v / all_gather_v / reduce_scatter_v / all_reduce / exchange_meta
+:260-327) with device tensors instead of numpy arrays.
+
+Two worlds implement it:
+  * ``NcclWorld``  -- production: one process per GPU (torchrun), collectives
+    over NCCL process groups built from the folded EP/ETP/EDP meshes.
+  * ``LocalWorld`` -- N simulated ranks as threads of one process sharing one
+    GPU (and its default stream); collectives are device copies performed by
+    the last rank to arrive, like SimWorld.  Used by the parity tests to run
+    multi-rank topologies on a single B200.  No kernel ever waits on another
+    rank's kernel, so emulated ranks cannot deadlock the GPU.
+
+Both also provide the engine-level primitives ``p2p`` (a batch of row-chunk
+sends/receives) and ``gather_counts`` (all-gather of small int vectors to
+host memory; the only host synchronisation of the dispatch).
+"""
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+from typing import Any, Callable, Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from .errors import ProtocolError, ValidationError
+
+Group = Tuple[int, ...]
+_STALL_TIMEOUT_S = 120.0
+
+
+@dataclass
+class VarBuffer:
+    """Variable-count row payload: ``values`` [sum(counts), row_width]."""
+
+    values: torch.Tensor
+    row_width: int
+    counts: np.ndarray
+
+    def __post_init__(self):
+        self.counts = np.asarray(self.counts, dtype=np.int64).ravel()
+        if self.row_width < 1:
+            raise ValidationError("row_width must be >= 1", constraint="row_width>=1")
+        if np.any(self.counts < 0):
+            raise ValidationError("counts must be >= 0", constraint="counts>=0")
+        if self.values.numel() != self.row_width * int(self.counts.sum()):
+            raise ValidationError(
+                f"values length {self.values.numel()} != row_width {self.row_width} * total rows "
+                f"{int(self.counts.sum())}", constraint="values==row_width*sum(counts)")
+        self.values = self.values.reshape(-1, self.row_width)
+
+    @classmethod
+    def from_rows(cls, rows: torch.Tensor, counts=None) -> "VarBuffer":
+        if rows.dim() != 2:
+            raise ValidationError("from_rows expects a 2-D tensor", constraint="rows-2d")
+        return cls(rows, rows.shape[1], [rows.shape[0]] if counts is None else counts)
+
+    def rows(self) -> torch.Tensor:
+        return self.values
+
+
+def _check_group(rank: int, group: Group):
+    if rank not in group:
+        raise ProtocolError(f"rank {rank} called a collective on group {group} it is not part of")
+    if any(group[i] >= group[i + 1] for i in range(len(group) - 1)):
+        raise ProtocolError(f"group must list distinct ranks in ascending order, got {group}")
+
+
+# =============================================================== LocalWorld
+class _Slot:
+    __slots__ = ("payloads", "results", "remaining")
+
+    def __init__(self):
+        self.payloads: Dict[int, Any] = {}
+        self.results: Optional[Dict[int, Any]] = None
+        self.remaining = 0
+
+
+class LocalWorld:
+    """N ranks as threads on one device (SimWorld analogue)."""
+
+    def __init__(self, n_ranks: int, device=None):
+        if n_ranks < 1:
+            raise ValidationError("n_ranks must be >= 1", constraint="n_ranks>=1")
+        self.n_ranks = n_ranks
+        self.device = torch.device(device or "cuda")
+        self._cond = threading.Condition()
+        self._slots: Dict[tuple, _Slot] = {}
+        self._seq: Dict[tuple, int] = {}
+        self._epoch = 0
+        self._failure: Optional[BaseException] = None
+
+    def run(self, program: Callable[["RankContext"], Any], *, workers: Optional[int] = None) -> List[Any]:
+        with self._cond:
+            self._epoch += 1
+            self._failure = None
+            self._seq = {}
+            self._slots = {}
+        results: List[Any] = [None] * self.n_ranks
+        errors: Dict[int, BaseException] = {}
+
+        def runner(rank: int):
+            try:
+                torch.cuda.set_device(self.device)
+                results[rank] = program(LocalRankContext(self, rank))
+            except _Aborted:
+                pass
+            except BaseException as exc:  # noqa: BLE001
+                errors[rank] = exc
+                with self._cond:
+                    if self._failure is None:
+                        self._failure = exc
+                    self._cond.notify_all()
+
+        if self.n_ranks == 1:
+            runner(0)
+        else:
+            threads = [threading.Thread(target=runner, args=(r,), daemon=True) for r in range(self.n_ranks)]
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join()
+        if self._failure is not None:
+            raise self._failure
+        if errors:
+            raise errors[min(errors)]
+        return results
+
+    def _rendezvous(self, rank: int, group: Group, payload: Any,
+                    compute: Callable[[Group, Dict[int, Any]], Dict[int, Any]]) -> Any:
+        _check_group(rank, group)
+        with self._cond:
+            if self._failure is not None:
+                raise _Aborted()
+            key = (group, rank)
+            seq = self._seq.get(key, 0)
+            self._seq[key] = seq + 1
+            skey = (self._epoch, seq, group)
+            slot = self._slots.setdefault(skey, _Slot())
+            slot.payloads[rank] = payload
+            if len(slot.payloads) == len(group):
+                slot.results = compute(group, slot.payloads)
+                slot.remaining = len(group)
+                slot.payloads = {}
+                self._cond.notify_all()
+            else:
+                while slot.results is None and self._failure is None:
+                    if not self._cond.wait(timeout=_STALL_TIMEOUT_S):
+                        exc = ProtocolError(
+                            f"collective rendezvous stalled: group {group} waited for "
+                            f"{sorted(set(group) - set(slot.payloads))} (round {seq})")
+                        self._failure = exc
+                        self._cond.notify_all()
+                        raise exc
+            if self._failure is not None:
+                raise _Aborted()
+            out = slot.results[rank]
+            slot.remaining -= 1
+            if slot.remaining == 0:
+                del self._slots[skey]
+        return out
+
+
+class _Aborted(BaseException):
+    pass
+
+
+class RankContext:
+    """Per-rank handle (collectives.py:249-327 analogue)."""
+
+    rank: int
+    n_ranks: int
+
+    # reference-API collectives -------------------------------------------
+    def all_to_all_v(self, group: Group, send: VarBuffer) -> VarBuffer:
+        if len(send.counts) != len(group):
+            raise ProtocolError(f"all_to_all_v: rank {self.rank} supplied {len(send.counts)} counts "
+                                f"for a group of {len(group)}")
+        w = send.row_width
+        all_counts = self.gather_counts(group, torch.as_tensor(send.counts, dtype=torch.int64))
+        me = group.index(self.rank)
+        recv_counts = all_counts[:, me]
+        out = torch.empty((int(recv_counts.sum()), w), dtype=send.values.dtype, device=send.values.device)
+        so = np.concatenate(([0], np.cumsum(send.counts)))
+        ro = np.concatenate(([0], np.cumsum(recv_counts)))
+        sends = [(group[j], send.values[so[j]:so[j + 1]]) for j in range(len(group))]
+        recvs = [(group[j], out[ro[j]:ro[j + 1]]) for j in range(len(group))]
+        self.p2p(group, sends, recvs)
+        return VarBuffer(out, w, recv_counts)
+
+    def all_gather_v(self, group: Group, send: VarBuffer) -> Tuple[VarBuffer, np.ndarray]:
+        if len(send.counts) != 1:
+            raise ProtocolError(f"all_gather_v: rank {self.rank} must supply a single row count")
+        w = send.row_width
+        counts = self.gather_counts(group, torch.as_tensor(send.counts, dtype=torch.int64))[:, 0]
+        out = torch.empty((int(counts.sum()), w), dtype=send.values.dtype, device=send.values.device)
+        off = np.concatenate(([0], np.cumsum(counts)))
+        sends = [(r, send.values) for r in group]
+        recvs = [(group[j], out[off[j]:off[j + 1]]) for j in range(len(group))]
+        self.p2p(group, sends, recvs)
+        return VarBuffer(out, w, counts), counts
+
+    def reduce_scatter_v(self, group: Group, values: torch.Tensor, partition_counts: Sequence[int],
+                         row_width: int) -> torch.Tensor:
+        counts = np.asarray(partition_counts, dtype=np.int64)
+        if len(counts) != len(group):
+            raise ProtocolError(f"reduce_scatter_v: rank {self.rank} supplied {len(counts)} "
+                                f"partitions for a group of {len(group)}")
+        vals = values.reshape(-1, row_width)
+        if vals.shape[0] != int(counts.sum()):
+            raise ProtocolError(f"reduce_scatter_v: rank {self.rank} buffer rows {vals.shape[0]} != "
+                                f"partition total {int(counts.sum())}")
+        off = np.concatenate(([0], np.cumsum(counts)))
+        me = group.index(self.rank)
+        mine = counts[me]
+        parts = [torch.empty((int(mine), row_width), dtype=vals.dtype, device=vals.device)
+                 for _ in group]
+        sends = [(group[j], vals[off[j]:off[j + 1]]) for j in range(len(group))]
+        recvs = [(group[j], parts[j]) for j in range(len(group))]
+        self.p2p(group, sends, recvs)
+        total = parts[0].clone()
+        for p in parts[1:]:  # fold in ascending rank order (collectives.py:386-388)
+            total += p
+        return total
+
+    def all_reduce(self, group: Group, values: torch.Tensor, op: str = "sum") -> torch.Tensor:
+        if op not in ("sum", "avg"):
+            raise ValidationError(f"all_reduce op must be sum or avg, got {op!r}", constraint="op")
+        return self._all_reduce(group, values, op)
+
+    def exchange_meta(self, group: Group, payload: Any) -> Dict[int, Any]:
+        raise NotImplementedError
+
+    # engine primitives ---------------------------------------------------
+    def p2p(self, group: Group, sends: List[Tuple[int, torch.Tensor]],
+            recvs: List[Tuple[int, torch.Tensor]]) -> None:
+        raise NotImplementedError
+
+    def gather_counts(self, group: Group, counts: torch.Tensor) -> np.ndarray:
+        """[len(group), n] int64 on the host: row i = member i's vector."""
+        raise NotImplementedError
+
+    def _all_reduce(self, group, values, op):
+        raise NotImplementedError
+
+
+class LocalRankContext(RankContext):
+    def __init__(self, world: LocalWorld, rank: int):
+        self.world = world
+        self.rank = rank
+        self.n_ranks = world.n_ranks
+
+    def exchange_meta(self, group, payload):
+        return self.world._rendezvous(self.rank, group, payload,
+                                      lambda g, p: {r: dict(p) for r in g})
+
+    def gather_counts(self, group, counts):
+        host = counts.detach().to("cpu", torch.int64).numpy().copy()
+        got = self.exchange_meta(group, host)
+        return np.stack([np.asarray(got[r]).ravel() for r in group])
+
+    def p2p(self, group, sends, recvs):
+        payload = (list(sends), list(recvs))
+
+        def compute(g, payloads):
+            # i-th send A->B pairs with the i-th recv on B from A (NCCL order)
+            for b in g:
+                seen: Dict[int, int] = {}
+                for src, dst in payloads[b][1]:
+                    i = seen.get(src, 0)
+                    seen[src] = i + 1
+                    mine = [t for (peer, t) in payloads[src][0] if peer == b]
+                    if i >= len(mine):
+                        raise ProtocolError(f"p2p: rank {b} expects a message from {src} that was not sent")
+                    t = mine[i]
+                    if t.numel() != dst.numel():
+                        raise ProtocolError(f"p2p: size mismatch {src}->{b}: {t.numel()} vs {dst.numel()}")
+                    if t.numel():
+                        dst.copy_(t.reshape(dst.shape))
+            return {r: None for r in g}
+
+        self.world._rendezvous(self.rank, group, payload, compute)
+
+    def _all_reduce(self, group, values, op):
+        def compute(g, payloads):
+            total = payloads[g[0]].clone()
+            for r in g[1:]:
+                total += payloads[r]
+            if op == "avg":
+                total /= len(g)
+            return {r: total.clone() for r in g}
+
+        return self.world._rendezvous(self.rank, group, values, compute)
+
+
+# ================================================================ NcclWorld
+class NcclWorld:
+    """One process per GPU over torch.distributed (NCCL on B200, gloo on CPU
+    for host-logic tests).  Call ``setup_groups`` with every group list the
+    layer will use, identically on all ranks, before the first collective."""
+
+    def __init__(self):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise ValidationError("torch.distributed is not initialised", constraint="dist-init")
+        self.dist = dist
+        self.n_ranks = dist.get_world_size()
+        self.rank = dist.get_rank()
+        self._pgs: Dict[Group, Any] = {}
+        self.device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+
+    def setup_groups(self, group_lists: Sequence[Sequence[Group]]) -> None:
+        for glist in group_lists:
+            for g in glist:
+                g = tuple(g)
+                if g in self._pgs:
+                    continue
+                if len(g) == self.n_ranks:
+                    self._pgs[g] = None  # default group
+                else:
+                    self._pgs[g] = self.dist.new_group(list(g))
+
+    def pg(self, group: Group):
+        if group not in self._pgs:
+            if len(group) == self.n_ranks:
+                return None
+            raise ProtocolError(f"process group {group} was not set up (call setup_groups)")
+        return self._pgs[group]
+
+    def run(self, program, *, workers=None) -> List[Any]:
+        out: List[Any] = [None] * self.n_ranks
+        out[self.rank] = program(NcclRankContext(self))
+        return out
+
+
+class NcclRankContext(RankContext):
+    def __init__(self, world: NcclWorld):
+        self.world = world
+        self.rank = world.rank
+        self.n_ranks = world.n_ranks
+
+    def exchange_meta(self, group, payload):
+        _check_group(self.rank, group)
+        objs: List[Any] = [None] * len(group)
+        self.world.dist.all_gather_object(objs, payload, group=self.world.pg(group))
+        return {r: o for r, o in zip(group, objs)}
+
+    def gather_counts(self, group, counts):
+        _check_group(self.rank, group)
+        dev = self.world.device
+        c = counts.to(dev, torch.int64).reshape(-1).contiguous()
+        out = torch.empty((len(group), c.numel()), dtype=torch.int64, device=dev)
+        self.world.dist.all_gather_into_tensor(out, c, group=self.world.pg(group))
+        return out.cpu().numpy()
+
+    def p2p(self, group, sends, recvs):
+        _check_group(self.rank, group)
+        dist = self.world.dist
+        pg = self.world.pg(group)
+        ops = []
+        self_sends = [t for (p, t) in sends if p == self.rank]
+        self_recvs = [t for (p, t) in recvs if p == self.rank]
+        if len(self_sends) != len(self_recvs):
+            raise ProtocolError("p2p: unmatched self send/recv")
+        for s, r in zip(self_sends, self_recvs):
+            if s.numel():
+                r.copy_(s.reshape(r.shape))
+        for p, t in sends:
+            if p != self.rank and t.numel():
+                ops.append(dist.P2POp(dist.isend, t.contiguous(), p, group=pg))
+        for p, t in recvs:
+            if p != self.rank and t.numel():
+                ops.append(dist.P2POp(dist.irecv, t, p, group=pg))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def _all_reduce(self, group, values, op):
+        _check_group(self.rank, group)
+        t = values.clone()
+        self.world.dist.all_reduce(t, group=self.world.pg(group))
+        if op == "avg":
+            t /= len(group)
+        return t

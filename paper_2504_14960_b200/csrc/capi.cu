@@ -1,0 +1,217 @@
+// extern "C" entry points of libb200moe.so: argument validation, error
+// reporting, dispatch to the kernels.  See include/b200moe.h.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace b200moe {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+// kernels (defined in the other translation units)
+int router_logits(const void*, int, const float*, int64_t, int64_t, int, float*, cudaStream_t);
+int router_topk(const float*, int64_t, int, int, int, int, float*, int32_t*, float*, double*,
+                cudaStream_t);
+size_t plan_ws_bytes(int64_t, int);
+int dispatch_plan(const int32_t*, const float*, const uint8_t*, const int32_t*, int64_t, int, int,
+                  int64_t, int, void*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*,
+                  int64_t*, float*, cudaStream_t);
+int capacity_by_gate(const int64_t*, const int32_t*, const double*, const int64_t*, int64_t, int,
+                     int, int64_t, uint8_t*, cudaStream_t);
+int router_bwd(const float*, const float*, const int32_t*, const float*, int64_t, int, int, int,
+               int, float*, cudaStream_t);
+int router_wgrad(const void*, int, const float*, int64_t, int64_t, int, float*, cudaStream_t);
+int permute(const void*, int, int64_t, int64_t, int, const int32_t*, const float*, void*,
+            const int32_t*, const int32_t*, int, int64_t, cudaStream_t);
+int permute_bwd(const void*, int, int64_t, int64_t, int, const int32_t*, const float*, const void*,
+                void*, float*, const int32_t*, const int32_t*, int, int64_t, cudaStream_t);
+int combine(const void*, int, int64_t, int64_t, int, const int32_t*, const float*, const float*,
+            const float*, int, void*, int, int, cudaStream_t);
+int gemm_simt(const b200moe_gemm_args*, cudaStream_t);
+int act_fwd(const void*, int, int, const int32_t*, int, int64_t, int64_t, void*, cudaStream_t);
+int act_bwd(const void*, const void*, int, int, const int32_t*, int, int64_t, int64_t, void*,
+            cudaStream_t);
+
+}  // namespace b200moe
+
+using namespace b200moe;
+
+#define REQUIRE(cond, ...)          \
+  do {                              \
+    if (!(cond)) {                  \
+      set_error(__VA_ARGS__);       \
+      return B200MOE_EINVAL;        \
+    }                               \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+static inline bool dt_ok(int d) { return d == B200MOE_F32 || d == B200MOE_BF16; }
+
+extern "C" {
+
+const char* b200moe_version(void) { return "b200moe 0.1.0 (sm_100a)"; }
+const char* b200moe_last_error(void) { return g_err; }
+
+int b200moe_device_check(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("no CUDA device");
+    return B200MOE_ENODEV;
+  }
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) {
+    set_error("device %d is sm_%d%d; this library is built for sm_100a only", dev, major, minor);
+    return B200MOE_ENODEV;
+  }
+  return B200MOE_OK;
+}
+
+int b200moe_router_logits(const void* x, int x_dtype, const float* w_g, int64_t T, int64_t H, int E,
+                          float* logits, void* stream) {
+  REQUIRE(dt_ok(x_dtype), "router_logits: bad dtype %d", x_dtype);
+  REQUIRE(T >= 0 && H >= 1 && E >= 1, "router_logits: bad shape T=%lld H=%lld E=%d", (long long)T,
+          (long long)H, E);
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(x && w_g && logits, "router_logits: null pointer");
+  return router_logits(x, x_dtype, w_g, T, H, E, logits, S(stream));
+}
+
+int b200moe_router_topk(const float* logits, int64_t T, int E, int k, int gate_fn, int renorm,
+                        float* scores, int32_t* topk_idx, float* gates, double* gates_f64,
+                        void* stream) {
+  REQUIRE(E >= 1 && k >= 1 && k <= E, "1<=k<=E violated (k=%d, E=%d)", k, E);
+  REQUIRE(k <= 32, "router_topk: k=%d > 32 unsupported", k);
+  REQUIRE(gate_fn == B200MOE_GATE_SOFTMAX || gate_fn == B200MOE_GATE_SIGMOID,
+          "unknown gate_fn %d", gate_fn);
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(logits && scores && topk_idx && gates, "router_topk: null pointer");
+  return router_topk(logits, T, E, k, gate_fn, renorm, scores, topk_idx, gates, gates_f64,
+                     S(stream));
+}
+
+size_t b200moe_dispatch_plan_ws(int64_t T, int E) { return plan_ws_bytes(T, E); }
+
+int b200moe_dispatch_plan(const int32_t* topk_idx, const float* gates, const uint8_t* kept_in,
+                          const int32_t* order, int64_t T, int k, int E, int64_t cap, int align,
+                          void* workspace, size_t workspace_bytes, uint8_t* kept_out,
+                          int32_t* expert_counts, int32_t* expert_offsets, int32_t* padded_offsets,
+                          int32_t* send_row, int32_t* gemm_row, int64_t* perm, float* perm_gates,
+                          void* stream) {
+  REQUIRE(E >= 1 && E <= 4096 && k >= 1 && k <= 16 && k <= E, "dispatch_plan: bad E=%d k=%d", E, k);
+  REQUIRE(align >= 1, "dispatch_plan: align must be >= 1");
+  REQUIRE(T >= 0 && T * k < (int64_t)INT32_MAX, "dispatch_plan: T*k must fit int32");
+  REQUIRE(workspace_bytes >= plan_ws_bytes(T, E), "dispatch_plan: workspace too small");
+  REQUIRE(expert_counts && expert_offsets && padded_offsets && workspace,
+          "dispatch_plan: null pointer");
+  if (T > 0) REQUIRE(topk_idx && kept_out && send_row && gemm_row && perm, "dispatch_plan: null pointer");
+  REQUIRE(!perm_gates || gates, "dispatch_plan: perm_gates needs gates");
+  return dispatch_plan(topk_idx, gates, kept_in, order, T, k, E, cap, align, workspace, kept_out,
+                       expert_counts, expert_offsets, padded_offsets, send_row, gemm_row, perm,
+                       perm_gates, S(stream));
+}
+
+int b200moe_capacity_by_gate(const int64_t* perm0, const int32_t* offsets0, const double* gates_f64,
+                             const int64_t* positions, int64_t T, int k, int E, int64_t cap,
+                             uint8_t* kept_out, void* stream) {
+  REQUIRE(cap >= 1, "capacity_by_gate: cap must be >= 1");
+  REQUIRE(E >= 1 && k >= 1, "capacity_by_gate: bad E/k");
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(perm0 && offsets0 && gates_f64 && kept_out, "capacity_by_gate: null pointer");
+  return capacity_by_gate(perm0, offsets0, gates_f64, positions, T, k, E, cap, kept_out, S(stream));
+}
+
+int b200moe_router_bwd(const float* dgates, const float* scores, const int32_t* topk_idx,
+                       const float* gates, int64_t T, int E, int k, int gate_fn, int renorm,
+                       float* dz, void* stream) {
+  REQUIRE(E >= 1 && k >= 1 && k <= E, "router_bwd: bad E=%d k=%d", E, k);
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(dgates && scores && topk_idx && gates && dz, "router_bwd: null pointer");
+  return router_bwd(dgates, scores, topk_idx, gates, T, E, k, gate_fn, renorm, dz, S(stream));
+}
+
+int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz, int64_t T, int64_t H, int E,
+                         float* dw_g, void* stream) {
+  REQUIRE(dt_ok(x_dtype) && H >= 1 && E >= 1 && T >= 0, "router_wgrad: bad args");
+  REQUIRE(dw_g, "router_wgrad: null pointer");
+  if (T == 0) return cudaMemsetAsync(dw_g, 0, H * E * sizeof(float), S(stream)) == cudaSuccess
+                         ? B200MOE_OK : B200MOE_ELAUNCH;
+  REQUIRE(x && dz, "router_wgrad: null pointer");
+  return router_wgrad(x, x_dtype, dz, T, H, E, dw_g, S(stream));
+}
+
+int b200moe_permute(const void* x, int dtype, int64_t T, int64_t H, int k, const int32_t* pair_row,
+                    const float* scale, void* out, const int32_t* padded_offsets,
+                    const int32_t* expert_counts, int E, int align, void* stream) {
+  REQUIRE(dt_ok(dtype) && H >= 1 && k >= 1 && T >= 0, "permute: bad args");
+  REQUIRE(out, "permute: null output");
+  if (T > 0) REQUIRE(x && pair_row, "permute: null pointer");
+  const int64_t max_pad = (padded_offsets && expert_counts) ? (align > 1 ? align - 1 : 0) : 0;
+  return permute(x, dtype, T, H, k, pair_row, scale, out, padded_offsets, expert_counts, E,
+                 max_pad, S(stream));
+}
+
+int b200moe_permute_bwd(const void* u, int dtype, int64_t T, int64_t H, int k,
+                        const int32_t* pair_row, const float* gates, const void* y_rows,
+                        void* dy_rows, float* dgates, const int32_t* padded_offsets,
+                        const int32_t* expert_counts, int E, int align, void* stream) {
+  REQUIRE(dt_ok(dtype) && H >= 1 && k >= 1 && T >= 0, "permute_bwd: bad args");
+  if (T > 0) REQUIRE(u && pair_row && gates && y_rows && dy_rows && dgates, "permute_bwd: null pointer");
+  const int64_t max_pad = (padded_offsets && expert_counts) ? (align > 1 ? align - 1 : 0) : 0;
+  return permute_bwd(u, dtype, T, H, k, pair_row, gates, y_rows, dy_rows, dgates, padded_offsets,
+                     expert_counts, E, max_pad, S(stream));
+}
+
+int b200moe_combine(const void* rows, int dtype, int64_t T, int64_t H, int k,
+                    const int32_t* pair_row, const float* gates, const float* dz,
+                    const float* w_gT, int E, void* out, int out_dtype, int accumulate,
+                    void* stream) {
+  REQUIRE(dt_ok(dtype) && dt_ok(out_dtype) && H >= 1 && k >= 1 && T >= 0, "combine: bad args");
+  REQUIRE(!dz || (w_gT && E >= 1), "combine: dz needs w_gT and E");
+  if (T > 0) REQUIRE(rows && pair_row && out, "combine: null pointer");
+  return combine(rows, dtype, T, H, k, pair_row, gates, dz, w_gT, E, out, out_dtype, accumulate,
+                 S(stream));
+}
+
+int b200moe_gemm_simt(const b200moe_gemm_args* a, void* stream) {
+  REQUIRE(a, "gemm_simt: null args");
+  REQUIRE(dt_ok(a->dtype_in) && dt_ok(a->dtype_out), "gemm_simt: bad dtype");
+  REQUIRE(a->grouped_dim == 0 || a->grouped_dim == 1, "gemm_simt: bad grouped_dim");
+  REQUIRE(a->G >= 1 && a->N >= 1, "gemm_simt: bad G/N");
+  REQUIRE(!a->accumulate || a->dtype_out == B200MOE_F32, "gemm_simt: accumulate needs fp32 out");
+  REQUIRE(a->A && a->B && a->C && a->group_off, "gemm_simt: null pointer");
+  if (a->grouped_dim == 0) REQUIRE(a->K >= 1 && a->max_rows >= 0, "gemm_simt: bad K/max_rows");
+  else REQUIRE(a->M >= 1, "gemm_simt: bad M");
+  return gemm_simt(a, S(stream));
+}
+
+int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,
+                    int64_t max_rows, int64_t F, void* h, void* stream) {
+  REQUIRE(dt_ok(dtype) && G >= 1 && F >= 1, "act_fwd: bad args");
+  REQUIRE(act == B200MOE_ACT_RELU || act == B200MOE_ACT_GELU || act == B200MOE_ACT_SWIGLU,
+          "act_fwd: unknown activation %d", act);
+  REQUIRE(act != B200MOE_ACT_SWIGLU || F % 32 == 0, "act_fwd: swiglu needs F %% 32 == 0");
+  REQUIRE(pre && h && group_off, "act_fwd: null pointer");
+  return act_fwd(pre, dtype, act, group_off, G, max_rows, F, h, S(stream));
+}
+
+int b200moe_act_bwd(const void* dh, const void* pre, int dtype, int act, const int32_t* group_off,
+                    int G, int64_t max_rows, int64_t F, void* dpre, void* stream) {
+  REQUIRE(dt_ok(dtype) && G >= 1 && F >= 1, "act_bwd: bad args");
+  REQUIRE(act == B200MOE_ACT_RELU || act == B200MOE_ACT_GELU || act == B200MOE_ACT_SWIGLU,
+          "act_bwd: unknown activation %d", act);
+  REQUIRE(act != B200MOE_ACT_SWIGLU || F % 32 == 0, "act_bwd: swiglu needs F %% 32 == 0");
+  REQUIRE(dh && pre && dpre && group_off, "act_bwd: null pointer");
+  return act_bwd(dh, pre, dtype, act, group_off, G, max_rows, F, dpre, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,307 @@
+// K2: token permute / unpermute-combine (forward and backward).
+//
+// Reference semantics: dispatcher.py:134-157 (permute, unpermute_combine),
+// :426-428 (backward dispatch rows + dgate), :467-468 + :490 (backward
+// combine + router term).  Token-major: each token row is read once with
+// 16-byte vector loads and written to (or gathered from) its k pair rows, so
+// the kernels are HBM-bound at  T*H*b + P*H*b  bytes.
+#include "common.cuh"
+
+namespace b200moe {
+
+template <typename T>
+__device__ __forceinline__ void scale_vec(Vec16<T>& v, float s) {
+#pragma unroll
+  for (int i = 0; i < Vec16<T>::N; ++i) v.v[i] = from_f32<T>(to_f32(v.v[i]) * s);
+}
+
+// ------------------------------------------------------------------ permute
+template <typename T, int KMAX, bool VEC>
+__global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ x, int64_t Tn, int64_t H,
+                                                      int k, const int32_t* __restrict__ pair_row,
+                                                      const float* __restrict__ scale,
+                                                      T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  int32_t rows[KMAX];
+  float sc[KMAX];
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    rows[s] = (s < k) ? pair_row[t * k + s] : -1;
+    sc[s] = (s < k && scale) ? scale[t * k + s] : 1.f;
+  }
+  const T* src = x + t * H;
+  if (VEC) {
+    constexpr int N = Vec16<T>::N;
+    const int64_t nv = H / N;
+    for (int64_t c = lane; c < nv; c += 32) {
+      Vec16<T> v;
+      v.raw = ld_nc_v4(src + c * N);
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (rows[s] < 0) continue;
+        Vec16<T> o = v;
+        if (scale) scale_vec(o, sc[s]);
+        st_v4(out + (int64_t)rows[s] * H + c * N, o.raw);
+      }
+    }
+  } else {
+    for (int64_t c = lane; c < H; c += 32) {
+      const float v = to_f32(src[c]);
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s)
+        if (rows[s] >= 0) out[(int64_t)rows[s] * H + c] = from_f32<T>(v * sc[s]);
+    }
+  }
+}
+
+// Zero the alignment padding of every expert segment.
+template <typename T>
+__global__ void zero_pad_kernel(T* __restrict__ buf, int64_t H, const int32_t* __restrict__ poff,
+                                const int32_t* __restrict__ cnt) {
+  const int e = blockIdx.y;
+  const int64_t row = (int64_t)poff[e] + cnt[e] + blockIdx.x;
+  if (row >= poff[e + 1]) return;
+  T* p = buf + row * H;
+  for (int64_t c = threadIdx.x; c < H; c += blockDim.x) p[c] = from_f32<T>(0.f);
+}
+
+// ------------------------------------------------------------- permute bwd
+template <typename T, int KMAX, bool VEC>
+__global__ void __launch_bounds__(256) permute_bwd_kernel(
+    const T* __restrict__ u, int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_row,
+    const float* __restrict__ gates, const T* __restrict__ y_rows, T* __restrict__ dy_rows,
+    float* __restrict__ dgates) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  int32_t rows[KMAX];
+  float g[KMAX], dot[KMAX];
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    rows[s] = (s < k) ? pair_row[t * k + s] : -1;
+    g[s] = (s < k) ? gates[t * k + s] : 0.f;
+    dot[s] = 0.f;
+  }
+  const T* src = u + t * H;
+  if (VEC) {
+    constexpr int N = Vec16<T>::N;
+    const int64_t nv = H / N;
+    for (int64_t c = lane; c < nv; c += 32) {
+      Vec16<T> v;
+      v.raw = ld_nc_v4(src + c * N);
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (rows[s] < 0) continue;
+        const int64_t off = (int64_t)rows[s] * H + c * N;
+        Vec16<T> y;
+        y.raw = ld_nc_v4(y_rows + off);
+        Vec16<T> o;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const float uv = to_f32(v.v[i]);
+          dot[s] = fmaf(uv, to_f32(y.v[i]), dot[s]);
+          o.v[i] = from_f32<T>(uv * g[s]);
+        }
+        st_v4(dy_rows + off, o.raw);
+      }
+    }
+  } else {
+    for (int64_t c = lane; c < H; c += 32) {
+      const float uv = to_f32(src[c]);
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (rows[s] < 0) continue;
+        const int64_t off = (int64_t)rows[s] * H + c;
+        dot[s] = fmaf(uv, to_f32(y_rows[off]), dot[s]);
+        dy_rows[off] = from_f32<T>(uv * g[s]);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    if (s >= k) break;
+    const float d = warp_sum(dot[s]);
+    if (lane == 0) dgates[t * k + s] = rows[s] >= 0 ? d : 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ combine
+// TPW tokens per warp so the optional router term (dz[t] @ w_g^T, w_g^T given
+// as [E, H]) reuses each w_g^T chunk across the warp's tokens.
+template <typename Tin, typename Tout, int KMAX, int TPW>
+__global__ void __launch_bounds__(256) combine_kernel(
+    const Tin* __restrict__ rows, int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_row,
+    const float* __restrict__ gates, const float* __restrict__ dz, const float* __restrict__ wgT,
+    int E, Tout* __restrict__ out, int accumulate) {
+  constexpr int N = 4;  // 4 elements per lane per step (8 B bf16 / 16 B fp32)
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * TPW;
+  if (t0 >= Tn) return;
+  int32_t r[TPW][KMAX];
+  float w[TPW][KMAX];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      const int64_t t = t0 + i;
+      const bool ok = t < Tn && s < k;
+      r[i][s] = ok ? pair_row[t * k + s] : -1;
+      w[i][s] = (ok && gates) ? gates[t * k + s] : 1.f;
+    }
+  for (int64_t h = (int64_t)lane * N; h < H; h += 32 * N) {
+    const int nh = (int)min((int64_t)N, H - h);
+    float acc[TPW][N];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc[i][j] = 0.f;
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (r[i][s] < 0) continue;
+        const Tin* p = rows + (int64_t)r[i][s] * H + h;
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+          if (j < nh) acc[i][j] = fmaf(w[i][s], to_f32(p[j]), acc[i][j]);
+      }
+    }
+    if (dz) {
+      for (int e = 0; e < E; ++e) {
+        float wv[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) wv[j] = (j < nh) ? __ldg(wgT + (int64_t)e * H + h + j) : 0.f;
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) {
+          const int64_t t = t0 + i;
+          if (t >= Tn) break;
+          const float d = __ldg(dz + t * E + e);
+#pragma unroll
+          for (int j = 0; j < N; ++j) acc[i][j] = fmaf(d, wv[j], acc[i][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t t = t0 + i;
+      if (t >= Tn) break;
+      Tout* o = out + t * H + h;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        if (j >= nh) break;
+        float v = acc[i][j];
+        if (accumulate) v += to_f32(o[j]);
+        o[j] = from_f32<Tout>(v);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+#define KDISPATCH(k, MACRO)            \
+  if (k <= 1) { MACRO(1); }            \
+  else if (k <= 2) { MACRO(2); }       \
+  else if (k <= 4) { MACRO(4); }       \
+  else if (k <= 8) { MACRO(8); }       \
+  else if (k <= 16) { MACRO(16); }     \
+  else {                               \
+    set_error("k=%d > 16 unsupported", k); \
+    return B200MOE_EUNSUPPORTED;       \
+  }
+
+template <typename T>
+static int launch_permute(const T* x, int64_t Tn, int64_t H, int k, const int32_t* pr,
+                          const float* scale, T* out, const int32_t* poff, const int32_t* cnt,
+                          int E, int64_t max_pad, cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(Tn, 8);
+  const bool vec = (H % Vec16<T>::N) == 0;
+#define PK(KM)                                                                                   \
+  {                                                                                              \
+    if (vec) permute_kernel<T, KM, true><<<grid, 256, 0, st>>>(x, Tn, H, k, pr, scale, out);     \
+    else permute_kernel<T, KM, false><<<grid, 256, 0, st>>>(x, Tn, H, k, pr, scale, out);        \
+  }
+  if (Tn > 0) { KDISPATCH(k, PK) }
+#undef PK
+  if (poff && cnt && max_pad > 0) {
+    dim3 g((unsigned)max_pad, (unsigned)E);
+    zero_pad_kernel<T><<<g, 128, 0, st>>>(out, H, poff, cnt);
+  }
+  B200MOE_CHECK_LAUNCH("permute");
+  return B200MOE_OK;
+}
+
+int permute(const void* x, int dt, int64_t Tn, int64_t H, int k, const int32_t* pr,
+            const float* scale, void* out, const int32_t* poff, const int32_t* cnt, int E,
+            int64_t max_pad, cudaStream_t st) {
+  if (dt == B200MOE_BF16)
+    return launch_permute(static_cast<const __nv_bfloat16*>(x), Tn, H, k, pr, scale,
+                          static_cast<__nv_bfloat16*>(out), poff, cnt, E, max_pad, st);
+  return launch_permute(static_cast<const float*>(x), Tn, H, k, pr, scale,
+                        static_cast<float*>(out), poff, cnt, E, max_pad, st);
+}
+
+template <typename T>
+static int launch_permute_bwd(const T* u, int64_t Tn, int64_t H, int k, const int32_t* pr,
+                              const float* gates, const T* y, T* dy, float* dg,
+                              const int32_t* poff, const int32_t* cnt, int E, int64_t max_pad,
+                              cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(Tn, 8);
+  const bool vec = (H % Vec16<T>::N) == 0;
+#define PB(KM)                                                                                 \
+  {                                                                                            \
+    if (vec) permute_bwd_kernel<T, KM, true><<<grid, 256, 0, st>>>(u, Tn, H, k, pr, gates, y, dy, dg); \
+    else permute_bwd_kernel<T, KM, false><<<grid, 256, 0, st>>>(u, Tn, H, k, pr, gates, y, dy, dg); \
+  }
+  if (Tn > 0) { KDISPATCH(k, PB) }
+#undef PB
+  if (poff && cnt && max_pad > 0) {
+    dim3 g((unsigned)max_pad, (unsigned)E);
+    zero_pad_kernel<T><<<g, 128, 0, st>>>(dy, H, poff, cnt);
+  }
+  B200MOE_CHECK_LAUNCH("permute_bwd");
+  return B200MOE_OK;
+}
+
+int permute_bwd(const void* u, int dt, int64_t Tn, int64_t H, int k, const int32_t* pr,
+                const float* gates, const void* y, void* dy, float* dg, const int32_t* poff,
+                const int32_t* cnt, int E, int64_t max_pad, cudaStream_t st) {
+  if (dt == B200MOE_BF16)
+    return launch_permute_bwd(static_cast<const __nv_bfloat16*>(u), Tn, H, k, pr, gates,
+                              static_cast<const __nv_bfloat16*>(y),
+                              static_cast<__nv_bfloat16*>(dy), dg, poff, cnt, E, max_pad, st);
+  return launch_permute_bwd(static_cast<const float*>(u), Tn, H, k, pr, gates,
+                            static_cast<const float*>(y), static_cast<float*>(dy), dg, poff, cnt,
+                            E, max_pad, st);
+}
+
+template <typename Tin, typename Tout>
+static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const int32_t* pr,
+                          const float* gates, const float* dz, const float* wgT, int E, Tout* out,
+                          int acc, cudaStream_t st) {
+  constexpr int TPW = 4;
+  const unsigned grid = (unsigned)ceil_div(ceil_div(Tn, TPW), 8);
+#define CB(KM) combine_kernel<Tin, Tout, KM, TPW><<<grid, 256, 0, st>>>(rows, Tn, H, k, pr, gates, dz, wgT, E, out, acc)
+  if (Tn > 0) { KDISPATCH(k, CB) }
+#undef CB
+  B200MOE_CHECK_LAUNCH("combine");
+  return B200MOE_OK;
+}
+
+int combine(const void* rows, int dt, int64_t Tn, int64_t H, int k, const int32_t* pr,
+            const float* gates, const float* dz, const float* wgT, int E, void* out, int odt,
+            int acc, cudaStream_t st) {
+  if (dt == B200MOE_BF16) {
+    auto r = static_cast<const __nv_bfloat16*>(rows);
+    if (odt == B200MOE_BF16)
+      return launch_combine(r, Tn, H, k, pr, gates, dz, wgT, E, static_cast<__nv_bfloat16*>(out), acc, st);
+    return launch_combine(r, Tn, H, k, pr, gates, dz, wgT, E, static_cast<float*>(out), acc, st);
+  }
+  auto r = static_cast<const float*>(rows);
+  if (odt == B200MOE_BF16)
+    return launch_combine(r, Tn, H, k, pr, gates, dz, wgT, E, static_cast<__nv_bfloat16*>(out), acc, st);
+  return launch_combine(r, Tn, H, k, pr, gates, dz, wgT, E, static_cast<float*>(out), acc, st);
+}
+
+}  // namespace b200moe

@@ -1,0 +1,611 @@
+// K1: router -- gating logits, softmax/sigmoid + top-k, capacity + dispatch
+// plan (stable counting sort by expert), router backward.
+//
+// Reference semantics: /root/reference/pkg/src/moefold/router.py:112-206 and
+// dispatcher.py:96-131, 470-490.  All integer outputs are deterministic (no
+// atomics whose order could leak into a result).
+#include <float.h>
+
+#include "common.cuh"
+
+namespace b200moe {
+
+// ---------------------------------------------------------------------------
+// logits = x @ w_g                                            (router.py:145)
+// ---------------------------------------------------------------------------
+// E <= 32: lanes split the hidden dim, each lane keeps TPW x E partial sums,
+// one butterfly reduction at the end.  W_g rows (E contiguous floats) are read
+// once per h and reused for the TPW tokens of the warp.
+template <typename T, int EP, int TPW>
+__global__ void __launch_bounds__(256) logits_lane_h_kernel(const T* __restrict__ x,
+                                                            const float* __restrict__ wg,
+                                                            int64_t Tn, int64_t H, int E,
+                                                            float* __restrict__ logits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t t0 = warp * TPW;
+  if (t0 >= Tn) return;
+  float acc[TPW][EP];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int e = 0; e < EP; ++e) acc[i][e] = 0.f;
+  for (int64_t h = lane; h < H; h += 32) {
+    float w[EP];
+#pragma unroll
+    for (int e = 0; e < EP; ++e) w[e] = (e < E) ? __ldg(wg + h * E + e) : 0.f;
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t t = t0 + i;
+      const float xv = (t < Tn) ? to_f32(x[t * H + h]) : 0.f;
+#pragma unroll
+      for (int e = 0; e < EP; ++e) acc[i][e] = fmaf(xv, w[e], acc[i][e]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int e = 0; e < EP; ++e) acc[i][e] = warp_sum(acc[i][e]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t t = t0 + i;
+      if (t >= Tn) break;
+#pragma unroll
+      for (int e = 0; e < EP; ++e)
+        if (e < E) logits[t * E + e] = acc[i][e];
+    }
+  }
+}
+
+// E > 32: lanes split the experts (NPL = E/32 per lane), x values are warp
+// broadcasts.
+template <typename T, int NPL, int TPW>
+__global__ void __launch_bounds__(256) logits_lane_e_kernel(const T* __restrict__ x,
+                                                            const float* __restrict__ wg,
+                                                            int64_t Tn, int64_t H, int E,
+                                                            float* __restrict__ logits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t t0 = warp * TPW;
+  if (t0 >= Tn) return;
+  float acc[TPW][NPL];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) acc[i][j] = 0.f;
+  for (int64_t h = 0; h < H; ++h) {
+    float w[NPL];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int e = lane + 32 * j;
+      w[j] = (e < E) ? __ldg(wg + h * E + e) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t t = t0 + i;
+      const float xv = (t < Tn) ? to_f32(x[t * H + h]) : 0.f;
+#pragma unroll
+      for (int j = 0; j < NPL; ++j) acc[i][j] = fmaf(xv, w[j], acc[i][j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TPW; ++i) {
+    const int64_t t = t0 + i;
+    if (t >= Tn) break;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int e = lane + 32 * j;
+      if (e < E) logits[t * E + e] = acc[i][j];
+    }
+  }
+}
+
+template <typename T>
+static int launch_logits(const T* x, const float* wg, int64_t Tn, int64_t H, int E, float* out,
+                         cudaStream_t st) {
+  const int threads = 256, wpb = threads / 32;
+#define LANE_H(EP, TPW)                                                              \
+  {                                                                                  \
+    int64_t warps = ceil_div(Tn, TPW);                                               \
+    logits_lane_h_kernel<T, EP, TPW><<<(unsigned)ceil_div(warps, wpb), threads, 0, st>>>( \
+        x, wg, Tn, H, E, out);                                                       \
+  }
+#define LANE_E(NPL, TPW)                                                             \
+  {                                                                                  \
+    int64_t warps = ceil_div(Tn, TPW);                                               \
+    logits_lane_e_kernel<T, NPL, TPW><<<(unsigned)ceil_div(warps, wpb), threads, 0, st>>>( \
+        x, wg, Tn, H, E, out);                                                       \
+  }
+  if (E <= 4) LANE_H(4, 8)
+  else if (E <= 8) LANE_H(8, 8)
+  else if (E <= 16) LANE_H(16, 4)
+  else if (E <= 32) LANE_H(32, 2)
+  else if (E <= 64) LANE_E(2, 8)
+  else if (E <= 128) LANE_E(4, 8)
+  else if (E <= 256) LANE_E(8, 4)
+  else {
+    set_error("router_logits: E=%d > 256 unsupported", E);
+    return B200MOE_EUNSUPPORTED;
+  }
+#undef LANE_H
+#undef LANE_E
+  B200MOE_CHECK_LAUNCH("router_logits");
+  return B200MOE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// scores + top-k + gates                              (router.py:112-162)
+// ---------------------------------------------------------------------------
+// One warp per token.  Scores are evaluated in float64 like the reference and
+// the selection key is (score desc, expert id asc) -- the stable argsort of
+// router.py:123.  Lane l owns experts l, l+32, ... (NPL per lane).
+template <int NPL>
+__global__ void __launch_bounds__(256) topk_kernel(const float* __restrict__ logits, int64_t Tn,
+                                                   int E, int k, int gate_fn, int renorm,
+                                                   float* __restrict__ scores,
+                                                   int32_t* __restrict__ topk_idx,
+                                                   float* __restrict__ gates,
+                                                   double* __restrict__ gates64) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  double s[NPL];
+  const float* row = logits + t * E;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int e = lane + 32 * j;
+    s[j] = (e < E) ? (double)row[e] : -DBL_MAX;
+  }
+  if (gate_fn == B200MOE_GATE_SOFTMAX) {
+    double m = -DBL_MAX;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) m = fmax(m, s[j]);
+    m = warp_max(m);
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int e = lane + 32 * j;
+      s[j] = (e < E) ? exp(s[j] - m) : 0.0;
+      sum += s[j];
+    }
+    sum = warp_sum(sum);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) s[j] = s[j] / sum;
+  } else {
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int e = lane + 32 * j;
+      s[j] = (e < E) ? 1.0 / (1.0 + exp(-s[j])) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int e = lane + 32 * j;
+    if (e < E) scores[t * E + e] = (float)s[j];
+  }
+  // k rounds of warp arg-max; `taken` marks this lane's selected entries.
+  unsigned taken = 0;
+  double raw_sum = 0.0;
+  double my_raw = 0.0;  // lane r keeps the raw score of slot r (k <= 32)
+  for (int r = 0; r < k; ++r) {
+    double best = -1.0;
+    int bid = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int e = lane + 32 * j;
+      if (e < E && !((taken >> j) & 1u)) {
+        if (s[j] > best || (s[j] == best && e < bid)) {
+          best = s[j];
+          bid = e;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bid, o);
+      if (ob > best || (ob == best && oi < bid)) {
+        best = ob;
+        bid = oi;
+      }
+    }
+    if ((bid & 31) == lane) taken |= 1u << (bid >> 5);
+    if (lane == r) my_raw = best;
+    raw_sum += best;  // same order on every lane: slot 0, 1, ...
+    if (lane == 0) topk_idx[t * k + r] = bid;
+  }
+  if (lane < k) {
+    const double g = renorm ? my_raw / raw_sum : my_raw;
+    gates[t * k + lane] = (float)g;
+    if (gates64) gates64[t * k + lane] = g;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// capacity + dispatch plan                (router.py:171-206, dispatcher.py:96-131)
+// ---------------------------------------------------------------------------
+// Tokens are processed in chunks of PLAN_CHUNK (one per thread).  Pass 1
+// counts pairs per (chunk, expert); pass 2 scans chunks per expert (fixed
+// order) and lays out expert segments; pass 3 ranks pairs inside the chunk
+// with warp ballots and writes rows.  Because a token's k experts are
+// distinct, the rank of pair (t, s) in (position, slot) order among pairs of
+// expert e equals the number of earlier tokens routed to e.
+constexpr int PLAN_CHUNK = 256;
+
+__global__ void __launch_bounds__(PLAN_CHUNK) plan_count_kernel(
+    const int32_t* __restrict__ topk, const uint8_t* __restrict__ kept_in,
+    const int32_t* __restrict__ order, int64_t Tn, int k, int E, int32_t* __restrict__ chunk_cnt) {
+  extern __shared__ int32_t cnt[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * PLAN_CHUNK + threadIdx.x;
+  if (i < Tn) {
+    const int64_t t = order ? order[i] : i;
+    for (int s = 0; s < k; ++s) {
+      if (kept_in && !kept_in[t * k + s]) continue;
+      atomicAdd(&cnt[topk[t * k + s]], 1);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    chunk_cnt[(int64_t)blockIdx.x * E + e] = cnt[e];
+}
+
+__global__ void __launch_bounds__(1024) plan_scan_kernel(int32_t* __restrict__ chunk_cnt,
+                                                         int64_t nchunks, int E, int64_t cap,
+                                                         int align, int32_t* __restrict__ counts,
+                                                         int32_t* __restrict__ offsets,
+                                                         int32_t* __restrict__ poffsets) {
+  extern __shared__ int32_t kept_cnt[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = 0;
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int32_t v = chunk_cnt[c * E + e];
+      chunk_cnt[c * E + e] = run;  // becomes the chunk base
+      run += v;
+    }
+    const int32_t kc = (cap > 0 && run > cap) ? (int32_t)cap : run;
+    kept_cnt[e] = kc;
+    counts[e] = kc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t o = 0, po = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = o;
+      poffsets[e] = po;
+      o += kept_cnt[e];
+      po += (kept_cnt[e] + align - 1) / align * align;
+    }
+    offsets[E] = o;
+    poffsets[E] = po;
+  }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(PLAN_CHUNK) plan_assign_kernel(
+    const int32_t* __restrict__ topk, const float* __restrict__ gates,
+    const uint8_t* __restrict__ kept_in, const int32_t* __restrict__ order, int64_t Tn, int k,
+    int E, int64_t cap, const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ offsets,
+    const int32_t* __restrict__ poffsets, uint8_t* __restrict__ kept_out,
+    int32_t* __restrict__ send_row, int32_t* __restrict__ gemm_row, int64_t* __restrict__ perm,
+    float* __restrict__ perm_gates) {
+  extern __shared__ int32_t wcnt[];  // [nwarps][E]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = PLAN_CHUNK / 32;
+  const int64_t i = (int64_t)blockIdx.x * PLAN_CHUNK + threadIdx.x;
+  const bool live = i < Tn;
+  const int64_t t = live ? (order ? order[i] : i) : 0;
+  int ex[KMAX];
+  bool val[KMAX];
+  int rk[KMAX];
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    ex[s] = -1;
+    val[s] = false;
+    rk[s] = 0;
+    if (s < k && live) {
+      ex[s] = topk[t * k + s];
+      val[s] = kept_in ? (kept_in[t * k + s] != 0) : true;
+    }
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  for (int e = 0; e < E; ++e) {
+    bool has = false;
+    int slot = -1;
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s)
+      if (val[s] && ex[s] == e) {
+        has = true;
+        slot = s;
+      }
+    const unsigned b = __ballot_sync(0xffffffffu, has);
+    if (has) {
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s)
+        if (s == slot) rk[s] = __popc(b & lt);
+    }
+    if (lane == 0) wcnt[w * E + e] = __popc(b);
+  }
+  __syncthreads();
+  // exclusive prefix over warps, per expert (fixed order)
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = chunk_base[(int64_t)blockIdx.x * E + e];
+    for (int ww = 0; ww < nw; ++ww) {
+      const int32_t v = wcnt[ww * E + e];
+      wcnt[ww * E + e] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (!live) return;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    if (s >= k) break;
+    const int64_t p = t * k + s;
+    if (!val[s]) {
+      kept_out[p] = 0;
+      send_row[p] = -1;
+      gemm_row[p] = -1;
+      continue;
+    }
+    const int e = ex[s];
+    const int32_t r = wcnt[w * E + e] + rk[s];
+    const bool keep = cap <= 0 || r < cap;
+    kept_out[p] = keep ? 1 : 0;
+    if (keep) {
+      const int32_t sr = offsets[e] + r;
+      send_row[p] = sr;
+      gemm_row[p] = poffsets[e] + r;
+      perm[sr] = p;
+      if (perm_gates) perm_gates[sr] = gates[p];
+    } else {
+      send_row[p] = -1;
+      gemm_row[p] = -1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// probability-priority capacity                              (router.py:195)
+// ---------------------------------------------------------------------------
+// Pairs are given expert-segmented (perm0/offsets0 of a dropless plan).  The
+// rank of a pair inside its segment under (-gate, position, slot) is counted
+// against every other pair of the segment, tiled through shared memory:
+// O(n_e^2) work per expert, deterministic.
+__global__ void __launch_bounds__(256) capacity_by_gate_kernel(
+    const int64_t* __restrict__ perm0, const int32_t* __restrict__ off0,
+    const double* __restrict__ g64, const int64_t* __restrict__ positions, int k, int64_t cap,
+    uint8_t* __restrict__ kept_out) {
+  __shared__ double sg[256];
+  __shared__ int64_t sp[256];
+  __shared__ int32_t ss[256];
+  const int e = blockIdx.y;
+  const int32_t beg = off0[e], n = off0[e + 1] - beg;
+  const int32_t mine = blockIdx.x * 256 + threadIdx.x;
+  if ((int32_t)(blockIdx.x * 256) >= n) return;
+  double g = 0.0;
+  int64_t pos = 0;
+  int slot = 0;
+  int64_t pair = -1;
+  if (mine < n) {
+    pair = perm0[beg + mine];
+    g = g64[pair];
+    pos = positions ? positions[pair / k] : pair / k;
+    slot = (int)(pair % k);
+  }
+  int64_t rank = 0;
+  for (int32_t base = 0; base < n; base += 256) {
+    __syncthreads();
+    const int32_t q = base + threadIdx.x;
+    if (q < n) {
+      const int64_t pq = perm0[beg + q];
+      sg[threadIdx.x] = g64[pq];
+      sp[threadIdx.x] = positions ? positions[pq / k] : pq / k;
+      ss[threadIdx.x] = (int32_t)(pq % k);
+    }
+    __syncthreads();
+    const int lim = min(256, n - base);
+    if (mine < n) {
+      for (int j = 0; j < lim; ++j) {
+        const double gq = sg[j];
+        const bool before = gq > g || (gq == g && (sp[j] < pos || (sp[j] == pos && ss[j] < slot)));
+        rank += before ? 1 : 0;
+      }
+    }
+  }
+  if (mine < n) kept_out[pair] = rank < cap ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// router backward                                  (dispatcher.py:470-488)
+// ---------------------------------------------------------------------------
+template <int NPL>
+__global__ void __launch_bounds__(256) router_bwd_kernel(const float* __restrict__ dgates,
+                                                         const float* __restrict__ scores,
+                                                         const int32_t* __restrict__ topk,
+                                                         const float* __restrict__ gates,
+                                                         int64_t Tn, int E, int k, int gate_fn,
+                                                         int renorm, float* __restrict__ dz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  // d_sel per slot, computed redundantly by every lane (k is small)
+  double total = 0.0, inner = 0.0;
+  if (renorm) {
+    for (int s = 0; s < k; ++s) {
+      total += (double)scores[t * E + topk[t * k + s]];
+      inner += (double)dgates[t * k + s] * (double)gates[t * k + s];
+    }
+  }
+  double ds[NPL], sc[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    ds[j] = 0.0;
+    const int e = lane + 32 * j;
+    sc[j] = (e < E) ? (double)scores[t * E + e] : 0.0;
+  }
+  for (int s = 0; s < k; ++s) {
+    const int e = topk[t * k + s];
+    double d = dgates[t * k + s];
+    if (renorm) d = (d - inner) / total;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (lane + 32 * j == e) ds[j] += d;
+  }
+  if (gate_fn == B200MOE_GATE_SOFTMAX) {
+    double dot = 0.0;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) dot += ds[j] * sc[j];
+    dot = warp_sum(dot);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int e = lane + 32 * j;
+      if (e < E) dz[t * E + e] = (float)(sc[j] * (ds[j] - dot));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int e = lane + 32 * j;
+      if (e < E) dz[t * E + e] = (float)(ds[j] * sc[j] * (1.0 - sc[j]));
+    }
+  }
+}
+
+// dW_g = x^T dz: one CTA per 32-wide hidden strip, warps stride the tokens,
+// then a fixed-order reduction over warps.
+template <typename T, int EB>
+__global__ void __launch_bounds__(256) router_wgrad_kernel(const T* __restrict__ x,
+                                                           const float* __restrict__ dz,
+                                                           int64_t Tn, int64_t H, int E,
+                                                           float* __restrict__ dwg) {
+  __shared__ float red[8][32][EB + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t h = (int64_t)blockIdx.x * 32 + lane;
+  for (int e0 = 0; e0 < E; e0 += EB) {
+    float acc[EB];
+#pragma unroll
+    for (int j = 0; j < EB; ++j) acc[j] = 0.f;
+    for (int64_t t = w; t < Tn; t += 8) {
+      const float xv = (h < H) ? to_f32(x[t * H + h]) : 0.f;
+      const float* d = dz + t * E + e0;
+#pragma unroll
+      for (int j = 0; j < EB; ++j)
+        if (e0 + j < E) acc[j] = fmaf(xv, __ldg(d + j), acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < EB; ++j) red[w][lane][j] = acc[j];
+    __syncthreads();
+    if (w == 0 && h < H) {
+#pragma unroll
+      for (int j = 0; j < EB; ++j) {
+        float s = 0.f;
+        for (int ww = 0; ww < 8; ++ww) s += red[ww][lane][j];
+        if (e0 + j < E) dwg[h * E + e0 + j] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+int router_logits(const void* x, int dt, const float* wg, int64_t Tn, int64_t H, int E,
+                  float* out, cudaStream_t st) {
+  if (dt == B200MOE_BF16)
+    return launch_logits(static_cast<const __nv_bfloat16*>(x), wg, Tn, H, E, out, st);
+  return launch_logits(static_cast<const float*>(x), wg, Tn, H, E, out, st);
+}
+
+int router_topk(const float* logits, int64_t Tn, int E, int k, int gate_fn, int renorm,
+                float* scores, int32_t* idx, float* gates, double* gates64, cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(Tn, 8);
+#define TK(NPL) topk_kernel<NPL><<<grid, 256, 0, st>>>(logits, Tn, E, k, gate_fn, renorm, scores, idx, gates, gates64)
+  if (E <= 32) TK(1);
+  else if (E <= 64) TK(2);
+  else if (E <= 128) TK(4);
+  else if (E <= 256) TK(8);
+  else {
+    set_error("router_topk: E=%d > 256 unsupported", E);
+    return B200MOE_EUNSUPPORTED;
+  }
+#undef TK
+  B200MOE_CHECK_LAUNCH("router_topk");
+  return B200MOE_OK;
+}
+
+size_t plan_ws_bytes(int64_t Tn, int E) {
+  const int64_t nch = ceil_div(Tn > 0 ? Tn : 1, PLAN_CHUNK);
+  return (size_t)(nch * E) * sizeof(int32_t);
+}
+
+int dispatch_plan(const int32_t* topk, const float* gates, const uint8_t* kept_in,
+                  const int32_t* order, int64_t Tn, int k, int E, int64_t cap, int align, void* ws,
+                  uint8_t* kept_out, int32_t* counts, int32_t* offsets, int32_t* poffsets,
+                  int32_t* send_row, int32_t* gemm_row, int64_t* perm, float* perm_gates,
+                  cudaStream_t st) {
+  const int64_t nch = ceil_div(Tn > 0 ? Tn : 1, PLAN_CHUNK);
+  int32_t* cc = static_cast<int32_t*>(ws);
+  plan_count_kernel<<<(unsigned)nch, PLAN_CHUNK, E * sizeof(int32_t), st>>>(topk, kept_in, order,
+                                                                           Tn, k, E, cc);
+  plan_scan_kernel<<<1, 1024, E * sizeof(int32_t), st>>>(cc, nch, E, cap, align, counts, offsets,
+                                                         poffsets);
+  const size_t smem = (size_t)(PLAN_CHUNK / 32) * E * sizeof(int32_t);
+#define PA(KM)                                                                                  \
+  plan_assign_kernel<KM><<<(unsigned)nch, PLAN_CHUNK, smem, st>>>(                              \
+      topk, gates, kept_in, order, Tn, k, E, cap, cc, offsets, poffsets, kept_out, send_row,    \
+      gemm_row, perm, perm_gates)
+  if (k <= 2) PA(2);
+  else if (k <= 4) PA(4);
+  else if (k <= 8) PA(8);
+  else if (k <= 16) PA(16);
+  else {
+    set_error("dispatch_plan: k=%d > 16 unsupported", k);
+    return B200MOE_EUNSUPPORTED;
+  }
+#undef PA
+  B200MOE_CHECK_LAUNCH("dispatch_plan");
+  return B200MOE_OK;
+}
+
+int capacity_by_gate(const int64_t* perm0, const int32_t* off0, const double* g64,
+                     const int64_t* positions, int64_t Tn, int k, int E, int64_t cap,
+                     uint8_t* kept_out, cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(Tn > 0 ? Tn : 1, 256), (unsigned)E);
+  capacity_by_gate_kernel<<<grid, 256, 0, st>>>(perm0, off0, g64, positions, k, cap, kept_out);
+  B200MOE_CHECK_LAUNCH("capacity_by_gate");
+  return B200MOE_OK;
+}
+
+int router_bwd(const float* dgates, const float* scores, const int32_t* topk, const float* gates,
+               int64_t Tn, int E, int k, int gate_fn, int renorm, float* dz, cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(Tn, 8);
+#define RB(NPL) router_bwd_kernel<NPL><<<grid, 256, 0, st>>>(dgates, scores, topk, gates, Tn, E, k, gate_fn, renorm, dz)
+  if (E <= 32) RB(1);
+  else if (E <= 64) RB(2);
+  else if (E <= 128) RB(4);
+  else if (E <= 256) RB(8);
+  else {
+    set_error("router_bwd: E=%d > 256 unsupported", E);
+    return B200MOE_EUNSUPPORTED;
+  }
+#undef RB
+  B200MOE_CHECK_LAUNCH("router_bwd");
+  return B200MOE_OK;
+}
+
+int router_wgrad(const void* x, int dt, const float* dz, int64_t Tn, int64_t H, int E, float* dwg,
+                 cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(H, 32);
+  if (dt == B200MOE_BF16)
+    router_wgrad_kernel<__nv_bfloat16, 16><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), dz, Tn, H, E, dwg);
+  else
+    router_wgrad_kernel<float, 16><<<grid, 256, 0, st>>>(static_cast<const float*>(x), dz, Tn, H,
+                                                         E, dwg);
+  B200MOE_CHECK_LAUNCH("router_wgrad");
+  return B200MOE_OK;
+}
+
+}  // namespace b200moe

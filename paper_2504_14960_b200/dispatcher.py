@@ -1,0 +1,580 @@
+"""Token-level dispatch: the MoE layer forward/backward on B200.
+
+Mirrors /root/reference/pkg/src/moefold/dispatcher.py (TokenBlock :44-59,
+DispatchPlan :62-93, build_dispatch_plan :96-131, permute :134-142,
+unpermute_combine :145-157, token_partition :160-194, fabricate_* :197-217,
+ForwardContext :220-229, BackwardResult :232-236, moe_forward :246-384,
+moe_backward :387-510).
+
+Per rank (SPMD), forward:
+  K1 router (logits, top-k, capacity + plan as one counting sort)
+  K2 permute into send order            -- or straight into the padded GEMM
+                                           layout when EP = ETP = 1
+  EP all-to-all-v (counts exchanged once, rows land expert-major /
+  sender-minor, so the reference's receive regroup disappears)
+  ETP all-gather-v -> K3 grouped FFN -> ETP reduce-scatter-v
+  EP all-to-all-v back -> K2 gate-weighted combine
+Backward mirrors it (AG <-> RS swapped), then the router backward and the
+dW_g all-reduce over the world (expert grads over EDP).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import experts as X
+from . import kernels as K
+from .collectives import LocalWorld, RankContext
+from .errors import ValidationError
+from .router import (DROP_FULLSEQUENCE, GATE_CODES, PRIORITY_POSITION, GatingParams,
+                     RoutingDecision, capacity_limit, check_finite, gather_full_sequence_decision,
+                     kept_mask, routing_from_logits)
+from .topology import (GroupSets, ParallelTopology, check_pp_consistency,
+                       generate_parallel_groups, sequence_group)
+
+ALIGN = K.GEMM_ALIGN
+
+
+@dataclass
+class TokenBlock:
+    """One rank's flattened token rows plus their global coordinates."""
+
+    values: object  # [rows, hidden] tensor (CUDA) or array
+    positions: object  # [rows] global token ids
+
+    def __post_init__(self):
+        v = self.values
+        if not isinstance(v, torch.Tensor):
+            v = torch.as_tensor(np.asarray(v, dtype=np.float64))
+        if v.dim() != 2:
+            raise ValidationError("token block must be 2-D", constraint="block-2d")
+        p = torch.as_tensor(np.asarray(self.positions) if not isinstance(self.positions, torch.Tensor)
+                            else self.positions, dtype=torch.int64).cpu()
+        if tuple(p.shape) != (v.shape[0],):
+            raise ValidationError("positions must have one entry per row",
+                                  constraint="positions-per-row")
+        self.values = v
+        self.positions = p
+
+
+@dataclass
+class DispatchPlan:
+    """Permutation and counts of one rank's exchange (dispatcher.py:62-93).
+
+    ``permutation``/``send_counts``/``gates`` follow the reference exactly
+    (host views are materialised lazily).  Device fields drive the kernels:
+    ``send_row``/``gemm_row`` [n,k] map each kept pair to its row in send order
+    / in the padded expert-major layout (-1 when dropped)."""
+
+    dev: K.PlanTensors
+    n_tokens: int
+    k: int
+    ep_size: int
+    local_experts: int
+    pair_gates: Optional[torch.Tensor] = None  # [n,k] fp32 device
+    recv_counts: Optional[np.ndarray] = None
+    _host: Dict = field(default_factory=dict, repr=False)
+
+    def _offsets(self) -> np.ndarray:
+        if "off" not in self._host:
+            self._host["off"] = self.dev.offsets.cpu().numpy().astype(np.int64)
+        return self._host["off"]
+
+    @property
+    def n_send(self) -> int:
+        return int(self._offsets()[-1])
+
+    @property
+    def permutation(self) -> np.ndarray:
+        return self.dev.perm[: self.n_send].cpu().numpy()
+
+    @property
+    def send_counts(self) -> np.ndarray:
+        return self.dev.counts.cpu().numpy().astype(np.int64).reshape(self.ep_size, self.local_experts)
+
+    @property
+    def gates(self) -> np.ndarray:
+        return self.dev.perm_gates[: self.n_send].cpu().numpy()
+
+    @property
+    def kept(self) -> torch.Tensor:
+        return self.dev.kept.bool()
+
+    @property
+    def pair_tokens(self) -> np.ndarray:
+        return self.permutation // self.k
+
+    @property
+    def pair_slots(self) -> np.ndarray:
+        return self.permutation % self.k
+
+    @property
+    def restore(self) -> np.ndarray:
+        return self.permutation
+
+
+def build_dispatch_plan(decision: RoutingDecision, ep_group_size: int,
+                        local_expert_count: int) -> DispatchPlan:
+    """Order a rank's kept pairs for dispatch (dispatcher.py:96-131): one
+    stable counting sort by global expert id on the device."""
+    E = ep_group_size * local_expert_count
+    idx = decision.experts.to(torch.int32).contiguous()
+    if idx.numel() and int(idx.max()) >= E:
+        raise ValidationError(f"expert id {int(idx.max())} out of range for {E} experts",
+                              constraint="expert<E")
+    n, k = idx.shape
+    plan = K.dispatch_plan(idx, decision.gates.float().contiguous(), E, cap=0,
+                           kept_in=decision.kept.to(torch.uint8).contiguous())
+    return DispatchPlan(plan, n, k, ep_group_size, local_expert_count,
+                        pair_gates=decision.gates.float().contiguous())
+
+
+def permute(values, plan: DispatchPlan) -> torch.Tensor:
+    """Gather token rows into send order (dispatcher.py:134-142)."""
+    v = values if isinstance(values, torch.Tensor) else torch.as_tensor(np.asarray(values))
+    v = v.to(plan.dev.send_row.device).contiguous()
+    if v.dtype not in (torch.float32, torch.bfloat16):
+        v = v.float()
+    if v.shape[0] != plan.n_tokens:
+        raise ValidationError(f"block has {v.shape[0]} rows, plan expects {plan.n_tokens}",
+                              constraint="rows==plan.n_tokens")
+    out = K.permute(v, plan.dev.send_row, plan.n_send)
+    return out[: plan.n_send]
+
+
+def unpermute_combine(rows, plan: DispatchPlan, hidden: int) -> torch.Tensor:
+    """Gate-weighted scatter back to token order (dispatcher.py:145-157)."""
+    r = rows if isinstance(rows, torch.Tensor) else torch.as_tensor(np.asarray(rows))
+    r = r.to(plan.dev.send_row.device).contiguous()
+    if r.dtype not in (torch.float32, torch.bfloat16):
+        r = r.float()
+    if r.shape[0] != plan.n_send:
+        raise ValidationError(f"{r.shape[0]} returned rows for {plan.n_send} plan slots",
+                              constraint="rows==plan-slots")
+    if r.shape[0] == 0:
+        r = torch.zeros((1, hidden), dtype=r.dtype, device=r.device)
+    return K.combine(r, plan.dev.send_row, plan.n_tokens, gates=plan.pair_gates)
+
+
+def token_partition(topology: ParallelTopology, seq_len: int, batch: int) -> List[np.ndarray]:
+    """Global token ids per rank: sequences dealt to DP replicas in contiguous
+    batches, each split over TP x CP context-major (dispatcher.py:160-194)."""
+    if topology.pp != 1:
+        raise ValidationError("token partitioning requires pp == 1", constraint="pp==1")
+    shards = topology.tp * topology.cp
+    if seq_len % shards:
+        raise ValidationError(f"seq_len={seq_len} is not divisible by tp*cp={shards}",
+                              constraint="tp*cp|seq_len")
+    if batch % topology.dp:
+        raise ValidationError(f"batch={batch} is not divisible by dp={topology.dp}",
+                              constraint="dp|batch")
+    chunk = seq_len // shards
+    per = batch // topology.dp
+    out = []
+    for rank in range(topology.world_size):
+        t, c, d, _ = topology.attn_coords(rank)
+        shard = c * topology.tp + t
+        starts = (d * per + np.arange(per)) * seq_len + shard * chunk
+        out.append((starts[:, None] + np.arange(chunk)[None, :]).reshape(-1).astype(np.int64))
+    return out
+
+
+def fabricate_token_blocks(topology, seq_len, batch, hidden, seed, dtype=torch.float32, device=None):
+    """Seeded stand-in for attention outputs (dispatcher.py:197-207): x ~ N(0,1)
+    from rng([seed, 2]); blocks hold device tensors of ``dtype``."""
+    x = np.random.default_rng([seed, 2]).standard_normal((batch * seq_len, hidden))
+    parts = token_partition(topology, seq_len, batch)
+    dev = torch.device(device or "cuda")
+    blocks = [TokenBlock(torch.as_tensor(x[p]).to(dev, dtype), p) for p in parts]
+    return x, blocks
+
+
+def fabricate_upstream(topology, seq_len, batch, hidden, seed, dtype=torch.float32, device=None):
+    """dispatcher.py:210-217 (rng([seed, 3]))."""
+    u = np.random.default_rng([seed, 3]).standard_normal((batch * seq_len, hidden))
+    parts = token_partition(topology, seq_len, batch)
+    dev = torch.device(device or "cuda")
+    return u, [torch.as_tensor(u[p]).to(dev, dtype) for p in parts]
+
+
+@dataclass
+class ForwardContext:
+    world: object
+    topology: ParallelTopology
+    params: GatingParams
+    weights_map: Dict[Tuple[int, int], X.ExpertWeights]
+    groups: GroupSets
+    per_rank: List[dict] = field(default_factory=list)
+
+
+@dataclass
+class BackwardResult:
+    input_grads: List[Optional[torch.Tensor]]
+    w_g_grad: torch.Tensor
+    expert_grads: Dict[Tuple[int, int], Tuple[List[torch.Tensor], List[torch.Tensor]]]
+
+
+# =========================================================== rank program
+@dataclass
+class LayerGroups:
+    ep: Tuple[int, ...]
+    etp: Tuple[int, ...]
+    edp: Tuple[int, ...]
+    world: Tuple[int, ...]
+    seq: Tuple[int, ...]
+
+
+@dataclass
+class ExchangeLayout:
+    """Host-side description of one rank's variable-count exchange, computed
+    from the all-gathered count vectors (the one host sync of the layer)."""
+
+    send_off: np.ndarray  # [ep, L] row offset of chunk (dest, le) in send order
+    send_cnt: np.ndarray  # [ep, L]
+    recv_off: np.ndarray  # [ep, L] row of chunk (src, le) in MY padded block
+    recv_cnt: np.ndarray  # [ep, L]
+    block_rows: np.ndarray  # [etp] padded rows of each ETP member's block
+    member_le_off: np.ndarray  # [etp, L+1] padded offsets of le segments inside member blocks
+    member_le_cnt: np.ndarray  # [etp, L] real rows of each le segment
+
+
+def exchange_layout(all_send_counts: np.ndarray, ep_pos: int, etp_all_recv: np.ndarray,
+                    L_: int, align: int = ALIGN) -> ExchangeLayout:
+    """Pure host arithmetic (tested on CPU).
+
+    all_send_counts [ep, ep*L]: row s = EP member s's per-global-expert counts
+    (within this EP group).  etp_all_recv [etp, L]: every ETP member's total
+    received rows per local expert."""
+    ep = all_send_counts.shape[0]
+    mine = all_send_counts[ep_pos].reshape(ep, L_)
+    send_off = np.concatenate(([0], np.cumsum(mine.reshape(-1))))[:-1].reshape(ep, L_)
+    recv_cnt = all_send_counts[:, ep_pos * L_:(ep_pos + 1) * L_]  # [src, le]
+    le_tot = recv_cnt.sum(axis=0)
+    padded = (le_tot + align - 1) // align * align
+    le_base = np.concatenate(([0], np.cumsum(padded)))
+    recv_off = le_base[None, :-1] + np.concatenate(
+        [np.zeros((1, L_), dtype=np.int64), np.cumsum(recv_cnt, axis=0)[:-1]], axis=0)
+    etp = etp_all_recv.shape[0]
+    m_pad = (etp_all_recv + align - 1) // align * align
+    member_le_off = np.concatenate([np.zeros((etp, 1), dtype=np.int64), np.cumsum(m_pad, axis=1)], axis=1)
+    return ExchangeLayout(send_off.astype(np.int64), mine.astype(np.int64), recv_off.astype(np.int64),
+                          recv_cnt.astype(np.int64), member_le_off[:, -1].astype(np.int64),
+                          member_le_off.astype(np.int64), etp_all_recv.astype(np.int64))
+
+
+def _zero_pads(buf: torch.Tensor, starts: List[int], ends: List[int]) -> None:
+    for s, e in zip(starts, ends):
+        if e > s:
+            buf[s:e].zero_()
+
+
+class RankLayer:
+    """Everything one rank needs to run the layer forward and backward."""
+
+    def __init__(self, params: GatingParams, weights: X.ExpertWeights, topology: ParallelTopology,
+                 groups: LayerGroups, rank: int, dtype, device, seq_len=None, check=False):
+        self.params = params
+        self.topo = topology
+        self.g = groups
+        self.rank = rank
+        self.dtype = dtype
+        self.device = device
+        self.seq_len = seq_len
+        self.check = check
+        self.E = params.num_experts
+        self.k = params.k
+        self.L = self.E // topology.ep
+        self.w = weights
+        self.pk = weights.packed(dtype, device)
+        self.wg = params.device_w_g(device)
+        self.wgT = params.device_w_gT(device)
+        self.single = len(groups.ep) == 1 and len(groups.etp) == 1
+
+    # ---------------------------------------------------------------- fwd
+    def forward(self, ctx: Optional[RankContext], x: torch.Tensor, positions: torch.Tensor) -> Tuple[torch.Tensor, dict]:
+        p = self.params
+        T, H = x.shape
+        x = x.to(self.device, self.dtype).contiguous()
+        if self.check:
+            check_finite(x, "token block")
+        logits = K.router_logits(x, self.wg)
+        dec = routing_from_logits(logits, p, positions)
+        return self.forward_routed(ctx, x, dec, logits)
+
+    def forward_routed(self, ctx, x, dec: RoutingDecision, logits=None):
+        p = self.params
+        T, H = x.shape
+        E, k = self.E, self.k
+        # ---- capacity (router.py:171-269) ----
+        if not p.dropless:
+            if p.drop_mode == DROP_FULLSEQUENCE:
+                _, dec = gather_full_sequence_decision(ctx, self.g.seq, dec, self.seq_len, E, p)
+            else:
+                dec.kept = kept_mask(dec, T, E, p).bool()
+        kept_in = None if p.dropless else dec.kept.to(torch.uint8).contiguous()
+        plan = K.dispatch_plan(dec.experts, dec.gates, E, cap=0, kept_in=kept_in)
+        saved = {"x": x, "dec": dec, "plan": plan, "logits": logits}
+        if self.single:
+            # padded expert-major layout straight from the plan; group sizes stay on device
+            R = T * k + E * (ALIGN - 1)
+            R = (R + ALIGN - 1) // ALIGN * ALIGN
+            xp = K.permute(x, plan.gemm_row, R, poffsets=plan.poffsets, counts=plan.counts, E=E)
+            goff = plan.poffsets
+            pre, h, y = X.ffn_forward(xp, goff, E, None, self.pk, R)
+            out = K.combine(y, plan.gemm_row, T, gates=dec.gates)
+            saved.update(xp=xp, pre=pre, h=h, y=y, goff=goff, G=E, gexp=None, R=R,
+                         pair_row=plan.gemm_row)
+            return out, saved
+        return self._forward_exchange(ctx, x, dec, plan, saved)
+
+    def _layout(self, ctx, plan) -> ExchangeLayout:
+        g = self.g
+        all_send = ctx.gather_counts(g.ep, plan.counts.to(torch.int64))  # [ep, E]
+        ep_pos = g.ep.index(self.rank)
+        # this EP group only routes to experts of its own EP coordinate set: E = ep*L
+        lay0 = exchange_layout(all_send, ep_pos, np.zeros((1, self.L), dtype=np.int64), self.L)
+        my_recv_tot = lay0.recv_cnt.sum(axis=0)
+        if len(g.etp) > 1:
+            etp_all = ctx.gather_counts(g.etp, torch.as_tensor(my_recv_tot))
+        else:
+            etp_all = my_recv_tot[None, :]
+        return exchange_layout(all_send, ep_pos, etp_all, self.L)
+
+    def _a2a(self, ctx, lay: ExchangeLayout, src: torch.Tensor, dst: torch.Tensor, forward: bool):
+        """forward: send-order rows -> my padded block; else the reverse."""
+        g = self.g
+        sends, recvs = [], []
+        for j, peer in enumerate(g.ep):
+            for le in range(self.L):
+                so, sc = int(lay.send_off[j, le]), int(lay.send_cnt[j, le])
+                ro, rc = int(lay.recv_off[j, le]), int(lay.recv_cnt[j, le])
+                if forward:
+                    sends.append((peer, src[so:so + sc]))
+                    recvs.append((peer, dst[ro:ro + rc]))
+                else:
+                    sends.append((peer, src[ro:ro + rc]))
+                    recvs.append((peer, dst[so:so + sc]))
+        ctx.p2p(g.ep, sends, recvs)
+
+    def _member_blocks(self, lay):
+        off = np.concatenate(([0], np.cumsum(lay.block_rows)))
+        return off
+
+    def _gather_blocks(self, ctx, lay, mine: torch.Tensor, width: int) -> torch.Tensor:
+        g = self.g
+        if len(g.etp) == 1:
+            return mine
+        off = self._member_blocks(lay)
+        full = torch.empty((int(off[-1]), width), dtype=mine.dtype, device=mine.device)
+        me = g.etp.index(self.rank)
+        sends = [(r, mine) for r in g.etp]
+        recvs = [(g.etp[m], full[off[m]:off[m + 1]]) for m in range(len(g.etp))]
+        ctx.p2p(g.etp, sends, recvs)
+        return full
+
+    def _reduce_blocks(self, ctx, lay, full: torch.Tensor) -> torch.Tensor:
+        g = self.g
+        if len(g.etp) == 1:
+            return full
+        off = self._member_blocks(lay)
+        me = g.etp.index(self.rank)
+        n_me = int(lay.block_rows[me])
+        parts = [torch.empty((n_me, full.shape[1]), dtype=full.dtype, device=full.device)
+                 for _ in g.etp]
+        sends = [(g.etp[m], full[off[m]:off[m + 1]]) for m in range(len(g.etp))]
+        recvs = [(g.etp[m], parts[m]) for m in range(len(g.etp))]
+        ctx.p2p(g.etp, sends, recvs)
+        acc = parts[0].float()
+        for q in parts[1:]:  # ascending ETP rank (collectives.py:386-388)
+            acc += q.float()
+        return acc.to(full.dtype)
+
+    def _groups_dev(self, lay):
+        etp = len(self.g.etp)
+        off = self._member_blocks(lay)
+        goff = []
+        for m in range(etp):
+            goff.extend((off[m] + lay.member_le_off[m, :-1]).tolist())
+        goff.append(int(off[-1]))
+        gexp = [le for _ in range(etp) for le in range(self.L)]
+        dev = self.device
+        return (torch.tensor(goff, dtype=torch.int32, device=dev),
+                torch.tensor(gexp, dtype=torch.int32, device=dev), len(gexp))
+
+    def _pad_ranges(self, lay, me):
+        starts, ends = [], []
+        for le in range(self.L):
+            base = int(lay.member_le_off[me, le])
+            starts.append(base + int(lay.member_le_cnt[me, le]))
+            ends.append(int(lay.member_le_off[me, le + 1]))
+        return starts, ends
+
+    def _forward_exchange(self, ctx, x, dec, plan, saved):
+        T, H = x.shape
+        lay = self._layout(ctx, plan)
+        n_send = int(lay.send_cnt.sum())
+        send = K.permute(x, plan.send_row, max(n_send, 1))
+        me_etp = self.g.etp.index(self.rank)
+        my_rows = int(lay.block_rows[me_etp])
+        block = torch.empty((max(my_rows, 1), H), dtype=x.dtype, device=x.device)
+        self._a2a(ctx, lay, send, block, forward=True)
+        _zero_pads(block, *self._pad_ranges(lay, me_etp))
+        xp = self._gather_blocks(ctx, lay, block[:my_rows], H)
+        goff, gexp, G = self._groups_dev(lay)
+        R = xp.shape[0]
+        pre, h, y = X.ffn_forward(xp, goff, G, gexp, self.pk, R)
+        y_mine = self._reduce_blocks(ctx, lay, y)
+        y_send = torch.empty((max(n_send, 1), H), dtype=x.dtype, device=x.device)
+        self._a2a(ctx, lay, y_mine, y_send, forward=False)
+        out = K.combine(y_send, plan.send_row, T, gates=dec.gates)
+        saved.update(xp=xp, pre=pre, h=h, y=y_send, goff=goff, G=G, gexp=gexp, R=R, lay=lay,
+                     pair_row=plan.send_row, n_send=n_send, my_rows=my_rows)
+        return out, saved
+
+    # ---------------------------------------------------------------- bwd
+    def backward(self, ctx, u: torch.Tensor, sv: dict):
+        p = self.params
+        x, dec, plan = sv["x"], sv["dec"], sv["plan"]
+        T, H = x.shape
+        u = u.to(self.device, self.dtype).contiguous()
+        if tuple(u.shape) != tuple(x.shape):
+            raise ValidationError(f"upstream shape {tuple(u.shape)} does not match input {tuple(x.shape)}",
+                                  constraint="upstream-shape")
+        E = self.E
+        if self.single:
+            dyp, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"], poffsets=plan.poffsets,
+                                        counts=plan.counts, E=E)
+            dxp, dw1g, dw2g = X.ffn_backward(dyp, sv["xp"], sv["pre"], sv["h"], sv["goff"], sv["G"],
+                                            None, self.pk, sv["R"])
+            dw1p, dw2p = dw1g, dw2g
+            rows = dxp
+        else:
+            lay = sv["lay"]
+            dy_send, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"])
+            me_etp = self.g.etp.index(self.rank)
+            my_rows = sv["my_rows"]
+            block = torch.empty((max(my_rows, 1), H), dtype=u.dtype, device=u.device)
+            self._a2a(ctx, lay, dy_send, block, forward=True)
+            _zero_pads(block, *self._pad_ranges(lay, me_etp))
+            dyp = self._gather_blocks(ctx, lay, block[:my_rows], H)
+            dxp, dw1g, dw2g = X.ffn_backward(dyp, sv["xp"], sv["pre"], sv["h"], sv["goff"], sv["G"],
+                                            sv["gexp"], self.pk, sv["R"])
+            # groups (member, le) -> local experts, summed in member order
+            dw1p = dw1g.reshape(len(self.g.etp), self.L, *dw1g.shape[1:]).sum(0)
+            dw2p = dw2g.reshape(len(self.g.etp), self.L, *dw2g.shape[1:]).sum(0)
+            dx_mine = self._reduce_blocks(ctx, lay, dxp)
+            rows = torch.empty((max(sv["n_send"], 1), H), dtype=u.dtype, device=u.device)
+            self._a2a(ctx, lay, dx_mine, rows, forward=False)
+        dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
+                          p.renormalize_topk)
+        dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT)
+        dwg = K.router_wgrad(x, dz)
+        return dx, dwg, dw1p, dw2p
+
+
+# ============================================================ layer API
+def _rank_groups(topology, groups: GroupSets, rank: int) -> LayerGroups:
+    return LayerGroups(groups.group_of("moe", "EP", rank), groups.group_of("moe", "ETP", rank),
+                       groups.group_of("moe", "EDP", rank), tuple(range(topology.world_size)),
+                       sequence_group(topology, rank))
+
+
+def _validate(blocks, topology, params, seq_len):
+    if topology.pp != 1:
+        raise ValidationError("numeric execution requires pp == 1", constraint="pp==1")
+    if len(blocks) != topology.world_size:
+        raise ValidationError(f"{len(blocks)} blocks for world_size {topology.world_size}",
+                              constraint="blocks==world")
+    groups = generate_parallel_groups(topology)
+    verdict = check_pp_consistency(groups)
+    if not verdict.consistent:
+        raise ValidationError(f"pipeline groups differ between meshes: {verdict.mismatch}",
+                              constraint="pp-consistency")
+    E = params.num_experts
+    if E % topology.ep or topology.ep > E:
+        raise ValidationError(f"ep={topology.ep} must divide num_experts={E}", constraint="ep|E")
+    if (not params.dropless) and params.drop_mode == DROP_FULLSEQUENCE and seq_len is None:
+        raise ValidationError("full-sequence dropping needs seq_len", constraint="seq_len-required")
+    return groups
+
+
+def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingParams, world,
+                seq_len: Optional[int] = None, workers: Optional[int] = None, *, dtype=None,
+                check_finite_inputs: bool = True):
+    """Run the MoE layer forward on every rank of ``world`` (dispatcher.py:246-384).
+
+    ``world`` is a LocalWorld (all ranks in this process) or an NcclWorld
+    (this process's rank only; other entries of the returned list are None).
+    ``dtype`` selects the compute precision (torch.float32 parity mode or
+    torch.bfloat16); default: the dtype of the blocks' values (fp64 -> fp32).
+    """
+    groups = _validate(blocks, topology, params, seq_len)
+    if hasattr(world, "setup_groups"):
+        world.setup_groups([groups.moe["EP"], groups.moe["ETP"], groups.moe["EDP"],
+                            [tuple(range(topology.world_size))],
+                            sorted({sequence_group(topology, r) for r in range(topology.world_size)})])
+
+    def program(ctx):
+        rank = ctx.rank
+        b = blocks[rank]
+        etp_idx, ep_idx, _, _ = topology.moe_coords(rank)
+        w = weights_map[(ep_idx, etp_idx)]
+        dev = getattr(world, "device", torch.device("cuda"))
+        dt = dtype or (b.values.dtype if b.values.dtype in (torch.float32, torch.bfloat16) else torch.float32)
+        layer = RankLayer(params, w, topology, _rank_groups(topology, groups, rank), rank, dt, dev,
+                          seq_len, check=check_finite_inputs)
+        out, saved = layer.forward(ctx, b.values, b.positions)
+        saved["layer"] = layer
+        return out, saved
+
+    results = world.run(program, workers=workers)
+    context = ForwardContext(world, topology, params, weights_map, groups)
+    outputs = []
+    for r in results:
+        outputs.append(None if r is None else r[0])
+        context.per_rank.append(None if r is None else r[1])
+    for sv in context.per_rank:
+        if sv is not None:
+            sv["decision"] = sv["dec"]
+    return outputs, context
+
+
+def moe_backward(upstream, context: ForwardContext, workers: Optional[int] = None) -> BackwardResult:
+    """Gradients of sum over ranks of <upstream, output> (dispatcher.py:387-510)."""
+    topology = context.topology
+    if len(upstream) != topology.world_size:
+        raise ValidationError(f"{len(upstream)} upstream blocks for world_size {topology.world_size}",
+                              constraint="upstream==world")
+    world_group = tuple(range(topology.world_size))
+
+    def program(ctx):
+        sv = context.per_rank[ctx.rank]
+        layer: RankLayer = sv["layer"]
+        u = upstream[ctx.rank]
+        if not isinstance(u, torch.Tensor):
+            u = torch.as_tensor(np.asarray(u, dtype=np.float64))
+        dx, dwg, dw1p, dw2p = layer.backward(ctx, u, sv)
+        if topology.world_size > 1:
+            dwg = ctx.all_reduce(world_group, dwg, "sum")
+        if len(layer.g.edp) > 1:
+            flat = torch.cat([dw1p.reshape(-1), dw2p.reshape(-1)])
+            red = ctx.all_reduce(layer.g.edp, flat, "sum")
+            dw1p = red[: dw1p.numel()].reshape(dw1p.shape)
+            dw2p = red[dw1p.numel():].reshape(dw2p.shape)
+        return dx, dwg, dw1p, dw2p, layer.pk.act
+
+    results = context.world.run(program, workers=workers)
+    input_grads = [None if r is None else r[0] for r in results]
+    w_g_grad = next(r[1] for r in results if r is not None)
+    expert_grads = {}
+    for rank, r in enumerate(results):
+        if r is None:
+            continue
+        etp_idx, ep_idx, edp_idx, _ = topology.moe_coords(rank)
+        if edp_idx == 0:
+            expert_grads[(ep_idx, etp_idx)] = (X.unpack_w1_grad(r[2], r[4]), X.unpack_w2_grad(r[3]))
+    return BackwardResult(input_grads, w_g_grad, expert_grads)

@@ -1,0 +1,326 @@
+"""Expert feed-forward networks (reference: /root/reference/pkg/src/moefold/experts.py).
+
+Public API mirrors the reference (ExpertWeights :40-63, full_expert_matrices
+:66-75, init_gating_matrix :78-81, init_expert_weights :84-127,
+expert_forward_shard :130-143, expert_backward_shard :146-172).
+
+B200 layout.  Weights live on the device packed per rank as
+  w1p [L, N1, H]  (N1 = F_shard for relu/gelu, 2*F_shard for SwiGLU)
+  w2p [L, H, F_shard]
+i.e. K-major for the forward GEMMs.  SwiGLU's gate/up columns are interleaved
+in 64-row blocks [32 gate | 32 up] so one accumulator tile holds matching
+gate/up pairs.  Token rows are expert-major and padded to GEMM_ALIGN rows per
+group; the grouped GEMMs read the group offsets from device memory.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import kernels as K
+from .errors import ValidationError
+
+ACT_RELU = "relu"
+ACT_GELU = "gelu"
+ACT_SWIGLU = "swiglu"
+ACTIVATIONS = (ACT_RELU, ACT_GELU, ACT_SWIGLU)
+
+
+def _as_np(a) -> np.ndarray:
+    if isinstance(a, torch.Tensor):
+        return a.detach().cpu().double().numpy()
+    return np.asarray(a, dtype=np.float64)
+
+
+# --------------------------------------------------------------- packing
+def swiglu_interleave_cols(w1: torch.Tensor) -> torch.Tensor:
+    """[H, 2F] = [gate | up]  ->  [2F, H] rows in 64-blocks [32 gate | 32 up]."""
+    H, F2 = w1.shape
+    F = F2 // 2
+    if F % 32:
+        raise ValidationError("swiglu needs ffn % 32 == 0 per shard", constraint="swiglu-ffn%32")
+    g = w1[:, :F].T.reshape(F // 32, 32, H)
+    u = w1[:, F:].T.reshape(F // 32, 32, H)
+    return torch.stack([g, u], dim=1).reshape(F2, H)
+
+
+def swiglu_deinterleave_rows(p: torch.Tensor) -> torch.Tensor:
+    """Inverse of swiglu_interleave_cols: [2F, H] -> [H, 2F] = [gate | up]."""
+    F2, H = p.shape
+    F = F2 // 2
+    b = p.reshape(F // 32, 2, 32, H)
+    g = b[:, 0].reshape(F, H)
+    u = b[:, 1].reshape(F, H)
+    return torch.cat([g, u], dim=0).T
+
+
+def swiglu_deinterleave_cols_rows(pre: torch.Tensor) -> torch.Tensor:
+    """Padded-layout activations [R, 2F] interleaved -> [R, 2F] = [gate | up]."""
+    R, F2 = pre.shape
+    F = F2 // 2
+    b = pre.reshape(R, F // 32, 2, 32)
+    return torch.cat([b[:, :, 0].reshape(R, F), b[:, :, 1].reshape(R, F)], dim=1)
+
+
+@dataclass
+class PackedExperts:
+    w1p: torch.Tensor  # [L, N1, H]
+    w2p: torch.Tensor  # [L, H, F]
+    act: str
+    hidden: int
+    ffn: int  # F_shard
+
+    @property
+    def n1(self) -> int:
+        return self.w1p.shape[1]
+
+    @property
+    def local(self) -> int:
+        return self.w1p.shape[0]
+
+    @property
+    def dtype(self):
+        return self.w1p.dtype
+
+
+def pack_experts(w1: Sequence, w2: Sequence, act: str, dtype, device) -> PackedExperts:
+    mats1, mats2 = [], []
+    for a, b in zip(w1, w2):
+        a = torch.as_tensor(a).to(device=device)
+        b = torch.as_tensor(b).to(device=device)
+        if act == ACT_SWIGLU:
+            mats1.append(swiglu_interleave_cols(a))
+        else:
+            mats1.append(a.T)
+        mats2.append(b.T)
+    w1p = torch.stack(mats1).to(dtype).contiguous()
+    w2p = torch.stack(mats2).to(dtype).contiguous()
+    H = w1p.shape[2]
+    F = w2p.shape[2]
+    return PackedExperts(w1p, w2p, act, H, F)
+
+
+def unpack_w1_grad(dw1p: torch.Tensor, act: str) -> List[torch.Tensor]:
+    """[L, N1, H] device grads -> list of reference-layout [H, N1']."""
+    if act == ACT_SWIGLU:
+        return [swiglu_deinterleave_rows(g) for g in dw1p]
+    return [g.T for g in dw1p]
+
+
+def unpack_w2_grad(dw2p: torch.Tensor) -> List[torch.Tensor]:
+    return [g.T for g in dw2p]
+
+
+# --------------------------------------------------------------- reference API
+@dataclass
+class ExpertWeights:
+    """One rank's shard of its local experts (experts.py:40-63).
+
+    ``w1[i]`` [hidden, ffn/etp] (SwiGLU: [hidden, 2*ffn/etp] = [gate|up]) and
+    ``w2[i]`` [ffn/etp, hidden] of local expert ``expert_ids[i]``; numpy
+    arrays or tensors.  ``packed(dtype, device)`` caches the device layout.
+    """
+
+    expert_ids: Tuple[int, ...]
+    w1: List
+    w2: List
+    activation: str
+    etp_rank: int
+    etp_size: int
+    _packed: Dict = field(default_factory=dict, repr=False, compare=False)
+
+    def local_index(self, expert_id: int) -> int:
+        try:
+            return tuple(self.expert_ids).index(expert_id)
+        except ValueError:
+            raise ValidationError(
+                f"expert {expert_id} is not hosted here (local: {self.expert_ids})",
+                constraint="expert-local") from None
+
+    def packed(self, dtype=torch.bfloat16, device=None) -> PackedExperts:
+        device = torch.device(device or "cuda")
+        key = (dtype, str(device))
+        if key not in self._packed:
+            self._packed[key] = pack_experts(self.w1, self.w2, self.activation, dtype, device)
+        return self._packed[key]
+
+
+def full_expert_matrices(num_experts: int, hidden: int, ffn: int, seed: int):
+    """Unsharded matrices U(+-1/sqrt(H)) from rng([seed, 1]) -- experts.py:66-75."""
+    rng = np.random.default_rng([seed, 1])
+    bound = 1.0 / np.sqrt(hidden)
+    w1 = [rng.uniform(-bound, bound, size=(hidden, ffn)) for _ in range(num_experts)]
+    w2 = [rng.uniform(-bound, bound, size=(ffn, hidden)) for _ in range(num_experts)]
+    return w1, w2
+
+
+def full_swiglu_matrices(num_experts: int, hidden: int, ffn: int, seed: int):
+    """Builder-defined SwiGLU init (no reference): per expert gate, up, down
+    U(+-1/sqrt(H)) from rng([seed, 4]); w1 = [gate | up]."""
+    rng = np.random.default_rng([seed, 4])
+    bound = 1.0 / np.sqrt(hidden)
+    w1, w2 = [], []
+    for _ in range(num_experts):
+        g = rng.uniform(-bound, bound, size=(hidden, ffn))
+        u = rng.uniform(-bound, bound, size=(hidden, ffn))
+        w1.append(np.concatenate([g, u], axis=1))
+        w2.append(rng.uniform(-bound, bound, size=(ffn, hidden)))
+    return w1, w2
+
+
+def init_gating_matrix(hidden: int, num_experts: int, seed: int) -> np.ndarray:
+    """experts.py:78-81."""
+    bound = 1.0 / np.sqrt(hidden)
+    return np.random.default_rng([seed, 0]).uniform(-bound, bound, size=(hidden, num_experts))
+
+
+def init_expert_weights(num_experts: int, hidden: int, ffn: int, etp_size: int, seed: int,
+                        ep_size: int = 1, activation: str = ACT_RELU
+                        ) -> Dict[Tuple[int, int], ExpertWeights]:
+    """Shard seeded expert matrices over the (ep, etp) grid -- experts.py:84-127."""
+    if ffn % etp_size:
+        raise ValidationError(f"ffn={ffn} is not divisible by etp_size={etp_size}",
+                              constraint="etp|ffn")
+    if num_experts % ep_size:
+        raise ValidationError(f"num_experts={num_experts} is not divisible by ep_size={ep_size}",
+                              constraint="ep|num_experts")
+    if activation not in ACTIVATIONS:
+        raise ValidationError(f"unknown activation {activation!r}", constraint="activation")
+    if activation == ACT_SWIGLU:
+        w1f, w2f = full_swiglu_matrices(num_experts, hidden, ffn, seed)
+    else:
+        w1f, w2f = full_expert_matrices(num_experts, hidden, ffn, seed)
+    local = num_experts // ep_size
+    shard = ffn // etp_size
+    out = {}
+    for ep_rank in range(ep_size):
+        ids = tuple(range(ep_rank * local, (ep_rank + 1) * local))
+        for etp_rank in range(etp_size):
+            cols = slice(etp_rank * shard, (etp_rank + 1) * shard)
+            if activation == ACT_SWIGLU:
+                w1 = [np.concatenate([w1f[e][:, :ffn][:, cols], w1f[e][:, ffn:][:, cols]], axis=1)
+                      for e in ids]
+            else:
+                w1 = [w1f[e][:, cols].copy() for e in ids]
+            out[(ep_rank, etp_rank)] = ExpertWeights(
+                expert_ids=ids, w1=w1, w2=[w2f[e][cols, :].copy() for e in ids],
+                activation=activation, etp_rank=etp_rank, etp_size=etp_size)
+    return out
+
+
+# --------------------------------------------------------------- grouped FFN
+def _gemm(A, B, C, **kw):
+    """Grouped GEMM dispatch: tcgen05 for bf16 when available, SIMT otherwise."""
+    from . import gemm_tc
+
+    if A.dtype == torch.bfloat16 and gemm_tc.available() and gemm_tc.supports(**kw):
+        return gemm_tc.gemm(A, B, C, **kw)
+    return K.gemm_simt(A, B, C, **kw)
+
+
+def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor],
+                pk: PackedExperts, max_rows: int):
+    """pre = xp W1_g ; h = act(pre) ; y = h W2_g  for every group g
+    (experts.py:130-143 batched over groups).  Returns (pre, h, y)."""
+    from . import gemm_tc
+
+    R = xp.shape[0]
+    H, F, N1 = pk.hidden, pk.ffn, pk.n1
+    act = L.ACT_CODES[pk.act]
+    dt = xp.dtype
+    h = torch.empty((R, F), dtype=dt, device=xp.device)
+    pre = torch.empty((R, N1), dtype=dt, device=xp.device)
+    if dt == torch.bfloat16 and gemm_tc.available() and gemm_tc.fused_act_ok(pk):
+        gemm_tc.ffn1_fused(xp, pk, pre, h, goff, G, gexp, max_rows)
+    else:
+        _gemm(xp, pk.w1p, pre, grouped_dim=0, G=G, M=0, N=N1, K=H, a_sm=H, a_sk=1,
+              b_sg=N1 * H, b_sk=1, b_sn=H, c_sg=0, ldc=N1, group_off=goff, group_expert=gexp,
+              max_rows=max_rows)
+        K.act_fwd(pre, act, goff, G, F, out=h)
+    y = torch.empty((R, H), dtype=dt, device=xp.device)
+    _gemm(h, pk.w2p, y, grouped_dim=0, G=G, M=0, N=H, K=F, a_sm=F, a_sk=1, b_sg=H * F, b_sk=1,
+          b_sn=F, c_sg=0, ldc=H, group_off=goff, group_expert=gexp, max_rows=max_rows)
+    return pre, h, y
+
+
+def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torch.Tensor,
+                 goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor], pk: PackedExperts,
+                 max_rows: int, want_dx: bool = True):
+    """experts.py:146-172 batched over groups: returns (dxp, dw1p, dw2p) with
+    dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert)."""
+    from . import gemm_tc
+
+    R = dyp.shape[0]
+    H, F, N1 = pk.hidden, pk.ffn, pk.n1
+    act = L.ACT_CODES[pk.act]
+    dt = dyp.dtype
+    dev = dyp.device
+    dpre = torch.empty((R, N1), dtype=dt, device=dev)
+    if dt == torch.bfloat16 and gemm_tc.available() and gemm_tc.fused_act_ok(pk):
+        gemm_tc.dgrad2_fused(dyp, pk, pre, dpre, goff, G, gexp, max_rows)
+    else:
+        dh = torch.empty((R, F), dtype=dt, device=dev)
+        _gemm(dyp, pk.w2p, dh, grouped_dim=0, G=G, M=0, N=F, K=H, a_sm=H, a_sk=1, b_sg=H * F,
+              b_sk=F, b_sn=1, c_sg=0, ldc=F, group_off=goff, group_expert=gexp, max_rows=max_rows)
+        K.act_bwd(dh, pre, act, goff, G, F, out=dpre)
+    dxp = None
+    if want_dx:
+        dxp = torch.empty((R, H), dtype=dt, device=dev)
+        _gemm(dpre, pk.w1p, dxp, grouped_dim=0, G=G, M=0, N=H, K=N1, a_sm=N1, a_sk=1,
+              b_sg=N1 * H, b_sk=H, b_sn=1, c_sg=0, ldc=H, group_off=goff, group_expert=gexp,
+              max_rows=max_rows)
+    dw2p = torch.empty((G, H, F), dtype=torch.float32, device=dev)
+    _gemm(dyp, h, dw2p, grouped_dim=1, G=G, M=H, N=F, K=0, a_sm=1, a_sk=H, b_sg=0, b_sk=F,
+          b_sn=1, c_sg=H * F, ldc=F, group_off=goff, max_rows=max_rows)
+    dw1p = torch.empty((G, N1, H), dtype=torch.float32, device=dev)
+    _gemm(dpre, xp, dw1p, grouped_dim=1, G=G, M=N1, N=H, K=0, a_sm=1, a_sk=N1, b_sg=0, b_sk=H,
+          b_sn=1, c_sg=N1 * H, ldc=H, group_off=goff, max_rows=max_rows)
+    return dxp, dw1p, dw2p
+
+
+def _single_group(n: int, device) -> torch.Tensor:
+    return torch.tensor([0, n], dtype=torch.int32, device=device)
+
+
+def expert_forward_shard(tokens, weights: ExpertWeights, expert_id: int, dtype=None):
+    """Partial FFN output of one expert shard -- experts.py:130-143.
+
+    ``tokens`` is a CUDA tensor (fp32 or bf16; numpy is moved to CUDA fp32).
+    Returns (out, cache) with cache = (tokens, pre) like the reference (``pre``
+    is in the packed column order for SwiGLU)."""
+    i = weights.local_index(expert_id)
+    x = tokens if isinstance(tokens, torch.Tensor) else torch.as_tensor(np.asarray(tokens, np.float64), dtype=torch.float32)
+    if not x.is_cuda:
+        x = x.cuda()
+    dt = dtype or x.dtype
+    x = x.to(dt).contiguous()
+    pk = weights.packed(dt, x.device)
+    sub = PackedExperts(pk.w1p[i:i + 1], pk.w2p[i:i + 1], pk.act, pk.hidden, pk.ffn)
+    goff = _single_group(x.shape[0], x.device)
+    pre, h, y = ffn_forward(x, goff, 1, None, sub, x.shape[0])
+    return y, (x, pre)
+
+
+def expert_backward_shard(upstream, cache, weights: ExpertWeights, expert_id: int):
+    """Gradients through one expert shard -- experts.py:146-172.
+
+    Returns (partial token grad, w1 shard grad, w2 shard grad) with weight
+    grads in the reference layout ([H, N1] and [F, H], fp32)."""
+    i = weights.local_index(expert_id)
+    x, pre = cache
+    u = upstream if isinstance(upstream, torch.Tensor) else torch.as_tensor(np.asarray(upstream, np.float64))
+    u = u.to(device=x.device, dtype=x.dtype).contiguous()
+    pk = weights.packed(x.dtype, x.device)
+    if tuple(u.shape) != (x.shape[0], pk.hidden):
+        raise ValidationError(
+            f"upstream shape {tuple(u.shape)} does not match forward output ({x.shape[0]}, {pk.hidden})",
+            constraint="upstream-shape")
+    sub = PackedExperts(pk.w1p[i:i + 1], pk.w2p[i:i + 1], pk.act, pk.hidden, pk.ffn)
+    goff = _single_group(x.shape[0], x.device)
+    h = K.act_fwd(pre, L.ACT_CODES[pk.act], goff, 1, pk.ffn)
+    dxp, dw1p, dw2p = ffn_backward(u, x, pre, h, goff, 1, None, sub, x.shape[0])
+    return dxp, unpack_w1_grad(dw1p, pk.act)[0], unpack_w2_grad(dw2p)[0]

@@ -1,0 +1,191 @@
+"""Torch-tensor wrappers over the C ABI (one function per entry point).
+
+Every wrapper launches on the current CUDA stream, allocates outputs with the
+torch caching allocator, and never synchronises.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Tuple
+
+import torch
+
+from . import _lib as L
+from .errors import ValidationError
+
+GEMM_ALIGN = 128  # rows per expert segment in the padded (GEMM) layout
+
+
+def _cuda(t: torch.Tensor, name: str, dtype=None) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValidationError(f"{name} must be a CUDA tensor", constraint=f"{name}-cuda")
+    if dtype is not None and t.dtype != dtype:
+        raise ValidationError(f"{name} must be {dtype}, got {t.dtype}", constraint=f"{name}-dtype")
+    if not t.is_contiguous():
+        raise ValidationError(f"{name} must be contiguous", constraint=f"{name}-contiguous")
+    return t
+
+
+def _sp():
+    return L.stream_ptr()
+
+
+def router_logits(x: torch.Tensor, w_g: torch.Tensor) -> torch.Tensor:
+    T, H = x.shape
+    E = w_g.shape[1]
+    _cuda(x, "x")
+    _cuda(w_g, "w_g", torch.float32)
+    out = torch.empty((T, E), dtype=torch.float32, device=x.device)
+    L.call("b200moe_router_logits", L.ptr(x), L.dtype_code(x.dtype), L.ptr(w_g), T, H, E,
+           L.ptr(out), _sp())
+    return out
+
+
+def router_topk(logits: torch.Tensor, k: int, gate_fn: int, renorm: bool, want_f64: bool = False):
+    T, E = logits.shape
+    _cuda(logits, "logits", torch.float32)
+    dev = logits.device
+    scores = torch.empty((T, E), dtype=torch.float32, device=dev)
+    idx = torch.empty((T, k), dtype=torch.int32, device=dev)
+    gates = torch.empty((T, k), dtype=torch.float32, device=dev)
+    g64 = torch.empty((T, k), dtype=torch.float64, device=dev) if want_f64 else None
+    L.call("b200moe_router_topk", L.ptr(logits), T, E, k, gate_fn, int(renorm), L.ptr(scores),
+           L.ptr(idx), L.ptr(gates), L.ptr(g64), _sp())
+    return scores, idx, gates, g64
+
+
+class PlanTensors:
+    """Device outputs of one b200moe_dispatch_plan call."""
+
+    __slots__ = ("kept", "counts", "offsets", "poffsets", "send_row", "gemm_row", "perm",
+                 "perm_gates", "T", "k", "E", "align")
+
+    def __init__(self, **kw):
+        for k_, v in kw.items():
+            setattr(self, k_, v)
+
+
+def dispatch_plan(topk_idx: torch.Tensor, gates: torch.Tensor, E: int, cap: int = 0,
+                  kept_in: Optional[torch.Tensor] = None, order: Optional[torch.Tensor] = None,
+                  align: int = GEMM_ALIGN, want_perm_gates: bool = True) -> PlanTensors:
+    T, k = topk_idx.shape
+    dev = topk_idx.device
+    _cuda(topk_idx, "topk_idx", torch.int32)
+    lib = L.load()
+    ws_bytes = int(lib.b200moe_dispatch_plan_ws(T, E))
+    ws = torch.empty((max(ws_bytes, 4),), dtype=torch.uint8, device=dev)
+    kept = torch.empty((T, k), dtype=torch.uint8, device=dev)
+    counts = torch.empty((E,), dtype=torch.int32, device=dev)
+    offsets = torch.empty((E + 1,), dtype=torch.int32, device=dev)
+    poffsets = torch.empty((E + 1,), dtype=torch.int32, device=dev)
+    send_row = torch.empty((T, k), dtype=torch.int32, device=dev)
+    gemm_row = torch.empty((T, k), dtype=torch.int32, device=dev)
+    perm = torch.empty((max(T * k, 1),), dtype=torch.int64, device=dev)
+    pg = torch.empty((max(T * k, 1),), dtype=torch.float32, device=dev) if want_perm_gates else None
+    L.call("b200moe_dispatch_plan", L.ptr(topk_idx), L.ptr(gates), L.ptr(kept_in), L.ptr(order),
+           T, k, E, int(cap), align, L.ptr(ws), ctypes.c_size_t(ws.numel()), L.ptr(kept),
+           L.ptr(counts), L.ptr(offsets), L.ptr(poffsets), L.ptr(send_row), L.ptr(gemm_row),
+           L.ptr(perm), L.ptr(pg), _sp())
+    return PlanTensors(kept=kept, counts=counts, offsets=offsets, poffsets=poffsets,
+                       send_row=send_row, gemm_row=gemm_row, perm=perm, perm_gates=pg, T=T, k=k,
+                       E=E, align=align)
+
+
+def capacity_by_gate(plan0: PlanTensors, gates64: torch.Tensor, positions: Optional[torch.Tensor],
+                     cap: int) -> torch.Tensor:
+    T, k, E = plan0.T, plan0.k, plan0.E
+    kept = torch.zeros((T, k), dtype=torch.uint8, device=gates64.device)
+    L.call("b200moe_capacity_by_gate", L.ptr(plan0.perm), L.ptr(plan0.offsets), L.ptr(gates64),
+           L.ptr(positions), T, k, E, int(cap), L.ptr(kept), _sp())
+    return kept
+
+
+def permute(x: torch.Tensor, pair_row: torch.Tensor, out_rows: int, scale=None,
+            poffsets=None, counts=None, E: int = 0, align: int = GEMM_ALIGN,
+            out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    T, H = x.shape
+    k = pair_row.shape[1]
+    _cuda(x, "x")
+    if out is None:
+        out = torch.empty((max(out_rows, 1), H), dtype=x.dtype, device=x.device)
+    L.call("b200moe_permute", L.ptr(x), L.dtype_code(x.dtype), T, H, k, L.ptr(pair_row),
+           L.ptr(scale), L.ptr(out), L.ptr(poffsets), L.ptr(counts), E, align, _sp())
+    return out
+
+
+def permute_bwd(u: torch.Tensor, pair_row: torch.Tensor, gates: torch.Tensor,
+                y_rows: torch.Tensor, poffsets=None, counts=None, E: int = 0,
+                align: int = GEMM_ALIGN) -> Tuple[torch.Tensor, torch.Tensor]:
+    T, H = u.shape
+    k = pair_row.shape[1]
+    _cuda(u, "upstream")
+    if u.dtype != y_rows.dtype:
+        raise ValidationError("upstream and expert rows must share a dtype", constraint="dtype")
+    dy = torch.empty_like(y_rows)
+    dg = torch.empty((T, k), dtype=torch.float32, device=u.device)
+    L.call("b200moe_permute_bwd", L.ptr(u), L.dtype_code(u.dtype), T, H, k, L.ptr(pair_row),
+           L.ptr(gates), L.ptr(y_rows), L.ptr(dy), L.ptr(dg), L.ptr(poffsets), L.ptr(counts), E,
+           align, _sp())
+    return dy, dg
+
+
+def combine(rows: torch.Tensor, pair_row: torch.Tensor, T: int, gates=None, dz=None, w_gT=None,
+            out: Optional[torch.Tensor] = None, out_dtype=None, accumulate: bool = False):
+    H = rows.shape[1]
+    k = pair_row.shape[1]
+    if out is None:
+        out = torch.empty((T, H), dtype=out_dtype or rows.dtype, device=rows.device)
+    E = 0 if dz is None else dz.shape[1]
+    L.call("b200moe_combine", L.ptr(rows), L.dtype_code(rows.dtype), T, H, k, L.ptr(pair_row),
+           L.ptr(gates), L.ptr(dz), L.ptr(w_gT), E, L.ptr(out), L.dtype_code(out.dtype),
+           int(accumulate), _sp())
+    return out
+
+
+def router_bwd(dgates, scores, topk_idx, gates, gate_fn: int, renorm: bool) -> torch.Tensor:
+    T, E = scores.shape
+    k = topk_idx.shape[1]
+    dz = torch.empty((T, E), dtype=torch.float32, device=scores.device)
+    L.call("b200moe_router_bwd", L.ptr(dgates), L.ptr(scores), L.ptr(topk_idx), L.ptr(gates), T,
+           E, k, gate_fn, int(renorm), L.ptr(dz), _sp())
+    return dz
+
+
+def router_wgrad(x: torch.Tensor, dz: torch.Tensor) -> torch.Tensor:
+    T, H = x.shape
+    E = dz.shape[1]
+    dwg = torch.empty((H, E), dtype=torch.float32, device=x.device)
+    L.call("b200moe_router_wgrad", L.ptr(x), L.dtype_code(x.dtype), L.ptr(dz), T, H, E,
+           L.ptr(dwg), _sp())
+    return dwg
+
+
+def gemm_simt(A, B, C, *, grouped_dim: int, G: int, M: int, N: int, K: int, a_sm, a_sk, b_sg,
+              b_sk, b_sn, c_sg, ldc, group_off, group_expert=None, max_rows: int = 0,
+              accumulate: bool = False):
+    args = L.GemmArgs(
+        dtype_in=L.dtype_code(A.dtype), dtype_out=L.dtype_code(C.dtype), grouped_dim=grouped_dim,
+        accumulate=int(accumulate), G=G, M=M, N=N, K=K,
+        A=L.ptr(A), a_sm=a_sm, a_sk=a_sk, B=L.ptr(B), b_sg=b_sg, b_sk=b_sk, b_sn=b_sn,
+        C=L.ptr(C), c_sg=c_sg, ldc=ldc, group_off=L.ptr(group_off),
+        group_expert=L.ptr(group_expert), max_rows=max_rows)
+    L.call("b200moe_gemm_simt", ctypes.byref(args), _sp())
+    return C
+
+
+def act_fwd(pre, act: int, group_off, G: int, F: int, out=None):
+    rows = pre.shape[0]
+    if out is None:
+        out = torch.empty((rows, F), dtype=pre.dtype, device=pre.device)
+    L.call("b200moe_act_fwd", L.ptr(pre), L.dtype_code(pre.dtype), act, L.ptr(group_off), G, rows,
+           F, L.ptr(out), _sp())
+    return out
+
+
+def act_bwd(dh, pre, act: int, group_off, G: int, F: int, out=None):
+    rows = pre.shape[0]
+    if out is None:
+        out = torch.empty_like(pre)
+    L.call("b200moe_act_bwd", L.ptr(dh), L.ptr(pre), L.dtype_code(pre.dtype), act,
+           L.ptr(group_off), G, rows, F, L.ptr(out), _sp())
+    return out

@@ -1,0 +1,300 @@
+"""Top-k gating and capacity-factor token dropping on the GPU.
+
+Mirrors /root/reference/pkg/src/moefold/router.py: GatingParams :30-74,
+RoutingDecision :77-109, compute_gates :127-162, capacity_limit :165-168,
+apply_capacity :171-206, gather_full_sequence_decision :209-269, load_stats
+:279-301, merge_decisions :304-320.  Arrays are CUDA tensors; the
+arithmetic runs in the K1 kernels of libb200moe (router.cu).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import kernels as K
+from .errors import NumericError, ProtocolError, ValidationError
+
+GATE_SOFTMAX = "softmax"
+GATE_SIGMOID = "sigmoid"
+DROP_SUBSEQUENCE = "subsequence"
+DROP_FULLSEQUENCE = "fullsequence"
+PRIORITY_POSITION = "position"
+PRIORITY_PROBABILITY = "probability"
+
+GATE_CODES = {GATE_SOFTMAX: L.GATE_SOFTMAX, GATE_SIGMOID: L.GATE_SIGMOID}
+
+
+def _device_default():
+    return torch.device("cuda")
+
+
+@dataclass
+class GatingParams:
+    """Router weights plus routing policy (router.py:30-74).  ``w_g`` is
+    stored as a CUDA float32 tensor [hidden, experts]."""
+
+    w_g: object
+    k: int
+    gate_fn: str = GATE_SOFTMAX
+    renormalize_topk: bool = False
+    capacity_factor: Optional[float] = None
+    drop_mode: str = DROP_SUBSEQUENCE
+    drop_priority: str = PRIORITY_POSITION
+
+    def __post_init__(self):
+        w = self.w_g
+        if not isinstance(w, torch.Tensor):
+            w = torch.as_tensor(np.asarray(w, dtype=np.float64))
+        if w.dim() != 2:
+            raise ValidationError("w_g must be 2-D [hidden, experts]", constraint="w_g-2d")
+        self.w_g = w
+        if not (1 <= self.k <= self.num_experts):
+            raise ValidationError(
+                f"k must satisfy 1 <= k <= num_experts ({self.num_experts}), got {self.k}",
+                constraint="1<=k<=E")
+        if self.gate_fn not in GATE_CODES:
+            raise ValidationError(f"unknown gate_fn {self.gate_fn!r}", constraint="gate_fn")
+        if self.drop_mode not in (DROP_SUBSEQUENCE, DROP_FULLSEQUENCE):
+            raise ValidationError(f"unknown drop_mode {self.drop_mode!r}", constraint="drop_mode")
+        if self.drop_priority not in (PRIORITY_POSITION, PRIORITY_PROBABILITY):
+            raise ValidationError(f"unknown drop_priority {self.drop_priority!r}",
+                                  constraint="drop_priority")
+        if self.capacity_factor is not None and self.capacity_factor < 1.0:
+            raise ValidationError(f"capacity_factor must be >= 1, got {self.capacity_factor}",
+                                  constraint="capacity_factor>=1")
+        self._dev_cache = {}
+
+    @property
+    def num_experts(self) -> int:
+        return self.w_g.shape[1]
+
+    @property
+    def hidden(self) -> int:
+        return self.w_g.shape[0]
+
+    @property
+    def dropless(self) -> bool:
+        return self.capacity_factor is None
+
+    def device_w_g(self, device=None) -> torch.Tensor:
+        """[H, E] fp32 on the device (cached)."""
+        device = torch.device(device or _device_default())
+        key = ("wg", str(device))
+        if key not in self._dev_cache:
+            self._dev_cache[key] = self.w_g.to(device=device, dtype=torch.float32).contiguous()
+        return self._dev_cache[key]
+
+    def device_w_gT(self, device=None) -> torch.Tensor:
+        """[E, H] fp32 on the device (cached) for the backward router term."""
+        device = torch.device(device or _device_default())
+        key = ("wgT", str(device))
+        if key not in self._dev_cache:
+            self._dev_cache[key] = self.device_w_g(device).T.contiguous()
+        return self._dev_cache[key]
+
+
+@dataclass
+class RoutingDecision:
+    """Per-token expert assignments (router.py:77-109): ``experts`` int32
+    [n,k] best first, ``gates`` fp32 [n,k], ``kept`` bool [n,k], ``positions``
+    int64 [n] (host or device), ``scores`` fp32 [n,E] when available."""
+
+    experts: torch.Tensor
+    gates: torch.Tensor
+    kept: torch.Tensor
+    positions: torch.Tensor
+    scores: Optional[torch.Tensor] = None
+    gates_f64: Optional[torch.Tensor] = None
+
+    @property
+    def n_tokens(self) -> int:
+        return self.experts.shape[0]
+
+    @property
+    def k(self) -> int:
+        return self.experts.shape[1]
+
+    def copy(self) -> "RoutingDecision":
+        c = lambda t: None if t is None else t.clone()  # noqa: E731
+        return RoutingDecision(c(self.experts), c(self.gates), c(self.kept), c(self.positions),
+                               c(self.scores), c(self.gates_f64))
+
+
+def check_finite(x: torch.Tensor, what: str) -> None:
+    """router.py:141-144 (one device reduction + host read)."""
+    if not bool(torch.isfinite(x).all()):
+        raise NumericError(f"{what} contains non-finite values")
+
+
+def routing_from_logits(logits: torch.Tensor, params: GatingParams, positions=None,
+                        want_f64: bool = False) -> RoutingDecision:
+    """Scores, top-k and gates from fp32 logits (router.py:146-162)."""
+    n = logits.shape[0]
+    scores, idx, gates, g64 = K.router_topk(
+        logits.contiguous(), params.k, GATE_CODES[params.gate_fn], params.renormalize_topk,
+        want_f64=want_f64 or params.drop_priority == PRIORITY_PROBABILITY)
+    if positions is None:
+        positions = torch.arange(n, dtype=torch.int64)
+    else:
+        positions = torch.as_tensor(positions, dtype=torch.int64)
+        if tuple(positions.shape) != (n,):
+            raise ValidationError("positions must have one entry per token", constraint="positions")
+    kept = torch.ones((n, params.k), dtype=torch.bool, device=logits.device)
+    return RoutingDecision(idx, gates, kept, positions, scores, g64)
+
+
+def compute_gates(x, params: GatingParams, positions=None, *, check: bool = True) -> RoutingDecision:
+    """Score a token block and select each token's top-k experts (router.py:127-162)."""
+    if not isinstance(x, torch.Tensor):
+        x = torch.as_tensor(np.asarray(x, dtype=np.float64), dtype=torch.float32)
+    if not x.is_cuda:
+        x = x.to(_device_default())
+    if x.dtype not in (torch.float32, torch.bfloat16):
+        x = x.float()
+    x = x.contiguous()
+    if x.dim() != 2 or x.shape[1] != params.hidden:
+        raise ValidationError(f"token block shape {tuple(x.shape)} incompatible with w_g "
+                              f"{tuple(params.w_g.shape)}", constraint="x-shape")
+    if check:
+        check_finite(x, "token block")
+        check_finite(params.device_w_g(x.device), "gating weights")
+    logits = K.router_logits(x, params.device_w_g(x.device))
+    return routing_from_logits(logits, params, positions)
+
+
+def capacity_limit(capacity_factor: float, l_scope: int, num_experts: int) -> int:
+    """floor(CF * L / E), at least one (router.py:165-168; no k factor)."""
+    return max(1, math.floor(capacity_factor * l_scope / num_experts))
+
+
+def _monotone(positions: torch.Tensor) -> bool:
+    p = positions.cpu() if positions.is_cuda else positions
+    return p.numel() < 2 or bool((p[1:] > p[:-1]).all())
+
+
+def kept_mask(decision: RoutingDecision, l_scope: int, num_experts: int,
+              params: GatingParams) -> torch.Tensor:
+    """Capacity drop flags as a uint8 [n,k] device tensor (router.py:171-206)."""
+    dev = decision.experts.device
+    n, k = decision.experts.shape
+    kept_in = decision.kept.to(torch.uint8).contiguous()
+    if params.dropless:
+        return kept_in
+    cap = capacity_limit(params.capacity_factor, l_scope, num_experts)
+    idx = decision.experts.contiguous()
+    if params.drop_priority == PRIORITY_POSITION:
+        order = None
+        if not _monotone(decision.positions):
+            order = torch.argsort(decision.positions.cpu(), stable=True).to(torch.int32).to(dev)
+        plan = K.dispatch_plan(idx, decision.gates, num_experts, cap=cap, kept_in=kept_in,
+                               order=order, want_perm_gates=False)
+        return plan.kept
+    g64 = decision.gates_f64 if decision.gates_f64 is not None else decision.gates.double()
+    plan0 = K.dispatch_plan(idx, decision.gates, num_experts, cap=0, kept_in=kept_in,
+                            want_perm_gates=False)
+    pos = decision.positions.to(dev, torch.int64)
+    kept = K.capacity_by_gate(plan0, g64.contiguous(), pos, cap)
+    return kept & kept_in
+
+
+def apply_capacity(decision: RoutingDecision, l_scope: int, num_experts: int,
+                   params: GatingParams) -> RoutingDecision:
+    """Drop pairs exceeding per-expert capacity within one scope (router.py:171-206)."""
+    if params.dropless:
+        return decision
+    if params.capacity_factor < 1.0:
+        raise ValidationError("capacity_factor must be >= 1", constraint="capacity_factor>=1")
+    out = decision.copy()
+    out.kept = kept_mask(decision, l_scope, num_experts, params).bool()
+    return out
+
+
+def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: int,
+                                  num_experts: int, params: GatingParams
+                                  ) -> Tuple[RoutingDecision, RoutingDecision]:
+    """Capacity per full sequence across the ranks sharding it (router.py:209-269).
+
+    The (position, slot, expert, gate) pairs of the group are all-gathered on
+    the device, capacity is applied per sequence with the K1 kernels, and the
+    flags of this rank's pairs are mapped back."""
+    from .collectives import VarBuffer
+
+    n, k = local.experts.shape
+    dev = local.experts.device
+    pos = local.positions.to(dev, torch.int64)
+    rows = torch.stack([
+        pos.repeat_interleave(k).double(),
+        torch.arange(k, device=dev).repeat(n).double(),
+        local.experts.reshape(-1).double(),
+        (local.gates_f64 if local.gates_f64 is not None else local.gates.double()).reshape(-1),
+    ], dim=1)
+    buf, _ = ctx.all_gather_v(tuple(group), VarBuffer.from_rows(rows))
+    g = buf.rows()
+    if g.shape[0] % k:
+        raise ProtocolError(f"full-sequence gather: {g.shape[0]} pairs is not a multiple of k={k}; "
+                            "shard lengths are inconsistent")
+    gpos = g[::k, 0].to(torch.int64)
+    order = torch.argsort(gpos, stable=True)
+    gpos = gpos[order]
+    if torch.unique(gpos).numel() != gpos.numel():
+        raise ProtocolError("full-sequence gather: duplicate token positions across shards")
+    gk = g.reshape(-1, k, 4)[order]
+    experts = gk[:, :, 2].to(torch.int32).contiguous()
+    g64 = gk[:, :, 3].contiguous()
+    global_dec = RoutingDecision(experts, g64.float(), torch.ones_like(experts, dtype=torch.bool),
+                                 gpos, None, g64)
+    kept = torch.ones_like(experts, dtype=torch.bool)
+    seq_ids = gpos // seq_len
+    for sid in torch.unique(seq_ids).tolist():
+        m = (seq_ids == sid).nonzero().reshape(-1)
+        sub = RoutingDecision(experts[m].contiguous(), global_dec.gates[m].contiguous(),
+                              kept[m].contiguous(), gpos[m], None, g64[m].contiguous())
+        kept[m] = kept_mask(sub, seq_len, num_experts, params).bool()
+    global_dec.kept = kept
+    # map back: local position -> row in the gathered (sorted) table
+    where = torch.searchsorted(gpos, pos)
+    out = local.copy()
+    out.kept = kept[where]
+    return global_dec, out
+
+
+@dataclass(frozen=True)
+class LoadStats:
+    counts: np.ndarray
+    imbalance: float
+    aux_loss: float
+
+
+def load_stats(decision: RoutingDecision, num_experts: int) -> LoadStats:
+    """Kept pairs per expert, imbalance, Switch aux loss (router.py:279-301)."""
+    e = decision.experts.reshape(-1).long()
+    kept = decision.kept.reshape(-1).bool()
+    counts = torch.bincount(e[kept], minlength=num_experts).cpu().numpy().astype(np.int64)
+    mean = counts.sum() / num_experts
+    imbalance = float(counts.max() / mean) if mean > 0 else float("nan")
+    if decision.scores is None or decision.n_tokens == 0:
+        aux = float("nan")
+    else:
+        f = torch.bincount(decision.experts[:, 0].long(), minlength=num_experts).double() / decision.n_tokens
+        s = decision.scores.double()
+        p = (s / s.sum(dim=1, keepdim=True)).mean(dim=0)
+        aux = float(num_experts * torch.dot(f, p))
+    return LoadStats(counts=counts, imbalance=imbalance, aux_loss=aux)
+
+
+def merge_decisions(decisions) -> RoutingDecision:
+    """Concatenate per-rank decisions ordered by global position (router.py:304-320)."""
+    dev = decisions[0].experts.device
+    cat = lambda name: torch.cat([getattr(d, name).to(dev) for d in decisions])  # noqa: E731
+    positions = cat("positions")
+    order = torch.argsort(positions, stable=True)
+    scores = None
+    if all(d.scores is not None for d in decisions):
+        scores = cat("scores")[order]
+    return RoutingDecision(cat("experts")[order], cat("gates")[order], cat("kept")[order],
+                           positions[order], scores)

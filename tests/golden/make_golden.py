@@ -195,7 +195,34 @@ def layer_cases():
     return out
 
 
+def topology_cases():
+    from moefold.topology import LAYOUT_LISTING1, generate_parallel_groups, sequence_group
+    import json
+
+    out = []
+    for w, tp, cp, pp, ep, etp, layout in [
+        (8, 2, 2, 1, 8, 1, "pp-outermost"), (8, 2, 2, 1, 4, 2, "pp-outermost"),
+        (16, 2, 4, 1, 8, 1, "pp-outermost"), (64, 2, 2, 2, 2, 2, "listing1"),
+        (8, 2, 2, 2, 2, 1, "listing1"), (12, 3, 2, 2, 3, 2, "pp-outermost"),
+    ]:
+        topo = ParallelTopology(world_size=w, tp=tp, cp=cp, pp=pp, ep=ep, etp=etp, layout=layout)
+        g = generate_parallel_groups(topo)
+        out.append(dict(args=[w, tp, cp, pp, ep, etp, layout],
+                        attention={k: [list(x) for x in v] for k, v in g.attention.items()},
+                        moe={k: [list(x) for x in v] for k, v in g.moe.items()},
+                        seq=[list(sequence_group(topo, r)) for r in range(w)],
+                        attn_coords=[list(topo.attn_coords(r)) for r in range(w)],
+                        moe_coords=[list(topo.moe_coords(r)) for r in range(w)]))
+    for tp, cp, dp in [(2, 2, 2), (1, 2, 4), (2, 1, 1)]:
+        topo = ParallelTopology(world_size=tp * cp * dp, tp=tp, cp=cp, ep=1)
+        out.append(dict(partition=[tp, cp, dp],
+                        parts=[p.tolist() for p in md.token_partition(topo, 16, 2 * dp)]))
+    with open(os.path.join(OUT, "topology.json"), "w") as f:
+        json.dump(out, f)
+
+
 def main():
+    topology_cases()
     np.savez_compressed(os.path.join(OUT, "router.npz"), **router_cases())
     np.savez_compressed(os.path.join(OUT, "capacity_plan.npz"), **capacity_cases())
     np.savez_compressed(os.path.join(OUT, "experts.npz"), **expert_cases())

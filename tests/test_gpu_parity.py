@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the pinned CPU oracle.
+
+Routing indices, kept masks, permutations and counts are compared bit-for-bit
+given identical logits; floats within rel-err 1e-5 (fp32 mode) and 2e-2
+(bf16) -- the tolerances of BASELINE.json's north star."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import moe_oracle as O  # noqa: E402
+
+import paper_2504_14960_b200 as B  # noqa: E402
+from paper_2504_14960_b200 import kernels as K  # noqa: E402
+
+FP32_TOL = 1e-5
+BF16_TOL = 2e-2
+
+
+def _cases(d, prefix):
+    return sorted({k.split("_")[0] for k in d if k.startswith(prefix)}, key=lambda s: int(s[1:]))
+
+
+def t(a, dtype=torch.float32):
+    return torch.as_tensor(np.asarray(a)).to("cuda", dtype).contiguous()
+
+
+def test_library_loads_on_b200():
+    from paper_2504_14960_b200 import _lib
+
+    _lib.load()  # raises unless sm_100
+
+
+def test_router_topk_matches_reference(golden):
+    d = golden("router")
+    for c in _cases(d, "r"):
+        E, k, sig, renorm = (int(v) for v in d[c + "_meta"])
+        scores, idx, gates, g64 = K.router_topk(t(d[c + "_logits"]), k, int(sig), bool(renorm), True)
+        np.testing.assert_array_equal(idx.cpu().numpy(), d[c + "_experts"], err_msg=c)
+        assert O.rel_err(g64.cpu().numpy(), d[c + "_gates"]) < 1e-14, c
+        assert O.rel_err(gates.cpu().numpy(), d[c + "_gates"]) < 1e-6, c
+        assert O.rel_err(scores.cpu().numpy(), d[c + "_scores"]) < 1e-6, c
+
+
+def test_capacity_and_plan_match_reference(golden):
+    d = golden("capacity_plan")
+    for c in _cases(d, "c"):
+        E, k, n, prob = (int(v) for v in d[c + "_meta"])
+        cf = float(d[c + "_cf"][0])
+        params = B.GatingParams(w_g=np.eye(E), k=k, capacity_factor=cf,
+                                drop_priority="probability" if prob else "position")
+        dec = B.router.routing_from_logits(t(d[c + "_logits"]), params)
+        np.testing.assert_array_equal(dec.experts.cpu().numpy(), d[c + "_experts"])
+        dropped = B.apply_capacity(dec, n, E, params)
+        np.testing.assert_array_equal(dropped.kept.cpu().numpy(), d[c + "_kept"], err_msg=c)
+        for ep in (1, 2, 4):
+            if c + f"_perm_ep{ep}" not in d:
+                continue
+            plan = B.build_dispatch_plan(dropped, ep, E // ep)
+            np.testing.assert_array_equal(plan.permutation, d[c + f"_perm_ep{ep}"], err_msg=c)
+            np.testing.assert_array_equal(plan.send_counts, d[c + f"_counts_ep{ep}"], err_msg=c)
+            assert O.rel_err(plan.gates, d[c + f"_pgates_ep{ep}"]) < 1e-6
+        plan = B.build_dispatch_plan(dropped, 1, E)
+        got = B.permute(t(d[c + "_x"]), plan).cpu().numpy()
+        np.testing.assert_array_equal(got, d[c + "_permuted"].astype(np.float32))
+        comb = B.unpermute_combine(t(d[c + "_rows"]), plan, 8).cpu().numpy()
+        assert O.rel_err(comb, d[c + "_combined"]) < FP32_TOL, c
+
+
+def test_plan_non_monotone_positions_and_edge_cases():
+    rng = np.random.default_rng(3)
+    E, k, n = 8, 2, 257
+    logits = rng.standard_normal((n, E)).astype(np.float32)
+    logits[:, 1] += 1.0
+    positions = rng.permutation(n) + 1000
+    params = B.GatingParams(w_g=np.eye(E), k=k, capacity_factor=1.0)
+    dec = B.router.routing_from_logits(t(logits), params, positions)
+    got = B.apply_capacity(dec, n, E, params).kept.cpu().numpy()
+    r = O.route_logits(logits, k)
+    want = O.apply_capacity(r.experts, r.gates, r.kept, positions, O.capacity_limit(1.0, n, E), E)
+    np.testing.assert_array_equal(got, want)
+    # empty block, single token, k == E
+    for n_, k_ in ((0, 2), (1, 2), (5, 8)):
+        lg = rng.standard_normal((n_, E)).astype(np.float32)
+        p = B.GatingParams(w_g=np.eye(E), k=k_)
+        dec = B.router.routing_from_logits(t(lg).reshape(n_, E), p)
+        plan = B.build_dispatch_plan(dec, 2, 4)
+        want = O.build_dispatch_plan(O.route_logits(lg.reshape(n_, E), k_).experts,
+                                     np.ones((n_, k_)), np.ones((n_, k_), bool), 2, 4)
+        np.testing.assert_array_equal(plan.permutation, want.permutation)
+        np.testing.assert_array_equal(plan.send_counts, want.send_counts)
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, FP32_TOL), (torch.bfloat16, BF16_TOL)])
+def test_expert_shards_match_reference(golden, dtype, tol):
+    d = golden("experts")
+    for ci, act in enumerate(("relu", "gelu")):
+        p = f"e{ci}_"
+        w = B.ExpertWeights((0,), [d[p + "w1"]], [d[p + "w2"]], act, 0, 1)
+        y, cache = B.expert_forward_shard(t(d[p + "x"], dtype), w, 0)
+        assert O.rel_err(y.float().cpu().numpy(), d[p + "y"]) < tol, act
+        dx, dw1, dw2 = B.expert_backward_shard(t(d[p + "u"], dtype), cache, w, 0)
+        assert O.rel_err(dx.float().cpu().numpy(), d[p + "dx"]) < tol, act
+        assert O.rel_err(dw1.cpu().numpy(), d[p + "dw1"]) < tol, act
+        assert O.rel_err(dw2.cpu().numpy(), d[p + "dw2"]) < tol, act
+
+
+def _gpu_logits_per_rank(ctx):
+    return [sv["logits"].cpu().numpy().astype(np.float64) for sv in ctx.per_rank]
+
+
+def _run_layer_case(d, c, dtype):
+    meta = [int(v) for v in d[c + "_meta"]]
+    w, tp, cp, ep, etp, E, k, H, F, seq, batch, seed, full, sig, renorm, gelu = meta
+    cf = float(d[c + "_cf"][0])
+    topo = B.ParallelTopology(world_size=w, tp=tp, cp=cp, ep=ep, etp=etp)
+    params = B.GatingParams(w_g=d[c + "_wg"], k=k, gate_fn="sigmoid" if sig else "softmax",
+                            renormalize_topk=bool(renorm), capacity_factor=None if cf < 0 else cf,
+                            drop_mode="fullsequence" if full else "subsequence")
+    weights = B.init_expert_weights(E, H, F, etp_size=etp, seed=seed, ep_size=ep,
+                                    activation="gelu" if gelu else "relu")
+    x, u = d[c + "_x"], d[c + "_u"]
+    positions = [d[c + f"_positions{r}"] for r in range(w)]
+    blocks = [B.TokenBlock(t(x[p], dtype), p) for p in positions]
+    world = B.LocalWorld(w)
+    outs, ctx = B.moe_forward(blocks, weights, topo, params, world, seq_len=seq)
+    res = B.moe_backward([t(u[p], dtype) for p in positions], ctx)
+    return meta, params, positions, outs, ctx, res
+
+
+def test_layer_cases_match_reference_fp32(golden):
+    """moe_forward/moe_backward (fp32 mode) on every golden topology, ranks
+    simulated on one GPU, vs the reference's own outputs and gradients."""
+    d = golden("layer")
+    tol = FP32_TOL
+    for c in _cases(d, "l"):
+        meta, params, positions, outs, ctx, res = _run_layer_case(d, c, torch.float32)
+        w, E, k = meta[0], meta[5], meta[6]
+        x = d[c + "_x"]
+        y = np.zeros_like(x)
+        dx = np.zeros_like(x)
+        for r, p in enumerate(positions):
+            dec = ctx.per_rank[r]["decision"]
+            lg = ctx.per_rank[r]["logits"].cpu().numpy()
+            ro = O.route_logits(lg, k, params.gate_fn, params.renormalize_topk)
+            np.testing.assert_array_equal(dec.experts.cpu().numpy(), ro.experts, err_msg=c)
+            np.testing.assert_array_equal(dec.experts.cpu().numpy(), d[c + "_experts"][p], err_msg=c)
+            np.testing.assert_array_equal(dec.kept.cpu().numpy(), d[c + "_kept"][p], err_msg=c)
+            y[p] = outs[r].float().cpu().numpy()
+            dx[p] = res.input_grads[r].float().cpu().numpy()
+        assert O.rel_err(y, d[c + "_y"]) < tol, (c, O.rel_err(y, d[c + "_y"]))
+        assert O.rel_err(dx, d[c + "_dx"]) < tol, (c, O.rel_err(dx, d[c + "_dx"]))
+        assert O.rel_err(res.w_g_grad.cpu().numpy(), d[c + "_dwg"]) < tol, c
+        ep, etp = meta[3], meta[4]
+        local = E // ep
+        for e in range(E):
+            ei, le = e // local, e % local
+            g1 = torch.cat([res.expert_grads[(ei, tt)][0][le] for tt in range(etp)], dim=1)
+            g2 = torch.cat([res.expert_grads[(ei, tt)][1][le] for tt in range(etp)], dim=0)
+            assert O.rel_err(g1.cpu().numpy(), d[c + "_dw1"][e]) < tol, (c, e)
+            assert O.rel_err(g2.cpu().numpy(), d[c + "_dw2"][e]) < tol, (c, e)
+
+
+def test_layer_cases_bf16_vs_oracle_with_gpu_logits(golden):
+    """bf16 mode on the golden topologies vs the pinned oracle fed the GPU's own
+    logits and the bf16-rounded inputs (routing bit-exact, values 2e-2)."""
+    d = golden("layer")
+    for c in _cases(d, "l"):
+        meta, params, positions, outs, ctx, res = _run_layer_case(d, c, torch.bfloat16)
+        w, E, k, seq, full = meta[0], meta[5], meta[6], meta[9], meta[12]
+        cf = float(d[c + "_cf"][0])
+        cfg = O.LayerConfig(k=k, gate_fn=params.gate_fn, renormalize=params.renormalize_topk,
+                            capacity_factor=None if cf < 0 else cf)
+        experts = [O.Expert(d[c + "_w1"][e], d[c + "_w2"][e], "gelu" if meta[15] else "relu")
+                   for e in range(E)]
+        lgs = [ctx.per_rank[r]["logits"].cpu().numpy().astype(np.float64) for r in range(w)]
+        kept_over = [None] * w
+        if full and cfg.capacity_factor is not None:
+            routs = [O.route_logits(lg, k, cfg.gate_fn, cfg.renormalize) for lg in lgs]
+            kept_over = O.full_sequence_kept([r.experts for r in routs], [r.gates for r in routs],
+                                             positions, seq, cfg.capacity_factor, E)
+        rnd = lambda a: t(a, torch.bfloat16).float().cpu().numpy().astype(np.float64)  # noqa: E731
+        x, u = d[c + "_x"], d[c + "_u"]
+        y = np.zeros_like(x); yw = np.zeros_like(x); dx = np.zeros_like(x); dxw = np.zeros_like(x)
+        for r, p in enumerate(positions):
+            yo, st = O.layer_forward(rnd(x[p]), lgs[r], experts, cfg, positions=p,
+                                     kept_override=kept_over[r])
+            g = O.layer_backward(rnd(u[p]), st, experts, cfg, w_g=d[c + "_wg"])
+            dec = ctx.per_rank[r]["decision"]
+            np.testing.assert_array_equal(dec.experts.cpu().numpy(), st.routing.experts, err_msg=c)
+            np.testing.assert_array_equal(dec.kept.cpu().numpy(), st.routing.kept, err_msg=c)
+            y[p], yw[p] = outs[r].float().cpu().numpy(), yo
+            dx[p], dxw[p] = res.input_grads[r].float().cpu().numpy(), g[0]
+        assert O.rel_err(y, yw) < BF16_TOL, (c, O.rel_err(y, yw))
+        assert O.rel_err(dx, dxw) < BF16_TOL, (c, O.rel_err(dx, dxw))
+
+
+def _oracle_layer(x, lg, experts, cfg, u, wg, positions=None):
+    y, st = O.layer_forward(x, lg, experts, cfg, positions=positions)
+    g = O.layer_backward(u, st, experts, cfg, w_g=wg)
+    return y, st, g
+
+
+@pytest.mark.parametrize("act", ["relu", "swiglu"])
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, FP32_TOL), (torch.bfloat16, BF16_TOL)])
+@pytest.mark.parametrize("cf", [None, 1.0])
+def test_c1_shape_layer_vs_oracle(act, dtype, tol, cf):
+    """C1 (BASELINE.json configs[0]): E8 top-2, H1024, F2816, T4096, EP=1."""
+    E, k, H, F, T, seed = 8, 2, 1024, 2816, 4096, 0
+    if act == "swiglu":
+        F = 2816  # multiple of 32
+    topo = B.ParallelTopology(world_size=1)
+    wg = O.gating_matrix(H, E, seed)
+    params = B.GatingParams(w_g=wg, k=k, capacity_factor=cf)
+    weights = B.init_expert_weights(E, H, F, 1, seed, activation=act)
+    x = O.token_rows(T, H, seed, 2)
+    u = O.token_rows(T, H, seed, 3)
+    block = B.TokenBlock(t(x, dtype), np.arange(T))
+    outs, ctx = B.moe_forward([block], weights, topo, params, B.LocalWorld(1))
+    res = B.moe_backward([t(u, dtype)], ctx)
+    lg = ctx.per_rank[0]["logits"].cpu().numpy().astype(np.float64)
+    w0 = weights[(0, 0)]
+    experts = [O.Expert(np.asarray(a), np.asarray(b), act) for a, b in zip(w0.w1, w0.w2)]
+    cfg = O.LayerConfig(k=k, capacity_factor=cf)
+    xin = x if dtype == torch.float32 else t(x, dtype).float().cpu().numpy().astype(np.float64)
+    uin = u if dtype == torch.float32 else t(u, dtype).float().cpu().numpy().astype(np.float64)
+    y, st, g = _oracle_layer(xin, lg, experts, cfg, uin, wg)
+    dec = ctx.per_rank[0]["decision"]
+    np.testing.assert_array_equal(dec.experts.cpu().numpy(), st.routing.experts)
+    np.testing.assert_array_equal(dec.kept.cpu().numpy(), st.routing.kept)
+    assert O.rel_err(outs[0].float().cpu().numpy(), y) < tol
+    assert O.rel_err(res.input_grads[0].float().cpu().numpy(), g[0]) < tol
+    assert O.rel_err(res.w_g_grad.cpu().numpy(), g[2]) < tol
+    for e in range(E):
+        assert O.rel_err(res.expert_grads[(0, 0)][0][e].cpu().numpy(), g[3][e]) < tol
+        assert O.rel_err(res.expert_grads[(0, 0)][1][e].cpu().numpy(), g[4][e]) < tol
