@@ -1,0 +1,339 @@
+"""MoE-layer fwd+bwd benchmark (BASELINE.json metric) on B200.
+
+Workload (N=1): Mixtral-8x7B MoE layer shape -- 8 experts top-2, hidden 4096,
+expert FFN 14336 (SwiGLU), 16384 tokens per GPU, dropless, bf16 -- all 8
+experts on the one GPU (EP=1).  N>1 (torchrun, one rank per GPU): EP=N with
+16384 tokens per GPU (weak scaling), NCCL all-to-all-v dispatch/combine.
+
+A step = router -> dispatch -> grouped SwiGLU FFN -> combine, then the full
+backward (input, router and expert weight gradients).  Synthetic N(0,1)
+tokens and U(+-1/sqrt(H)) weights (the reference's init distributions).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle port
+(numpy float64, the reference's algorithm) on a bounded token sample instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer fwd+bwd tokens/s"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU")
+    ap.add_argument("--hidden", type=int, default=4096)
+    ap.add_argument("--ffn", type=int, default=14336)
+    ap.add_argument("--experts", type=int, default=8)
+    ap.add_argument("--topk", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="a few steps, no extra legs (for ncu)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops", 1665.1), d.get("bf16_tflops_sustained", 1401.1), d.get("hbm_gbs", 6536.0), "measured"
+    except OSError:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_reference_sample(a, n_tokens: int, reps: int = 1, warm: int = 0):
+    """Time the CPU oracle (numpy float64 restatement of the reference's
+    moe_forward + moe_backward) on `n_tokens` tokens at full H/F/k width.
+    Only k experts are materialised (every token routes to both), which keeps
+    the per-token work of the full config while bounding host memory."""
+    import numpy as np
+
+    from oracle import moe_oracle as O
+
+    threads = os.cpu_count() or 1
+    H, F, k = a.hidden, a.ffn, a.topk
+    E = k
+    rng = np.random.default_rng(0)
+    b = 1.0 / np.sqrt(H)
+    experts = []
+    for _ in range(E):
+        w1 = rng.uniform(-b, b, size=(H, 2 * F))
+        w2 = rng.uniform(-b, b, size=(F, H))
+        experts.append(O.Expert(w1, w2, "swiglu"))
+    wg = rng.uniform(-b, b, size=(H, E))
+    cfg = O.LayerConfig(k=k)
+    x = rng.standard_normal((n_tokens, H))
+    u = rng.standard_normal((n_tokens, H))
+    times = []
+    for i in range(warm + reps):
+        t0 = time.perf_counter()
+        y, st = O.layer_forward(x, x @ wg, experts, cfg)
+        O.layer_backward(u, st, experts, cfg, w_g=wg)
+        dt = time.perf_counter() - t0
+        if i >= warm:
+            times.append(dt)
+    return n_tokens / (sum(times) / len(times)), threads, times
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = 128
+    tok_s, threads, times = cpu_reference_sample(a, n, reps=a.steps, warm=a.warmup)
+    sample = (f"{n} tokens/step at H={a.hidden} F={a.ffn} SwiGLU top-{a.topk} (k experts "
+              f"materialised), numpy float64 oracle port, {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT,
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1000.0 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(a),
+        "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": tok_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def workload_config(a):
+    return {"workload": f"Mixtral-8x7B MoE layer (C2 shape): E{a.experts} top-{a.topk} H{a.hidden} "
+                        f"F{a.ffn} SwiGLU, {a.tokens} tokens/GPU, dropless",
+            "tokens_per_gpu": a.tokens, "experts": a.experts, "top_k": a.topk,
+            "hidden": a.hidden, "ffn": a.ffn, "activation": "swiglu",
+            "parallelism": f"ep{a.gpus}", "l2": "per-step working set >10 GB (>> 126 MB L2)"}
+
+
+# --------------------------------------------------------------- GPU arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_14960_b200 as B
+    from paper_2504_14960_b200 import _lib
+    from paper_2504_14960_b200 import dispatcher as D
+    from paper_2504_14960_b200 import gemm_tc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+
+    E, k, H, F, T = a.experts, a.topk, a.hidden, a.ffn, a.tokens
+    topo = B.ParallelTopology(world_size=world, ep=world)
+    seed = 0
+    rng = np.random.default_rng([seed, 0])
+    bnd = 1.0 / np.sqrt(H)
+    wg = torch.as_tensor(rng.uniform(-bnd, bnd, size=(H, E)), dtype=torch.float32)
+    params = B.GatingParams(w_g=wg, k=k)
+    L_ = E // world
+    # random-init local experts directly on the device (U(+-1/sqrt(H)))
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    w1 = [((torch.rand((H, 2 * F), generator=g, device=dev) * 2 - 1) * bnd) for _ in range(L_)]
+    w2 = [((torch.rand((F, H), generator=g, device=dev) * 2 - 1) * bnd) for _ in range(L_)]
+    ep_idx = rank
+    weights = B.ExpertWeights(tuple(range(ep_idx * L_, (ep_idx + 1) * L_)), w1, w2, "swiglu", 0, 1)
+    weights.packed(torch.bfloat16, dev)
+    del w1, w2
+    groups = B.generate_parallel_groups(topo)
+    if world > 1:
+        nw = B.NcclWorld()
+        nw.setup_groups([groups.moe["EP"], groups.moe["ETP"], groups.moe["EDP"], [tuple(range(world))]])
+        ctx = B.collectives.NcclRankContext(nw)
+    else:
+        nw = B.LocalWorld(1, dev)
+        ctx = B.collectives.LocalRankContext(nw, 0)
+    layer = D.RankLayer(params, weights, topo, D._rank_groups(topo, groups, rank), rank,
+                        torch.bfloat16, dev)
+    x = torch.randn((T, H), generator=g, device=dev).to(torch.bfloat16)
+    u = torch.randn((T, H), generator=g, device=dev).to(torch.bfloat16)
+    positions = torch.arange(T, dtype=torch.int64) + rank * T
+
+    def step():
+        out, sv = layer.forward(ctx, x, positions)
+        dx, dwg, dw1, dw2 = layer.backward(ctx, u, sv)
+        if world > 1:
+            dwg = ctx.all_reduce(tuple(range(world)), dwg)
+        return out, dx
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.reset_launch_count()
+    total_ms = 0.0
+    for _ in range(a.steps):
+        flush.zero_()  # evict L2 between timed steps (outside the events)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step()
+        e1.record()
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+    launches = _lib.launch_count()
+    clk = clocks.stop()
+    ms = total_ms / a.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    value = world * T / (ms / 1e3)
+
+    # ---- roofline: event-timed expert GEMM launches of one instrumented step
+    burst, sustained, hbm, src = peaks()
+    gemm_tc.PROFILE.enable()
+    step()
+    torch.cuda.synchronize()
+    per_launch = gemm_tc.PROFILE.collect()
+    gemm_tc.PROFILE.disable()
+    P = T * k  # kept pairs per GPU (dropless)
+    flops_step = 18.0 * P * H * F  # SwiGLU fwd 6PHF + bwd 12PHF
+    gemm_ms = sum(ms_ for _, ms_ in per_launch)
+    achieved = flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    roof = {"bound": "tensor", "kernel": "gemm_tc (grouped SwiGLU FFN, 6 launches/step)",
+            "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+            "frac": achieved / sustained if achieved else None, "traffic": None,
+            "peak_kind": f"{src} sustained bf16 (burst {burst})",
+            "algorithmic_flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
+            "gemm_share_of_step": gemm_ms / ms if ms else None,
+            "launches_ms": [[n, round(m, 4)] for n, m in per_launch],
+            "layer_frac_of_peak": value / world * flops_step / T / 1e12 / sustained}
+
+    # ---- e2e through the public API with host (pinned) buffers
+    e2e = None
+    if not a.no_e2e and not a.profile_only:
+        xh = x.cpu().pin_memory()
+        uh = u.cpu().pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        dxh = torch.empty_like(xh).pin_memory()
+        blocks = [None] * world
+        blocks[rank] = B.TokenBlock(xh, positions)
+        ups = [None] * world
+        ups[rank] = uh
+        wmap = {(rank, 0): weights}
+        api_world = nw
+
+        def e2e_step():
+            outs, fctx = B.moe_forward(blocks, wmap, topo, params, api_world, dtype=torch.bfloat16,
+                                       check_finite_inputs=False)
+            yh.copy_(outs[rank], non_blocking=True)
+            res = B.moe_backward(ups, fctx)
+            dxh.copy_(res.input_grads[rank], non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            e2e_step()
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / a.steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t)
+        e2e = {"value": world * T / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * xh.numel() * xh.element_size(),
+               "d2h_bytes_per_step": 2 * yh.numel() * yh.element_size(),
+               "ms_per_step": e2e_ms,
+               "path": "moe_forward/moe_backward API, pinned host x/u in, y/dx out"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
+        n = 256
+        tok_s, threads, _ = cpu_reference_sample(a, n)
+        cpu = {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{n} tokens at H={a.hidden} F={a.ffn} SwiGLU top-{a.topk}, numpy float64 "
+                         f"oracle port of moe_forward+moe_backward, {threads} threads"}
+
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload_config(a),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+        }), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -168,6 +168,36 @@ typedef struct {
 /* Portable SIMT implementation (fp32 parity mode and cross-check). */
 B200MOE_API int b200moe_gemm_simt(const b200moe_gemm_args* args, void* stream);
 
+/* Tensor-core grouped GEMM (tcgen05 + TMEM + TMA, bf16 in, fp32 accumulate)
+ * with fused expert epilogues.  Operands:
+ *   A K-major  [a_rows, lda]      (row = token, K contiguous)
+ *   A MN-major [a_rows, lda]      (row = K index = token, M contiguous; grouped K)
+ *   B K-major  [b_batch, N, ldb]  (weights, K contiguous)
+ *   B MN-major [b_batch, K, ldb]  (N contiguous); grouped K: [a_rows, ldb]
+ * grouped_dim 0 (M): group g owns rows [group_off[g], group_off[g+1]) of A and
+ *   C, uses weight batch group_expert[g] (identity when NULL).
+ * grouped_dim 1 (K): group g reduces over rows [group_off[g], group_off[g+1])
+ *   (multiples of 64), C_g = C + g*c_sg.
+ * epilogue: 0 store (bf16/fp32, accumulate), 1 SwiGLU fwd (C=pre, H=h),
+ *   2 SwiGLU bwd (acc=dh [.,N=F], PRE=pre, C=dpre), 3 act fwd, 4 act bwd.
+ * num_ctas: persistent grid size (<= 0: one CTA per SM). */
+typedef struct {
+  int G;
+  int grouped_dim;
+  int64_t M, N, K;
+  const void* A; int a_major; int64_t lda; int64_t a_rows;
+  const void* B; int b_major; int64_t ldb; int64_t b_batch; int64_t b_batch_stride;
+  void* C; int64_t ldc; int64_t c_sg; int out_dtype; int accumulate;
+  const int32_t* group_off;
+  const int32_t* group_expert;
+  int epilogue; int act;
+  void* H; int64_t ldh;
+  const void* PRE; int64_t ldpre;
+  int num_ctas;
+} b200moe_tc_gemm_args;
+
+B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);
+
 /* Elementwise expert activations in the padded row layout, rows < group_off[G].
  * SwiGLU layout: pre has 2F columns, 64-column blocks of [32 gate | 32 up]. */
 B200MOE_API int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,

@@ -266,9 +266,13 @@ def expert_forward(x: np.ndarray, ex: Expert) -> Tuple[np.ndarray, np.ndarray]:
     return h @ ex.w2, pre
 
 
-def expert_backward(dy: np.ndarray, x: np.ndarray, pre: np.ndarray, ex: Expert):
+def expert_backward(dy: np.ndarray, x: np.ndarray, pre: np.ndarray, ex: Expert,
+                    relu_mask: Optional[np.ndarray] = None):
     """experts.py:146-172: recompute the activation from ``pre``; returns
-    (dx_partial, dw1, dw2)."""
+    (dx_partial, dw1, dw2).  ``relu_mask`` optionally supplies relu'(pre) as
+    observed by the implementation under test: where a pre-activation lies
+    within rounding of 0 the two sides may legitimately disagree on the sign
+    (the discontinuity oracle.py:176-186 skips as an unstable probe)."""
     dy = np.asarray(dy, dtype=np.float64)
     if ex.act == "swiglu":
         f = pre.shape[1] // 2
@@ -278,8 +282,11 @@ def expert_backward(dy: np.ndarray, x: np.ndarray, pre: np.ndarray, ex: Expert):
         dpre = np.concatenate([dh * u * silu_grad(g), dh * silu(g)], axis=1)
     else:
         h = act_fwd(pre, ex.act)
+        if ex.act == "relu" and relu_mask is not None:
+            h = np.where(relu_mask, pre, 0.0)
         dh = dy @ ex.w2.T
-        dpre = dh * act_grad(pre, ex.act)
+        grad = act_grad(pre, ex.act) if relu_mask is None or ex.act != "relu" else relu_mask.astype(np.float64)
+        dpre = dh * grad
     dw2 = h.T @ dy
     dw1 = x.T @ dpre
     return dpre @ ex.w1.T, dw1, dw2
@@ -355,7 +362,8 @@ def layer_forward(x: np.ndarray, logits: np.ndarray, experts: Sequence[Expert],
 
 
 def layer_backward(u: np.ndarray, st: LayerState, experts: Sequence[Expert], cfg: LayerConfig,
-                   w_g: Optional[np.ndarray] = None, shared: Optional[Expert] = None):
+                   w_g: Optional[np.ndarray] = None, shared: Optional[Expert] = None,
+                   relu_masks: Optional[Dict[int, np.ndarray]] = None):
     """Backward of ``sum(u * forward)`` -- dispatcher.py:409-500.
 
     Returns (dx, dlogits, dwg or None, dw1 list, dw2 list, shared grads or None).
@@ -376,7 +384,8 @@ def layer_backward(u: np.ndarray, st: LayerState, experts: Sequence[Expert], cfg
     for e in range(E):
         rows = np.flatnonzero(e_sorted == e)
         if rows.size:
-            d, g1, g2 = expert_backward(dy_perm[rows], st.xs[e], st.pres[e], experts[e])
+            mask = None if relu_masks is None else relu_masks.get(e)
+            d, g1, g2 = expert_backward(dy_perm[rows], st.xs[e], st.pres[e], experts[e], mask)
             dx_perm[rows] = d
             dw1[e] += g1
             dw2[e] += g2

@@ -19,6 +19,7 @@ F32, BF16 = 0, 1
 GATE_SOFTMAX, GATE_SIGMOID = 0, 1
 ACT_RELU, ACT_GELU, ACT_SWIGLU = 0, 1, 2
 ACT_CODES = {"relu": ACT_RELU, "gelu": ACT_GELU, "swiglu": ACT_SWIGLU}
+MAJOR_K, MAJOR_MN = 0, 1
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -55,6 +56,7 @@ _SIGS = {
     "b200moe_permute_bwd": [P, I32, I64, I64, I32, P, P, P, P, P, P, P, I32, I32, P],
     "b200moe_combine": [P, I32, I64, I64, I32, P, P, P, P, I32, P, I32, I32, P],
     "b200moe_gemm_simt": [ctypes.POINTER(GemmArgs), P],
+    "b200moe_gemm_tc": [P, P],  # argtypes refined in gemm_tc.py
     "b200moe_act_fwd": [P, I32, I32, P, I32, I64, I64, P, P],
     "b200moe_act_bwd": [P, P, I32, I32, P, I32, I64, I64, P, P],
 }
@@ -105,9 +107,35 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(msg)
 
 
+# kernels launched per entry point (bench.py reports the total as gpu_launches)
+_LAUNCHES = {"b200moe_dispatch_plan": 3}
+_NO_LAUNCH = {"b200moe_version", "b200moe_last_error", "b200moe_device_check",
+              "b200moe_dispatch_plan_ws"}
+_launches = 0
+
+
+def note_launches(n: int) -> None:
+    global _launches
+    _launches += n
+
+
+def reset_launch_count() -> None:
+    global _launches
+    _launches = 0
+
+
+def launch_count() -> int:
+    return _launches
+
+
 def call(name: str, *args) -> None:
     lib = load()
     check(getattr(lib, name)(*args), name)
+    if name not in _NO_LAUNCH:
+        n = _LAUNCHES.get(name, 1)
+        if name in ("b200moe_permute", "b200moe_permute_bwd") and args[-5]:
+            n += 1  # alignment-padding zero kernel
+        note_launches(n)
 
 
 def ptr(t) -> Optional[int]:

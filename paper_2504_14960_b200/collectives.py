@@ -87,7 +87,10 @@ class LocalWorld:
         if n_ranks < 1:
             raise ValidationError("n_ranks must be >= 1", constraint="n_ranks>=1")
         self.n_ranks = n_ranks
-        self.device = torch.device(device or "cuda")
+        dev = torch.device(device or "cuda")
+        if dev.type == "cuda" and dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
         self._cond = threading.Condition()
         self._slots: Dict[tuple, _Slot] = {}
         self._seq: Dict[tuple, int] = {}

@@ -36,6 +36,7 @@ int permute_bwd(const void*, int, int64_t, int64_t, int, const int32_t*, const f
 int combine(const void*, int, int64_t, int64_t, int, const int32_t*, const float*, const float*,
             const float*, int, void*, int, int, cudaStream_t);
 int gemm_simt(const b200moe_gemm_args*, cudaStream_t);
+int gemm_tc(const b200moe_tc_gemm_args*, cudaStream_t);
 int act_fwd(const void*, int, int, const int32_t*, int, int64_t, int64_t, void*, cudaStream_t);
 int act_bwd(const void*, const void*, int, int, const int32_t*, int, int64_t, int64_t, void*,
             cudaStream_t);
@@ -114,7 +115,7 @@ int b200moe_dispatch_plan(const int32_t* topk_idx, const float* gates, const uin
   REQUIRE(expert_counts && expert_offsets && padded_offsets && workspace,
           "dispatch_plan: null pointer");
   if (T > 0) REQUIRE(topk_idx && kept_out && send_row && gemm_row && perm, "dispatch_plan: null pointer");
-  REQUIRE(!perm_gates || gates, "dispatch_plan: perm_gates needs gates");
+  REQUIRE(T == 0 || !perm_gates || gates, "dispatch_plan: perm_gates needs gates");
   return dispatch_plan(topk_idx, gates, kept_in, order, T, k, E, cap, align, workspace, kept_out,
                        expert_counts, expert_offsets, padded_offsets, send_row, gemm_row, perm,
                        perm_gates, S(stream));
@@ -192,6 +193,25 @@ int b200moe_gemm_simt(const b200moe_gemm_args* a, void* stream) {
   if (a->grouped_dim == 0) REQUIRE(a->K >= 1 && a->max_rows >= 0, "gemm_simt: bad K/max_rows");
   else REQUIRE(a->M >= 1, "gemm_simt: bad M");
   return gemm_simt(a, S(stream));
+}
+
+int b200moe_gemm_tc(const b200moe_tc_gemm_args* a, void* stream) {
+  REQUIRE(a, "gemm_tc: null args");
+  REQUIRE(a->grouped_dim == 0 || a->grouped_dim == 1, "gemm_tc: bad grouped_dim");
+  REQUIRE(a->N >= 1 && a->a_rows >= 0 && a->b_batch >= 1, "gemm_tc: bad shape");
+  REQUIRE(a->grouped_dim == 1 || a->K >= 1, "gemm_tc: bad K");
+  REQUIRE(a->grouped_dim == 0 || a->M >= 1, "gemm_tc: bad M");
+  REQUIRE(a->A && a->B && a->C && a->group_off, "gemm_tc: null pointer");
+  REQUIRE(a->epilogue >= 0 && a->epilogue <= 4, "gemm_tc: bad epilogue %d", a->epilogue);
+  REQUIRE(a->epilogue == 0 || a->grouped_dim == 0, "gemm_tc: fused epilogues need grouped M");
+  REQUIRE(a->epilogue == 0 || a->out_dtype == B200MOE_BF16, "gemm_tc: fused epilogues write bf16");
+  REQUIRE(!a->accumulate || a->out_dtype == B200MOE_F32, "gemm_tc: accumulate needs fp32 out");
+  REQUIRE((a->epilogue != 1 && a->epilogue != 3) || a->H, "gemm_tc: epilogue needs H");
+  REQUIRE((a->epilogue != 2 && a->epilogue != 4) || a->PRE, "gemm_tc: epilogue needs PRE");
+  REQUIRE(a->epilogue != 1 || a->N % 64 == 0, "gemm_tc: SwiGLU fwd needs N %% 64 == 0");
+  REQUIRE(a->epilogue != 2 || a->N % 32 == 0, "gemm_tc: SwiGLU bwd needs N %% 32 == 0");
+  if (a->a_rows == 0) return B200MOE_OK;
+  return gemm_tc(a, S(stream));
 }
 
 int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,

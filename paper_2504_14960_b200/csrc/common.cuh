@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
 
 #include "../../include/b200moe.h"
 

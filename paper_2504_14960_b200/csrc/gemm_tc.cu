@@ -1,0 +1,661 @@
+// K3: grouped expert GEMM on 5th-gen tensor cores (sm_100a).
+//
+//   tcgen05.mma (kind::f16, bf16 x bf16 -> fp32 in TMEM), operands staged in
+//   shared memory by TMA (cp.async.bulk.tensor, 128B swizzle) through an
+//   mbarrier ring, accumulators double-buffered in TMEM (2 x 256 columns) so
+//   the epilogue of tile i overlaps the MMAs of tile i+1.  Persistent CTAs
+//   (one per SM) walk a static tile schedule built from the group offsets in
+//   device memory, so variable per-expert token counts never reach the host.
+//
+//   warp 0      TMA producer (one lane)
+//   warp 1      MMA issuer   (one lane)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld -> fused activation -> global stores
+//
+// Reference arithmetic: experts.py:130-172 (forward x@W1, act, @W2; backward
+// dW2 = act^T dy, dh = dy W2^T, dpre = dh*act', dW1 = x^T dpre, dx = dpre W1^T).
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace b200moe {
+
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int TMEM_COLS = 512;  // 2 accumulator buffers of BN fp32 columns
+constexpr int MAX_G = 1024;
+constexpr int NUM_THREADS = 256;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 1024 /*barriers*/ +
+                           (MAX_G + 1) * 4;
+
+enum Epi : int {
+  EPI_STORE = 0,       // C = acc (bf16 or fp32, optional accumulate)
+  EPI_SWIGLU_FWD = 1,  // acc = [gate|up] interleaved 32-col blocks -> pre (bf16), h = silu(g)*u
+  EPI_SWIGLU_BWD = 2,  // acc = dh [.. F]; reads pre -> dpre (interleaved)
+  EPI_ACT_FWD = 3,     // acc = pre -> pre (bf16), h = act(pre)
+  EPI_ACT_BWD = 4,     // acc = dh; reads pre -> dpre = dh * act'(pre)
+};
+
+struct Params {
+  int G;
+  int grouped_k;   // 0: groups over M, 1: groups over K
+  int64_t M, N, K; // fixed extents (M for grouped-K, K for grouped-M)
+  const int32_t* goff;
+  const int32_t* gexp;
+  int64_t max_rows;
+  // epilogue
+  int epi;
+  int act;         // relu/gelu for EPI_ACT_*
+  int out_f32;
+  int accumulate;
+  void* C;
+  int64_t ldc;
+  int64_t c_sg;
+  void* H;         // second output (h) for *_FWD epilogues
+  int64_t ldh;
+  const void* PRE; // pre-activation input for *_BWD epilogues
+  int64_t ldpre;
+};
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
+// Bounded wait: a protocol bug traps (launch error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++n > (1u << 26)) {
+      printf("b200moe gemm_tc: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint32_t dst, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start
+// address, leading/stride byte offsets (>>4), version 1, 128B swizzle.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M=128, N=BN.
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+  return (1u << 4)                     // D format f32
+         | (1u << 7) | (1u << 10)      // A, B = bf16
+         | ((a_mn ? 1u : 0u) << 15)    // A major
+         | ((b_mn ? 1u : 0u) << 16)    // B major
+         | ((uint32_t)(BN >> 3) << 17) // N
+         | ((uint32_t)(BM >> 4) << 24); // M
+}
+
+// ------------------------------------------------------------- scheduling
+struct Tile {
+  int g;
+  int64_t m0, m_end;  // rows (grouped-M: absolute rows of the padded layout)
+  int64_t n0;
+  int64_t kbeg;       // first K coordinate (grouped-K: absolute row)
+  int nkb;            // number of BK blocks
+  int bidx;           // weight/expert index for B (grouped-M)
+};
+
+__device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, int t) {
+  // largest g with prefix[g] <= t
+  int lo = 0, hi = p.G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  Tile r;
+  r.g = lo;
+  const int local = t - prefix[lo];
+  const int64_t g0 = p.goff[lo], g1 = p.goff[lo + 1];
+  if (!p.grouped_k) {
+    const int mt = (int)((g1 - g0 + BM - 1) / BM);
+    const int nb = local / mt, mb = local % mt;
+    r.m0 = g0 + (int64_t)mb * BM;
+    r.m_end = g1;
+    r.n0 = (int64_t)nb * BN;
+    r.kbeg = 0;
+    r.nkb = (int)((p.K + BK - 1) / BK);
+    r.bidx = p.gexp ? p.gexp[lo] : lo;
+  } else {
+    const int mt = (int)((p.M + BM - 1) / BM);
+    const int nb = local / mt, mb = local % mt;
+    r.m0 = (int64_t)mb * BM;
+    r.m_end = p.M;
+    r.n0 = (int64_t)nb * BN;
+    r.kbeg = g0;
+    // groups are 64-aligned in the padded layout; a ragged last group reads
+    // past the buffer end, which TMA zero-fills
+    r.nkb = (int)((g1 - g0 + BK - 1) / BK);
+    r.bidx = 0;
+  }
+  return r;
+}
+
+// ------------------------------------------------------------- epilogues
+__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+__device__ __forceinline__ float gelu_tc(float x) {
+  const float c = 0.7978845608028654f;
+  return 0.5f * x * (1.f + tanhf(c * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_tc(float x) {
+  const float c = 0.7978845608028654f;
+  const float t = tanhf(c * (x + 0.044715f * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * x * x);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_bf16(uint32_t v) {
+  __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&v);
+  return __bfloat1622float2(h);
+}
+
+// store 32 consecutive values (fp32 in f[]) of one row at column n (masked by N)
+__device__ __forceinline__ void store_row32(void* base, bool f32, int64_t row_off, int64_t n,
+                                            int64_t N, const float* f, bool accumulate) {
+  if (f32) {
+    float* p = static_cast<float*>(base) + row_off + n;
+    if (n + 32 <= N && (((uintptr_t)p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 v = make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]);
+        if (accumulate) {
+          const float4 o = *reinterpret_cast<const float4*>(p + i);
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        *reinterpret_cast<float4*>(p + i) = v;
+      }
+    } else {
+      for (int i = 0; i < 32 && n + i < N; ++i) p[i] = accumulate ? p[i] + f[i] : f[i];
+    }
+  } else {
+    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + row_off + n;
+    if (n + 32 <= N && (((uintptr_t)p) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 v;
+        v.x = pack_bf16(f[i], f[i + 1]);
+        v.y = pack_bf16(f[i + 2], f[i + 3]);
+        v.z = pack_bf16(f[i + 4], f[i + 5]);
+        v.w = pack_bf16(f[i + 6], f[i + 7]);
+        *reinterpret_cast<uint4*>(p + i) = v;
+      }
+    } else {
+      for (int i = 0; i < 32 && n + i < N; ++i) p[i] = __float2bfloat16_rn(f[i]);
+    }
+  }
+}
+
+__device__ __forceinline__ void load_row32_bf16(const void* base, int64_t off, float* f) {
+  const uint4* p = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 v = p[i];
+    float2 a = unpack_bf16(v.x), b = unpack_bf16(v.y), c = unpack_bf16(v.z), d = unpack_bf16(v.w);
+    f[8 * i + 0] = a.x; f[8 * i + 1] = a.y; f[8 * i + 2] = b.x; f[8 * i + 3] = b.y;
+    f[8 * i + 4] = c.x; f[8 * i + 5] = c.y; f[8 * i + 6] = d.x; f[8 * i + 7] = d.y;
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sA = base;
+  const uint32_t sB = base + STAGES * A_STAGE_BYTES;
+  const uint32_t bars = base + STAGES * STAGE_BYTES;
+  // barrier layout: full[S], empty[S], tfull[2], tempty[2], tmem slot
+  const uint32_t full_bar = bars, empty_bar = bars + 8 * STAGES;
+  const uint32_t tfull_bar = bars + 16 * STAGES, tempty_bar = tfull_bar + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * STAGE_BYTES + 16 * STAGES + 32);
+  int32_t* prefix = reinterpret_cast<int32_t*>(gbase + STAGES * STAGE_BYTES + 1024);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // per-group tile counts -> prefix (smem)
+  for (int g = threadIdx.x; g < p.G; g += NUM_THREADS) {
+    int tiles;
+    if (!p.grouped_k) {
+      const int64_t rows = p.goff[g + 1] - p.goff[g];
+      tiles = (int)(((rows + BM - 1) / BM) * ((p.N + BN - 1) / BN));
+    } else {
+      tiles = (int)(((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN));
+    }
+    prefix[g + 1] = tiles;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(full_bar + 8 * i, 1);
+      mbar_init(empty_bar + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull_bar + 8 * i, 1);
+      mbar_init(tempty_bar + 8 * i, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_a);
+    prefetch_map(&map_b);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    prefix[0] = 0;
+    for (int g = 0; g < p.G; ++g) prefix[g + 1] += prefix[g];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = prefix[p.G];
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile tl = decode(p, prefix, t);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          mbar_wait(empty_bar + 8 * stage, phase ^ 1);
+          const uint32_t fb = full_bar + 8 * stage;
+          mbar_expect_tx(fb, STAGE_BYTES);
+          const int kc = (int)(tl.kbeg + (int64_t)kb * BK);
+          const uint32_t a_dst = sA + stage * A_STAGE_BYTES;
+          const uint32_t b_dst = sB + stage * B_STAGE_BYTES;
+          if (!A_MN) {
+            // A [rows, K] K-major: box {64 K, 128 rows}
+            tma_load_3d(&map_a, a_dst, fb, kc, (int)tl.m0, 0);
+          } else {
+            // A stored [K, M] (M contiguous): 2 boxes {64 M, 64 K}
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_3d(&map_a, a_dst + i * 8192, fb, (int)tl.m0 + 64 * i, kc, 0);
+          }
+          if (!B_MN) {
+            // B stored [L, N, K]: box {64 K, 256 N, 1}
+            tma_load_3d(&map_b, b_dst, fb, kc, (int)tl.n0, tl.bidx);
+          } else {
+            // B stored [L, K, N] (N contiguous): 4 boxes {64 N, 64 K, 1}
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_3d(&map_b, b_dst + i * 8192, fb, (int)tl.n0 + 64 * i, kc, tl.bidx);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile tl = decode(p, prefix, t);
+        mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          mbar_wait(full_bar + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t a_s = sA + stage * A_STAGE_BYTES;
+          const uint32_t b_s = sB + stage * B_STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 32 B inside the 128B swizzle atom; MN-major:
+            // advance 16 K-rows (2 x 1024 B core-matrix groups).
+            const uint64_t ad = A_MN ? smem_desc(a_s + k * 2048, 8192, 1024)
+                                     : smem_desc(a_s + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(b_s + k * 2048, 8192, 1024)
+                                     : smem_desc(b_s + k * 32, 16, 1024);
+            tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(empty_bar + 8 * stage);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (tl.nkb > 0) tc_commit(tfull_bar + 8 * acc);
+        else mbar_arrive(tfull_bar + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
+    const int row_in_tile = 32 * q + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const Tile tl = decode(p, prefix, t);
+      mbar_wait(tfull_bar + 8 * acc, acc_phase);
+      tc_fence_after();
+      const int64_t row = tl.m0 + row_in_tile;
+      const bool live = row < tl.m_end;
+      const bool zero = tl.nkb == 0;
+      const int64_t c_off = p.grouped_k ? (int64_t)tl.g * p.c_sg : 0;
+      const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
+      if (p.epi == EPI_STORE) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_row + c * 32, v);
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = zero ? 0.f : __uint_as_float(v[i]);
+          const int64_t n = tl.n0 + c * 32;
+          if (live && n < p.N) store_row32(p.C, p.out_f32, c_off + row * p.ldc, n, p.N, f, p.accumulate);
+        }
+      } else if (p.epi == EPI_SWIGLU_FWD) {
+        // columns: 4 blocks of [32 gate | 32 up]; h column = (n0 + 64 b)/2 + i
+#pragma unroll 1
+        for (int b = 0; b < BN / 64; ++b) {
+          uint32_t vg[32], vu[32];
+          tmem_ld32(t_row + b * 64, vg);
+          tmem_ld32(t_row + b * 64 + 32, vu);
+          const int64_t n = tl.n0 + b * 64;
+          if (!live || n >= p.N) continue;
+          float g[32], u[32], h[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            // round the pre-activations to bf16 first so the saved `pre`
+            // and `h` agree exactly with what the backward recomputes
+            g[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(vg[i])));
+            u[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(vu[i])));
+            h[i] = silu_f(g[i]) * u[i];
+          }
+          store_row32(p.C, false, row * p.ldc, n, p.N, g, false);
+          store_row32(p.C, false, row * p.ldc, n + 32, p.N, u, false);
+          store_row32(p.H, false, row * p.ldh, n / 2, p.N / 2, h, false);
+        }
+      } else if (p.epi == EPI_SWIGLU_BWD) {
+        // acc = dh over F columns; pre/dpre are [.., 2F] interleaved
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_row + c * 32, v);
+          const int64_t n = tl.n0 + c * 32;  // F column, multiple of 32
+          if (!live || n >= p.N) continue;
+          const int64_t pc = (n / 32) * 64;  // gate block column in pre
+          float g[32], u[32], dg[32], du[32];
+          load_row32_bf16(p.PRE, row * p.ldpre + pc, g);
+          load_row32_bf16(p.PRE, row * p.ldpre + pc + 32, u);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float d = __uint_as_float(v[i]);
+            const float s = 1.f / (1.f + __expf(-g[i]));
+            dg[i] = d * u[i] * s * (1.f + g[i] * (1.f - s));
+            du[i] = d * g[i] * s;
+          }
+          store_row32(p.C, false, row * p.ldc, pc, 2 * p.N, dg, false);
+          store_row32(p.C, false, row * p.ldc, pc + 32, 2 * p.N, du, false);
+        }
+      } else if (p.epi == EPI_ACT_FWD) {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_row + c * 32, v);
+          const int64_t n = tl.n0 + c * 32;
+          if (!live || n >= p.N) continue;
+          float pre[32], h[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            pre[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[i])));
+            h[i] = p.act == B200MOE_ACT_RELU ? fmaxf(pre[i], 0.f) : gelu_tc(pre[i]);
+          }
+          store_row32(p.C, false, row * p.ldc, n, p.N, pre, false);
+          store_row32(p.H, false, row * p.ldh, n, p.N, h, false);
+        }
+      } else {  // EPI_ACT_BWD
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_row + c * 32, v);
+          const int64_t n = tl.n0 + c * 32;
+          if (!live || n >= p.N) continue;
+          float pre[32], d[32];
+          load_row32_bf16(p.PRE, row * p.ldpre + n, pre);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float gr = p.act == B200MOE_ACT_RELU ? (pre[i] > 0.f ? 1.f : 0.f) : gelu_grad_tc(pre[i]);
+            d[i] = __uint_as_float(v[i]) * gr;
+          }
+          store_row32(p.C, false, row * p.ldc, n, p.N, d, false);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar + 8 * acc);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+// 3-D bf16 tensor map {d0 (contiguous), d1, d2} with box {64, box1, 1}, 128B swizzle.
+static int make_map(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                    uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box1) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("gemm_tc: cuTensorMapEncodeTiled unavailable");
+    return B200MOE_ELAUNCH;
+  }
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_elems * 2, stride2_elems * 2};
+  cuuint32_t box[3] = {64, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("gemm_tc: cuTensorMapEncodeTiled failed (%d) dims=%llu,%llu,%llu", (int)r,
+              (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2);
+    return B200MOE_EINVAL;
+  }
+  return B200MOE_OK;
+}
+
+int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
+  using namespace tc;
+  if (a->G < 1 || a->G > MAX_G) {
+    set_error("gemm_tc: G=%d out of range [1, %d]", a->G, MAX_G);
+    return B200MOE_EUNSUPPORTED;
+  }
+  const bool a_mn = a->a_major == B200MOE_MAJOR_MN;
+  const bool b_mn = a->b_major == B200MOE_MAJOR_MN;
+  if (a->grouped_dim == 0 && a_mn) {
+    set_error("gemm_tc: grouped-M needs a K-major A operand");
+    return B200MOE_EUNSUPPORTED;
+  }
+  if (a->grouped_dim == 1 && !(a_mn && b_mn)) {
+    set_error("gemm_tc: grouped-K needs MN-major A and B operands");
+    return B200MOE_EUNSUPPORTED;
+  }
+  if ((a->lda % 8) || (a->ldb % 8)) {
+    set_error("gemm_tc: leading dimensions must be multiples of 8 elements (16 B)");
+    return B200MOE_EUNSUPPORTED;
+  }
+  CUtensorMap ma, mb;
+  int rc;
+  const uint64_t R = (uint64_t)a->a_rows;
+  if (!a_mn)  // A [R, K]: box {64 K, 128 rows}
+    rc = make_map(&ma, a->A, (uint64_t)a->K, R, 1, (uint64_t)a->lda, (uint64_t)a->lda * R, BM);
+  else        // A [R(K), M]: box {64 M, 64 K}
+    rc = make_map(&ma, a->A, (uint64_t)a->M, R, 1, (uint64_t)a->lda, (uint64_t)a->lda * R, 64);
+  if (rc) return rc;
+  if (!b_mn)  // B [batch, N, K]: box {64 K, 256 N, 1}
+    rc = make_map(&mb, a->B, (uint64_t)a->K, (uint64_t)a->N, (uint64_t)a->b_batch,
+                  (uint64_t)a->ldb, (uint64_t)a->b_batch_stride, BN);
+  else {      // B [batch, Kdim, N]: box {64 N, 64 K, 1}
+    const uint64_t kdim = a->grouped_dim == 1 ? R : (uint64_t)a->K;
+    const uint64_t bstride = a->b_batch > 1 ? (uint64_t)a->b_batch_stride : (uint64_t)a->ldb * kdim;
+    rc = make_map(&mb, a->B, (uint64_t)a->N, kdim, (uint64_t)a->b_batch, (uint64_t)a->ldb, bstride, 64);
+  }
+  if (rc) return rc;
+
+  Params p{};
+  p.G = a->G;
+  p.grouped_k = a->grouped_dim;
+  p.M = a->M;
+  p.N = a->N;
+  p.K = a->K;
+  p.goff = a->group_off;
+  p.gexp = a->group_expert;
+  p.max_rows = a->a_rows;
+  p.epi = a->epilogue;
+  p.act = a->act;
+  p.out_f32 = a->out_dtype == B200MOE_F32;
+  p.accumulate = a->accumulate;
+  p.C = a->C;
+  p.ldc = a->ldc;
+  p.c_sg = a->c_sg;
+  p.H = a->H;
+  p.ldh = a->ldh;
+  p.PRE = a->PRE;
+  p.ldpre = a->ldpre;
+
+  auto kern = a_mn ? (b_mn ? gemm_tc_kernel<true, true> : gemm_tc_kernel<true, false>)
+                    : (b_mn ? gemm_tc_kernel<false, true> : gemm_tc_kernel<false, false>);
+  static bool attr_set[4] = {false, false, false, false};
+  const int ki = (a_mn ? 2 : 0) + (b_mn ? 1 : 0);
+  if (!attr_set[ki]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+        cudaSuccess) {
+      set_error("gemm_tc: cannot set %d B dynamic shared memory", SMEM_BYTES);
+      return B200MOE_ELAUNCH;
+    }
+    attr_set[ki] = true;
+  }
+  const int grid = a->num_ctas > 0 ? a->num_ctas : num_sms();
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  B200MOE_CHECK_LAUNCH("gemm_tc");
+  return B200MOE_OK;
+}
+
+}  // namespace b200moe
