@@ -257,11 +257,18 @@ def main():
 
     # ---- roofline: event-timed expert GEMM launches of one instrumented step
     burst, sustained, hbm, src = peaks()
-    gemm_tc.PROFILE.enable()
+    flush.zero_()
+    torch.cuda.synchronize()
+    _lib.PROFILE.enable()
     step()
     torch.cuda.synchronize()
-    per_launch = gemm_tc.PROFILE.collect()
-    gemm_tc.PROFILE.disable()
+    all_launches, span_ms = _lib.PROFILE.collect()
+    _lib.PROFILE.disable()
+    per_launch = [(n, m) for n, m in all_launches if n.startswith("gemm_tc")]
+    other = {}
+    for n, m in all_launches:
+        if not n.startswith("gemm_tc"):
+            other[n] = other.get(n, 0.0) + m
     P = T * k  # kept pairs per GPU (dropless)
     flops_step = 18.0 * P * H * F  # SwiGLU fwd 6PHF + bwd 12PHF
     gemm_ms = sum(ms_ for _, ms_ in per_launch)
@@ -273,6 +280,9 @@ def main():
             "algorithmic_flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
             "gemm_share_of_step": gemm_ms / ms if ms else None,
             "launches_ms": [[n, round(m, 4)] for n, m in per_launch],
+            "other_kernels_ms": {n: round(m, 4) for n, m in sorted(other.items(), key=lambda x: -x[1])},
+            "instrumented_span_ms": span_ms,
+            "launch_gaps_ms": span_ms - sum(m for _, m in all_launches),
             "layer_frac_of_peak": value / world * flops_step / T / 1e12 / sustained}
 
     # ---- e2e through the public API with host (pinned) buffers

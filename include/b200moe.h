@@ -108,10 +108,12 @@ B200MOE_API int b200moe_router_bwd(const float* dgates, const float* scores, con
                        const float* gates, int64_t T, int E, int k, int gate_fn, int renorm,
                        float* dz, void* stream);
 
-/* dw_g[H,E] (fp32, overwritten) = x^T dz, fixed-order (deterministic)
- *                                                        -- dispatcher.py:489 */
+/* dw_g[H,E] (fp32, overwritten) = x^T dz, split over token chunks and
+ * reduced in a fixed order (deterministic).  workspace: >=
+ * b200moe_router_wgrad_ws(T, H, E) bytes.                -- dispatcher.py:489 */
+B200MOE_API size_t b200moe_router_wgrad_ws(int64_t T, int64_t H, int E);
 B200MOE_API int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz, int64_t T, int64_t H, int E,
-                         float* dw_g, void* stream);
+                         float* dw_g, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------- permute/combine */
 

@@ -51,7 +51,8 @@ _SIGS = {
     "b200moe_dispatch_plan": [P, P, P, P, I64, I32, I32, I64, I32, P, SZ, P, P, P, P, P, P, P, P, P],
     "b200moe_capacity_by_gate": [P, P, P, P, I64, I32, I32, I64, P, P],
     "b200moe_router_bwd": [P, P, P, P, I64, I32, I32, I32, I32, P, P],
-    "b200moe_router_wgrad": [P, I32, P, I64, I64, I32, P, P],
+    "b200moe_router_wgrad_ws": [I64, I64, I32],
+    "b200moe_router_wgrad": [P, I32, P, I64, I64, I32, P, P, SZ, P],
     "b200moe_permute": [P, I32, I64, I64, I32, P, P, P, P, P, I32, I32, P],
     "b200moe_permute_bwd": [P, I32, I64, I64, I32, P, P, P, P, P, P, P, I32, I32, P],
     "b200moe_combine": [P, I32, I64, I64, I32, P, P, P, P, I32, P, I32, I32, P],
@@ -64,6 +65,7 @@ _RESTYPES = {
     "b200moe_version": ctypes.c_char_p,
     "b200moe_last_error": ctypes.c_char_p,
     "b200moe_dispatch_plan_ws": SZ,
+    "b200moe_router_wgrad_ws": SZ,
 }
 
 _lib: Optional[ctypes.CDLL] = None
@@ -109,8 +111,9 @@ def check(rc: int, what: str) -> None:
 
 # kernels launched per entry point (bench.py reports the total as gpu_launches)
 _LAUNCHES = {"b200moe_dispatch_plan": 3}
+_LAUNCHES["b200moe_router_wgrad"] = 2
 _NO_LAUNCH = {"b200moe_version", "b200moe_last_error", "b200moe_device_check",
-              "b200moe_dispatch_plan_ws"}
+              "b200moe_dispatch_plan_ws", "b200moe_router_wgrad_ws"}
 _launches = 0
 
 
@@ -128,9 +131,52 @@ def launch_count() -> int:
     return _launches
 
 
+class Profile:
+    """Optional CUDA-event timing around every launching C-ABI call (bench)."""
+
+    def __init__(self):
+        self.on = False
+        self.events = []
+
+    def enable(self):
+        self.on, self.events = True, []
+
+    def disable(self):
+        self.on = False
+
+    def begin(self):
+        import torch
+
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def end(self, name, e0):
+        import torch
+
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self.events.append((name, e0, e1))
+
+    def collect(self):
+        """[(name, ms)] plus the span from the first start to the last end."""
+        import torch
+
+        torch.cuda.synchronize()
+        per = [(n, a.elapsed_time(b)) for n, a, b in self.events]
+        span = self.events[0][1].elapsed_time(self.events[-1][2]) if self.events else 0.0
+        return per, span
+
+
+PROFILE = Profile()
+
+
 def call(name: str, *args) -> None:
     lib = load()
+    e0 = PROFILE.begin() if PROFILE.on and name not in _NO_LAUNCH else None
     check(getattr(lib, name)(*args), name)
+    if e0 is not None:
+        PROFILE.end(name.replace("b200moe_", ""), e0)
     if name not in _NO_LAUNCH:
         n = _LAUNCHES.get(name, 1)
         if name in ("b200moe_permute", "b200moe_permute_bwd") and args[-5]:

@@ -28,7 +28,8 @@ int capacity_by_gate(const int64_t*, const int32_t*, const double*, const int64_
                      int, int64_t, uint8_t*, cudaStream_t);
 int router_bwd(const float*, const float*, const int32_t*, const float*, int64_t, int, int, int,
                int, float*, cudaStream_t);
-int router_wgrad(const void*, int, const float*, int64_t, int64_t, int, float*, cudaStream_t);
+size_t router_wgrad_ws_bytes(int64_t, int64_t, int);
+int router_wgrad(const void*, int, const float*, int64_t, int64_t, int, float*, void*, cudaStream_t);
 int permute(const void*, int, int64_t, int64_t, int, const int32_t*, const float*, void*,
             const int32_t*, const int32_t*, int, int64_t, cudaStream_t);
 int permute_bwd(const void*, int, int64_t, int64_t, int, const int32_t*, const float*, const void*,
@@ -140,14 +141,17 @@ int b200moe_router_bwd(const float* dgates, const float* scores, const int32_t* 
   return router_bwd(dgates, scores, topk_idx, gates, T, E, k, gate_fn, renorm, dz, S(stream));
 }
 
+size_t b200moe_router_wgrad_ws(int64_t T, int64_t H, int E) { return router_wgrad_ws_bytes(T, H, E); }
+
 int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz, int64_t T, int64_t H, int E,
-                         float* dw_g, void* stream) {
+                         float* dw_g, void* workspace, size_t workspace_bytes, void* stream) {
   REQUIRE(dt_ok(x_dtype) && H >= 1 && E >= 1 && T >= 0, "router_wgrad: bad args");
   REQUIRE(dw_g, "router_wgrad: null pointer");
   if (T == 0) return cudaMemsetAsync(dw_g, 0, H * E * sizeof(float), S(stream)) == cudaSuccess
                          ? B200MOE_OK : B200MOE_ELAUNCH;
-  REQUIRE(x && dz, "router_wgrad: null pointer");
-  return router_wgrad(x, x_dtype, dz, T, H, E, dw_g, S(stream));
+  REQUIRE(x && dz && workspace, "router_wgrad: null pointer");
+  REQUIRE(workspace_bytes >= router_wgrad_ws_bytes(T, H, E), "router_wgrad: workspace too small");
+  return router_wgrad(x, x_dtype, dz, T, H, E, dw_g, workspace, S(stream));
 }
 
 int b200moe_permute(const void* x, int dtype, int64_t T, int64_t H, int k, const int32_t* pair_row,

@@ -199,6 +199,100 @@ __global__ void __launch_bounds__(256) combine_kernel(
   }
 }
 
+// Vectorised combine (H % 8 == 0): each lane owns 8 consecutive columns per
+// step; the TPW x k row loads of a step are independent 16-byte loads (bf16)
+// so every warp keeps TPW*k requests in flight.
+template <typename Tin, typename Tout, int KMAX, int TPW>
+__global__ void __launch_bounds__(256) combine_vec_kernel(
+    const Tin* __restrict__ rows, int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_row,
+    const float* __restrict__ gates, const float* __restrict__ dz, const float* __restrict__ wgT,
+    int E, Tout* __restrict__ out, int accumulate) {
+  constexpr int V = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * TPW;
+  if (t0 >= Tn) return;
+  int32_t r[TPW][KMAX];
+  float w[TPW][KMAX];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      const int64_t t = t0 + i;
+      const bool ok = t < Tn && s < k;
+      r[i][s] = ok ? pair_row[t * k + s] : -1;
+      w[i][s] = (ok && gates) ? gates[t * k + s] : 1.f;
+    }
+  for (int64_t h = (int64_t)lane * V; h < H; h += 32 * V) {
+    float acc[TPW][V];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i)
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[i][j] = 0.f;
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (r[i][s] < 0) continue;
+        const Tin* p = rows + (int64_t)r[i][s] * H + h;
+        float v[V];
+        if (sizeof(Tin) == 2) {
+          Vec16<Tin> a;
+          a.raw = ld_nc_v4(p);
+#pragma unroll
+          for (int j = 0; j < V; ++j) v[j] = to_f32(a.v[j]);
+        } else {
+          Vec16<Tin> a, b;
+          a.raw = ld_nc_v4(p);
+          b.raw = ld_nc_v4(p + 4);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { v[j] = to_f32(a.v[j]); v[4 + j] = to_f32(b.v[j]); }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[i][j] = fmaf(w[i][s], v[j], acc[i][j]);
+      }
+    }
+    if (dz) {
+      for (int e = 0; e < E; ++e) {
+        const float4* wp = reinterpret_cast<const float4*>(wgT + (int64_t)e * H + h);
+        const float4 wa = __ldg(wp), wb = __ldg(wp + 1);
+        const float wv[V] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) {
+          const int64_t t = min(t0 + i, Tn - 1);
+          const float d = __ldg(dz + t * E + e);
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[i][j] = fmaf(d, wv[j], acc[i][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t t = t0 + i;
+      if (t >= Tn) break;
+      Tout* o = out + t * H + h;
+      if (accumulate) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[i][j] += to_f32(o[j]);
+      }
+      if (sizeof(Tout) == 2) {
+        Vec16<Tout> q;
+#pragma unroll
+        for (int j = 0; j < V; ++j) q.v[j] = from_f32<Tout>(acc[i][j]);
+        st_v4(o, q.raw);
+      } else {
+        Vec16<Tout> a, b;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          a.v[j] = from_f32<Tout>(acc[i][j]);
+          b.v[j] = from_f32<Tout>(acc[i][4 + j]);
+        }
+        st_v4(o, a.raw);
+        st_v4(o + 4, b.raw);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 #define KDISPATCH(k, MACRO)            \
   if (k <= 1) { MACRO(1); }            \
@@ -282,9 +376,15 @@ static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const i
                           int acc, cudaStream_t st) {
   constexpr int TPW = 4;
   const unsigned grid = (unsigned)ceil_div(ceil_div(Tn, TPW), 8);
+  if (H % 8 == 0) {
+#define CV(KM) combine_vec_kernel<Tin, Tout, KM, TPW><<<grid, 256, 0, st>>>(rows, Tn, H, k, pr, gates, dz, wgT, E, out, acc)
+    if (Tn > 0) { KDISPATCH(k, CV) }
+#undef CV
+  } else {
 #define CB(KM) combine_kernel<Tin, Tout, KM, TPW><<<grid, 256, 0, st>>>(rows, Tn, H, k, pr, gates, dz, wgT, E, out, acc)
-  if (Tn > 0) { KDISPATCH(k, CB) }
+    if (Tn > 0) { KDISPATCH(k, CB) }
 #undef CB
+  }
   B200MOE_CHECK_LAUNCH("combine");
   return B200MOE_OK;
 }

@@ -172,6 +172,25 @@ struct Tile {
   int bidx;           // weight/expert index for B (grouped-M)
 };
 
+// Panel rasterisation inside a group: PANEL_M m-tiles x all n-tiles, so the
+// ~148 tiles in flight share A k-slabs across n-tiles and B k-slabs across
+// the panel's m-tiles (keeps the concurrent working set in L2 even when one
+// operand of the group is larger than L2, e.g. wgrad of W1: M = 2F = 28672).
+constexpr int PANEL_M = 8;
+
+__device__ __forceinline__ void raster(int local, int mt, int nt, int& mb, int& nb) {
+  const int full = mt / PANEL_M;
+  if (local < full * PANEL_M * nt) {
+    const int pnl = local / (PANEL_M * nt), r = local % (PANEL_M * nt);
+    mb = pnl * PANEL_M + r % PANEL_M;
+    nb = r / PANEL_M;
+  } else {
+    const int rem = mt - full * PANEL_M, r = local - full * PANEL_M * nt;
+    mb = full * PANEL_M + r % rem;
+    nb = r / rem;
+  }
+}
+
 __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, int t) {
   // largest g with prefix[g] <= t
   int lo = 0, hi = p.G - 1;
@@ -184,9 +203,11 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
   r.g = lo;
   const int local = t - prefix[lo];
   const int64_t g0 = p.goff[lo], g1 = p.goff[lo + 1];
+  const int nt = (int)((p.N + BN - 1) / BN);
+  int mb, nb;
   if (!p.grouped_k) {
     const int mt = (int)((g1 - g0 + BM - 1) / BM);
-    const int nb = local / mt, mb = local % mt;
+    raster(local, mt, nt, mb, nb);
     r.m0 = g0 + (int64_t)mb * BM;
     r.m_end = g1;
     r.n0 = (int64_t)nb * BN;
@@ -195,7 +216,7 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
     r.bidx = p.gexp ? p.gexp[lo] : lo;
   } else {
     const int mt = (int)((p.M + BM - 1) / BM);
-    const int nb = local / mt, mb = local % mt;
+    raster(local, mt, nt, mb, nb);
     r.m0 = (int64_t)mb * BM;
     r.m_end = p.M;
     r.n0 = (int64_t)nb * BN;

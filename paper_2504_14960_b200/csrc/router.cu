@@ -58,6 +58,75 @@ __global__ void __launch_bounds__(256) logits_lane_h_kernel(const T* __restrict_
   }
 }
 
+// E in {4, 8} and H % 8 == 0: lanes own 8 consecutive hidden columns per
+// step (one 16-byte load per token for bf16), the matching 8 x E block of W_g
+// is read as float4 and reused for the warp's TPW tokens.  HBM-bound on x.
+template <typename T, int EP, int TPW>
+__global__ void __launch_bounds__(256) logits_vec_kernel(const T* __restrict__ x,
+                                                         const float* __restrict__ wg, int64_t Tn,
+                                                         int64_t H, float* __restrict__ logits) {
+  constexpr int V = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t t0 = warp * TPW;
+  if (t0 >= Tn) return;
+  float acc[TPW][EP];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int e = 0; e < EP; ++e) acc[i][e] = 0.f;
+  for (int64_t h = (int64_t)lane * V; h < H; h += 32 * V) {
+    float xv[TPW][V];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t t = min(t0 + i, Tn - 1);
+      const T* p = x + t * H + h;
+      if (sizeof(T) == 2) {
+        Vec16<T> v;
+        v.raw = ld_nc_v4(p);
+#pragma unroll
+        for (int j = 0; j < V; ++j) xv[i][j] = to_f32(v.v[j]);
+      } else {
+        Vec16<T> a, b;
+        a.raw = ld_nc_v4(p);
+        b.raw = ld_nc_v4(p + 4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xv[i][j] = to_f32(a.v[j]);
+          xv[i][4 + j] = to_f32(b.v[j]);
+        }
+      }
+    }
+    const float4* wrow = reinterpret_cast<const float4*>(wg + h * EP);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float w[EP];
+#pragma unroll
+      for (int q = 0; q < EP / 4; ++q) {
+        const float4 f = __ldg(wrow + j * (EP / 4) + q);
+        w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TPW; ++i)
+#pragma unroll
+        for (int e = 0; e < EP; ++e) acc[i][e] = fmaf(xv[i][j], w[e], acc[i][e]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int e = 0; e < EP; ++e) acc[i][e] = warp_sum(acc[i][e]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t t = t0 + i;
+      if (t >= Tn) break;
+#pragma unroll
+      for (int e = 0; e < EP; ++e) logits[t * EP + e] = acc[i][e];
+    }
+  }
+}
+
 // E > 32: lanes split the experts (NPL = E/32 per lane), x values are warp
 // broadcasts.
 template <typename T, int NPL, int TPW>
@@ -117,7 +186,15 @@ static int launch_logits(const T* x, const float* wg, int64_t Tn, int64_t H, int
     logits_lane_e_kernel<T, NPL, TPW><<<(unsigned)ceil_div(warps, wpb), threads, 0, st>>>( \
         x, wg, Tn, H, E, out);                                                       \
   }
-  if (E <= 4) LANE_H(4, 8)
+  if ((E == 8 || E == 4) && H % 8 == 0) {
+    constexpr int TPW = 4;
+    const int64_t warps = ceil_div(Tn, TPW);
+    if (E == 8)
+      logits_vec_kernel<T, 8, TPW><<<(unsigned)ceil_div(warps, wpb), threads, 0, st>>>(x, wg, Tn, H, out);
+    else
+      logits_vec_kernel<T, 4, TPW><<<(unsigned)ceil_div(warps, wpb), threads, 0, st>>>(x, wg, Tn, H, out);
+  }
+  else if (E <= 4) LANE_H(4, 8)
   else if (E <= 8) LANE_H(8, 8)
   else if (E <= 16) LANE_H(16, 4)
   else if (E <= 32) LANE_H(32, 2)
@@ -472,39 +549,65 @@ __global__ void __launch_bounds__(256) router_bwd_kernel(const float* __restrict
   }
 }
 
-// dW_g = x^T dz: one CTA per 32-wide hidden strip, warps stride the tokens,
-// then a fixed-order reduction over warps.
-template <typename T, int EB>
-__global__ void __launch_bounds__(256) router_wgrad_kernel(const T* __restrict__ x,
-                                                           const float* __restrict__ dz,
-                                                           int64_t Tn, int64_t H, int E,
-                                                           float* __restrict__ dwg) {
-  __shared__ float red[8][32][EB + 1];
+// dW_g = x^T dz, split over token chunks for parallelism and reduced in a
+// fixed order (deterministic).  Pass 1: CTA (64-wide hidden strip, chunk of
+// WG_CHUNK tokens) -> partial[chunk][h][e]; lane owns 2 adjacent h, warps
+// stride the chunk's tokens, warps reduce through smem.  Pass 2: sum chunks.
+constexpr int WG_CHUNK = 256;
+constexpr int WG_EB = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256) router_wgrad_partial_kernel(const T* __restrict__ x,
+                                                                   const float* __restrict__ dz,
+                                                                   int64_t Tn, int64_t H, int E,
+                                                                   float* __restrict__ part) {
+  __shared__ float red[8][64][WG_EB + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t h = (int64_t)blockIdx.x * 32 + lane;
-  for (int e0 = 0; e0 < E; e0 += EB) {
-    float acc[EB];
+  const int64_t h0 = (int64_t)blockIdx.x * 64 + 2 * lane;
+  const int64_t tb = (int64_t)blockIdx.y * WG_CHUNK;
+  const int64_t te = min(Tn, tb + WG_CHUNK);
+  for (int e0 = 0; e0 < E; e0 += WG_EB) {
+    float acc0[WG_EB], acc1[WG_EB];
 #pragma unroll
-    for (int j = 0; j < EB; ++j) acc[j] = 0.f;
-    for (int64_t t = w; t < Tn; t += 8) {
-      const float xv = (h < H) ? to_f32(x[t * H + h]) : 0.f;
+    for (int j = 0; j < WG_EB; ++j) acc0[j] = acc1[j] = 0.f;
+    for (int64_t t = tb + w; t < te; t += 8) {
+      const float x0 = (h0 < H) ? to_f32(x[t * H + h0]) : 0.f;
+      const float x1 = (h0 + 1 < H) ? to_f32(x[t * H + h0 + 1]) : 0.f;
       const float* d = dz + t * E + e0;
 #pragma unroll
-      for (int j = 0; j < EB; ++j)
-        if (e0 + j < E) acc[j] = fmaf(xv, __ldg(d + j), acc[j]);
+      for (int j = 0; j < WG_EB; ++j) {
+        const float dv = (e0 + j < E) ? __ldg(d + j) : 0.f;
+        acc0[j] = fmaf(x0, dv, acc0[j]);
+        acc1[j] = fmaf(x1, dv, acc1[j]);
+      }
     }
 #pragma unroll
-    for (int j = 0; j < EB; ++j) red[w][lane][j] = acc[j];
+    for (int j = 0; j < WG_EB; ++j) {
+      red[w][2 * lane][j] = acc0[j];
+      red[w][2 * lane + 1][j] = acc1[j];
+    }
     __syncthreads();
-    if (w == 0 && h < H) {
-#pragma unroll
-      for (int j = 0; j < EB; ++j) {
+    for (int i = threadIdx.x; i < 64 * WG_EB; i += 256) {
+      const int hh = i / WG_EB, j = i % WG_EB;
+      const int64_t h = (int64_t)blockIdx.x * 64 + hh;
+      if (h < H && e0 + j < E) {
         float s = 0.f;
-        for (int ww = 0; ww < 8; ++ww) s += red[ww][lane][j];
-        if (e0 + j < E) dwg[h * E + e0 + j] = s;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += red[ww][hh][j];
+        part[((int64_t)blockIdx.y * H + h) * E + e0 + j] = s;
       }
     }
     __syncthreads();
+  }
+}
+
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int64_t nchunks,
+                                           int64_t HE, float* __restrict__ dwg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < HE;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int64_t c = 0; c < nchunks; ++c) s += part[c * HE + i];
+    dwg[i] = s;
   }
 }
 
@@ -595,15 +698,24 @@ int router_bwd(const float* dgates, const float* scores, const int32_t* topk, co
   return B200MOE_OK;
 }
 
+size_t router_wgrad_ws_bytes(int64_t Tn, int64_t H, int E) {
+  return (size_t)ceil_div(Tn > 0 ? Tn : 1, WG_CHUNK) * H * E * sizeof(float);
+}
+
 int router_wgrad(const void* x, int dt, const float* dz, int64_t Tn, int64_t H, int E, float* dwg,
-                 cudaStream_t st) {
-  const unsigned grid = (unsigned)ceil_div(H, 32);
+                 void* ws, cudaStream_t st) {
+  const int64_t nch = ceil_div(Tn, WG_CHUNK);
+  float* part = static_cast<float*>(ws);
+  dim3 grid((unsigned)ceil_div(H, 64), (unsigned)nch);
   if (dt == B200MOE_BF16)
-    router_wgrad_kernel<__nv_bfloat16, 16><<<grid, 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(x), dz, Tn, H, E, dwg);
+    router_wgrad_partial_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), dz, Tn, H, E, part);
   else
-    router_wgrad_kernel<float, 16><<<grid, 256, 0, st>>>(static_cast<const float*>(x), dz, Tn, H,
-                                                         E, dwg);
+    router_wgrad_partial_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), dz, Tn,
+                                                             H, E, part);
+  const int64_t HE = H * E;
+  router_wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(HE, 256), 148 * 8), 256, 0, st>>>(
+      part, nch, HE, dwg);
   B200MOE_CHECK_LAUNCH("router_wgrad");
   return B200MOE_OK;
 }

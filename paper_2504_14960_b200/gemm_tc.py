@@ -69,40 +69,19 @@ def supports(**kw) -> bool:
     return (kw["a_sm"] == 1 and kw["b_sn"] == 1 and _ok8(kw["a_sk"], kw["b_sk"], kw["M"], kw["N"]))
 
 
-class _Profile:
-    """Optional CUDA-event timing of every tensor-core launch (bench roofline)."""
-
-    def __init__(self):
-        self.on = False
-        self.events = []
-
-    def enable(self):
-        self.on, self.events = True, []
-
-    def disable(self):
-        self.on = False
-
-    def collect(self):
-        torch.cuda.synchronize()
-        return [(name, a.elapsed_time(b)) for name, a, b in self.events]
-
-
-PROFILE = _Profile()
 _EPI_NAMES = {EPI_STORE: "store", EPI_SWIGLU_FWD: "swiglu_fwd", EPI_SWIGLU_BWD: "swiglu_bwd",
               EPI_ACT_FWD: "act_fwd", EPI_ACT_BWD: "act_bwd"}
 
 
 def _run(args: TcGemmArgs) -> None:
     lib = _lib()
-    if PROFILE.on:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+    prof = L.PROFILE
+    e0 = prof.begin() if prof.on else None
     L.check(lib.b200moe_gemm_tc(ctypes.byref(args), L.stream_ptr()), "b200moe_gemm_tc")
     L.note_launches(1)
-    if PROFILE.on:
-        e1.record()
+    if e0 is not None:
         kind = "wgrad" if args.grouped_dim == 1 else _EPI_NAMES[args.epilogue]
-        PROFILE.events.append((f"gemm_tc[{kind} N={args.N} K={args.K} M={args.M}]", e0, e1))
+        prof.end(f"gemm_tc[{kind} N={args.N} K={args.K} M={args.M}]", e0)
 
 
 def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg, ldc, group_off,

@@ -155,8 +155,10 @@ def router_wgrad(x: torch.Tensor, dz: torch.Tensor) -> torch.Tensor:
     T, H = x.shape
     E = dz.shape[1]
     dwg = torch.empty((H, E), dtype=torch.float32, device=x.device)
+    ws_bytes = int(L.load().b200moe_router_wgrad_ws(T, H, E))
+    ws = torch.empty((max(ws_bytes // 4, 1),), dtype=torch.float32, device=x.device)
     L.call("b200moe_router_wgrad", L.ptr(x), L.dtype_code(x.dtype), L.ptr(dz), T, H, E,
-           L.ptr(dwg), _sp())
+           L.ptr(dwg), L.ptr(ws), ctypes.c_size_t(ws.numel() * 4), _sp())
     return dwg
 
 
