@@ -57,6 +57,10 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.window = None  # (t0, t1) wall-clock of the timed region
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def start(self):
         try:
@@ -73,7 +77,7 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append([time.time()] + parts)
 
     def stop(self):
         if self.proc is None:
@@ -83,12 +87,19 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:  # noqa: BLE001
             self.proc.kill()
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
-        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        rows = self.rows
+        if self.window is not None:
+            inside = [r for r in rows if self.window[0] - 0.25 <= r[0] <= self.window[1] + 0.25]
+            rows = inside or rows
+        rows = [r[1:] for r in rows]
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in rows if r[1].replace(".", "").isdigit()), default=None)
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
         med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm)}
+        pw = sorted(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm),
+                "power_w_median": pw[len(pw) // 2] if pw else None}
 
 
 def peaks():
@@ -235,18 +246,28 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(1.0)  # let nvidia-smi start sampling before the timed region
     _lib.reset_launch_count()
     total_ms = 0.0
+    # every launch of the timed steps is bracketed by CUDA events on the
+    # launching stream (the roofline's per-kernel durations come from these)
+    per_step_launches = []
+    t_wall0 = time.time()
     for _ in range(a.steps):
         flush.zero_()  # evict L2 between timed steps (outside the events)
         barrier()
+        _lib.PROFILE.enable()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         step()
         e1.record()
         barrier()
+        per_step_launches.append(_lib.PROFILE.collect())
+        _lib.PROFILE.disable()
         total_ms += e0.elapsed_time(e1)
+    t_wall1 = time.time()
     launches = _lib.launch_count()
+    clocks.mark(t_wall0, t_wall1)
     clk = clocks.stop()
     ms = total_ms / a.steps
     if world > 1:
@@ -255,15 +276,13 @@ def main():
         ms = float(t)
     value = world * T / (ms / 1e3)
 
-    # ---- roofline: event-timed expert GEMM launches of one instrumented step
+    # ---- roofline: expert GEMM launches averaged over the timed steps
     burst, sustained, hbm, src = peaks()
-    flush.zero_()
-    torch.cuda.synchronize()
-    _lib.PROFILE.enable()
-    step()
-    torch.cuda.synchronize()
-    all_launches, span_ms = _lib.PROFILE.collect()
-    _lib.PROFILE.disable()
+    nsteps = len(per_step_launches)
+    n_launch = len(per_step_launches[0][0])
+    all_launches = [(per_step_launches[0][0][i][0],
+                     sum(s[0][i][1] for s in per_step_launches) / nsteps) for i in range(n_launch)]
+    span_ms = sum(s[1] for s in per_step_launches) / nsteps
     per_launch = [(n, m) for n, m in all_launches if n.startswith("gemm_tc")]
     other = {}
     for n, m in all_launches:

@@ -357,9 +357,9 @@ class NcclRankContext(RankContext):
         _check_group(self.rank, group)
         dev = self.world.device
         c = counts.to(dev, torch.int64).reshape(-1).contiguous()
-        out = torch.empty((len(group), c.numel()), dtype=torch.int64, device=dev)
+        out = torch.empty((len(group) * c.numel(),), dtype=torch.int64, device=dev)
         self.world.dist.all_gather_into_tensor(out, c, group=self.world.pg(group))
-        return out.cpu().numpy()
+        return out.cpu().numpy().reshape(len(group), c.numel())
 
     def p2p(self, group, sends, recvs):
         _check_group(self.rank, group)

@@ -1,0 +1,101 @@
+"""Multi-GPU parity check of the NCCL path (run under torchrun, >= 2 GPUs).
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port 29511 tests/dist_layer_check.py
+
+Every rank runs moe_forward/moe_backward over NCCL (one process per GPU) and,
+independently, the same topology with all ranks emulated on its own GPU
+(LocalWorld), then compares its rank's outputs and gradients.  Also checks
+the NCCL result against the CPU oracle fed the GPU logits.  Exits non-zero on
+any mismatch."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2504_14960_b200 as B  # noqa: E402
+from oracle import moe_oracle as O  # noqa: E402
+
+
+def rel(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+def cases(world):
+    # tp, cp, ep, etp, cf, drop_mode, act
+    if world == 2:
+        return [(1, 1, 2, 1, None, "subsequence", "swiglu"), (2, 1, 1, 2, None, "subsequence", "relu"),
+                (1, 2, 2, 1, 1.0, "fullsequence", "gelu"), (2, 1, 2, 1, 1.0, "subsequence", "swiglu")]
+    return [(1, 1, world, 1, None, "subsequence", "swiglu"), (2, 1, 2, 2, 1.0, "subsequence", "relu"),
+            (2, 2, 2, 2, 1.0, "fullsequence", "gelu"), (1, 2, world // 2, 2, None, "subsequence", "swiglu")]
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    E, k, H, F, seq = 8, 2, 128, 256, 256
+    failures = []
+    for ci, (tp, cp, ep, etp, cf, mode, act) in enumerate(cases(world)):
+        for dtype, tol in ((torch.float32, 1e-5), (torch.bfloat16, 2e-2)):
+            seed = 40 + ci
+            topo = B.ParallelTopology(world_size=world, tp=tp, cp=cp, ep=ep, etp=etp)
+            params = B.GatingParams(w_g=B.init_gating_matrix(H, E, seed), k=k, capacity_factor=cf,
+                                    drop_mode=mode)
+            weights = B.init_expert_weights(E, H, F, etp, seed, ep_size=ep, activation=act)
+            _, blocks = B.fabricate_token_blocks(topo, seq, topo.dp, H, seed, dtype=dtype, device=dev)
+            _, ups = B.fabricate_upstream(topo, seq, topo.dp, H, seed, dtype=dtype, device=dev)
+            nw = B.NcclWorld()
+            outs, fctx = B.moe_forward(blocks, weights, topo, params, nw, seq_len=seq)
+            res = B.moe_backward(ups, fctx)
+            lw = B.LocalWorld(world, dev)
+            outs2, fctx2 = B.moe_forward(blocks, weights, topo, params, lw, seq_len=seq)
+            res2 = B.moe_backward(ups, fctx2)
+            torch.cuda.synchronize()
+            tag = f"case{ci} {topo} cf={cf} {mode} {act} {dtype}"
+            d1 = fctx.per_rank[rank]["decision"]
+            d2 = fctx2.per_rank[rank]["decision"]
+            if not (torch.equal(d1.experts, d2.experts) and torch.equal(d1.kept, d2.kept)):
+                failures.append(f"{tag}: routing differs")
+            errs = {"y": rel(outs[rank], outs2[rank]), "dx": rel(res.input_grads[rank], res2.input_grads[rank]),
+                    "dwg": rel(res.w_g_grad, res2.w_g_grad)}
+            te, ee, de, pe = topo.moe_coords(rank)
+            if de == 0:
+                g1, g2 = res.expert_grads[(ee, te)], res2.expert_grads[(ee, te)]
+                errs["dw1"] = max(rel(a, b) for a, b in zip(g1[0], g2[0]))
+                errs["dw2"] = max(rel(a, b) for a, b in zip(g1[1], g2[1]))
+            # against the oracle on the same (rounded) inputs with the GPU logits (no relu: smooth)
+            if act != "relu" and mode == "subsequence":
+                xin = blocks[rank].values.double().cpu().numpy()
+                lg = fctx.per_rank[rank]["logits"].double().cpu().numpy()
+                full = B.init_expert_weights(E, H, F, 1, seed, activation=act)[(0, 0)]
+                exps = [O.Expert(np.asarray(a), np.asarray(b), act) for a, b in zip(full.w1, full.w2)]
+                cfg = O.LayerConfig(k=k, capacity_factor=cf)
+                yo, st = O.layer_forward(xin, lg, exps, cfg, positions=blocks[rank].positions.numpy())
+                errs["y_vs_oracle"] = O.rel_err(outs[rank].double().cpu().numpy(), yo)
+            worst = max(errs.values())
+            status = "OK" if worst < tol else "FAIL"
+            print(f"[rank {rank}] {status} {tag} " + " ".join(f"{n}={v:.2e}" for n, v in errs.items()),
+                  flush=True)
+            if worst >= tol:
+                failures.append(tag)
+    dist.barrier()
+    dist.destroy_process_group()
+    if failures:
+        print(f"[rank {rank}] FAILURES: {failures}", flush=True)
+        sys.exit(1)
+    print(f"[rank {rank}] all multi-GPU parity checks passed", flush=True)
+
+
+if __name__ == "__main__":
+    main()
