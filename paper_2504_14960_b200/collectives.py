@@ -243,6 +243,16 @@ class RankContext:
             recvs: List[Tuple[int, torch.Tensor]]) -> None:
         raise NotImplementedError
 
+    def a2a_single(self, group: Group, send: torch.Tensor, send_splits: Sequence[int],
+                   recv: torch.Tensor, recv_splits: Sequence[int]) -> None:
+        """Rows [sum(send_splits[:j]), +send_splits[j]) of ``send`` go to
+        member j; ``recv`` receives members' rows in ascending member order."""
+        so = np.concatenate(([0], np.cumsum(send_splits))).astype(np.int64)
+        ro = np.concatenate(([0], np.cumsum(recv_splits))).astype(np.int64)
+        sends = [(group[j], send[so[j]:so[j + 1]]) for j in range(len(group))]
+        recvs = [(group[j], recv[ro[j]:ro[j + 1]]) for j in range(len(group))]
+        self.p2p(group, sends, recvs)
+
     def gather_counts(self, group: Group, counts: torch.Tensor) -> np.ndarray:
         """[len(group), n] int64 on the host: row i = member i's vector."""
         raise NotImplementedError
@@ -355,11 +365,17 @@ class NcclRankContext(RankContext):
 
     def gather_counts(self, group, counts):
         _check_group(self.rank, group)
+        from . import _lib
+
         dev = self.world.device
+        e0 = _lib.PROFILE.begin() if _lib.PROFILE.on else None
         c = counts.to(dev, torch.int64).reshape(-1).contiguous()
         out = torch.empty((len(group) * c.numel(),), dtype=torch.int64, device=dev)
         self.world.dist.all_gather_into_tensor(out, c, group=self.world.pg(group))
-        return out.cpu().numpy().reshape(len(group), c.numel())
+        host = out.cpu().numpy().reshape(len(group), c.numel())
+        if e0 is not None:
+            _lib.PROFILE.end("nccl:count_allgather+sync", e0)
+        return host
 
     def p2p(self, group, sends, recvs):
         _check_group(self.rank, group)
@@ -382,6 +398,21 @@ class NcclRankContext(RankContext):
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+
+    def a2a_single(self, group, send, send_splits, recv, recv_splits):
+        from . import _lib
+
+        _check_group(self.rank, group)
+        ns, nr = int(sum(send_splits)), int(sum(recv_splits))
+        if len(group) == 1:
+            if ns:
+                recv[:nr].copy_(send[:ns])
+            return
+        e0 = _lib.PROFILE.begin() if _lib.PROFILE.on else None
+        self.world.dist.all_to_all_single(recv[:nr], send[:ns], [int(v) for v in recv_splits],
+                                          [int(v) for v in send_splits], group=self.world.pg(group))
+        if e0 is not None:
+            _lib.PROFILE.end(f"nccl:a2a[{ns}->{nr} rows]", e0)
 
     def _all_reduce(self, group, values, op):
         _check_group(self.rank, group)

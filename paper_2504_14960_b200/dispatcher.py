@@ -229,47 +229,51 @@ class LayerGroups:
 
 
 @dataclass
-class ExchangeLayout:
-    """Host-side description of one rank's variable-count exchange, computed
-    from the all-gathered count vectors (the one host sync of the layer)."""
+class ExchangePlan:
+    """Host-side sizes of one rank's EP all-to-all-v and ETP gather, computed
+    from the all-gathered per-expert counts (the one host sync of the layer).
 
-    send_off: np.ndarray  # [ep, L] row offset of chunk (dest, le) in send order
-    send_cnt: np.ndarray  # [ep, L]
-    recv_off: np.ndarray  # [ep, L] row of chunk (src, le) in MY padded block
-    recv_cnt: np.ndarray  # [ep, L]
-    block_rows: np.ndarray  # [etp] padded rows of each ETP member's block
-    member_le_off: np.ndarray  # [etp, L+1] padded offsets of le segments inside member blocks
-    member_le_cnt: np.ndarray  # [etp, L] real rows of each le segment
+    A rank's send buffer is its padded per-global-expert layout; the block it
+    receives from sender s is s's chunks for this rank's local experts, each
+    padded to ``align`` rows.  With ETP the gathered buffer is member-major."""
+
+    send_splits: List[int]  # rows to each EP peer (padded)
+    recv_splits: List[int]  # rows from each EP peer (padded)
+    recv_padded: np.ndarray  # [ep, L] padded rows of (sender, local expert) segments
+    recv_counts: np.ndarray  # [ep, L] real rows of those segments
+    block_off: np.ndarray  # [etp+1] member block offsets in the gathered buffer
+    group_off: List[int]  # [G+1] GEMM group offsets (member, sender, le) in the gathered buffer
+    group_expert: List[int]  # [G] local expert of each group
 
 
-def exchange_layout(all_send_counts: np.ndarray, ep_pos: int, etp_all_recv: np.ndarray,
-                    L_: int, align: int = ALIGN) -> ExchangeLayout:
+def _pad(c, align):
+    return (np.asarray(c, dtype=np.int64) + align - 1) // align * align
+
+
+def exchange_plan(counts: np.ndarray, ep_pos: int, L_: int, etp_recv: Optional[np.ndarray] = None,
+                  align: int = ALIGN) -> ExchangePlan:
     """Pure host arithmetic (tested on CPU).
 
-    all_send_counts [ep, ep*L]: row s = EP member s's per-global-expert counts
-    (within this EP group).  etp_all_recv [etp, L]: every ETP member's total
-    received rows per local expert."""
-    ep = all_send_counts.shape[0]
-    mine = all_send_counts[ep_pos].reshape(ep, L_)
-    send_off = np.concatenate(([0], np.cumsum(mine.reshape(-1))))[:-1].reshape(ep, L_)
-    recv_cnt = all_send_counts[:, ep_pos * L_:(ep_pos + 1) * L_]  # [src, le]
-    le_tot = recv_cnt.sum(axis=0)
-    padded = (le_tot + align - 1) // align * align
-    le_base = np.concatenate(([0], np.cumsum(padded)))
-    recv_off = le_base[None, :-1] + np.concatenate(
-        [np.zeros((1, L_), dtype=np.int64), np.cumsum(recv_cnt, axis=0)[:-1]], axis=0)
-    etp = etp_all_recv.shape[0]
-    m_pad = (etp_all_recv + align - 1) // align * align
-    member_le_off = np.concatenate([np.zeros((etp, 1), dtype=np.int64), np.cumsum(m_pad, axis=1)], axis=1)
-    return ExchangeLayout(send_off.astype(np.int64), mine.astype(np.int64), recv_off.astype(np.int64),
-                          recv_cnt.astype(np.int64), member_le_off[:, -1].astype(np.int64),
-                          member_le_off.astype(np.int64), etp_all_recv.astype(np.int64))
-
-
-def _zero_pads(buf: torch.Tensor, starts: List[int], ends: List[int]) -> None:
-    for s, e in zip(starts, ends):
-        if e > s:
-            buf[s:e].zero_()
+    counts [ep, ep*L]: row s = EP member s's kept pairs per global expert of
+    this EP group.  etp_recv [etp, ep*L] (None when ETP = 1): every ETP
+    member's ``recv_padded`` flattened, in ETP-rank order."""
+    counts = np.asarray(counts, dtype=np.int64)
+    ep = counts.shape[0]
+    padded = _pad(counts, align)
+    send_splits = [int(padded[ep_pos, d * L_:(d + 1) * L_].sum()) for d in range(ep)]
+    recv_padded = padded[:, ep_pos * L_:(ep_pos + 1) * L_]
+    recv_counts = counts[:, ep_pos * L_:(ep_pos + 1) * L_]
+    recv_splits = [int(recv_padded[s].sum()) for s in range(ep)]
+    members = [recv_padded.reshape(-1)] if etp_recv is None else [np.asarray(r).reshape(-1) for r in etp_recv]
+    block_off = np.concatenate(([0], np.cumsum([int(m.sum()) for m in members]))).astype(np.int64)
+    group_off, group_expert = [], []
+    for mi, m in enumerate(members):
+        off = block_off[mi] + np.concatenate(([0], np.cumsum(m)))[:-1]
+        group_off.extend(int(o) for o in off)
+        group_expert.extend(i % L_ for i in range(m.size))
+    group_off.append(int(block_off[-1]))
+    return ExchangePlan(send_splits, recv_splits, recv_padded, recv_counts, block_off, group_off,
+                        group_expert)
 
 
 class RankLayer:
@@ -331,58 +335,41 @@ class RankLayer:
             return out, saved
         return self._forward_exchange(ctx, x, dec, plan, saved)
 
-    def _layout(self, ctx, plan) -> ExchangeLayout:
+    # ------------------------------------------------------- EP / ETP exchange
+    # Rows are permuted straight into the padded per-global-expert layout,
+    # which is destination-major with every (dest, local expert) chunk padded
+    # to ALIGN rows.  One all_to_all_single per direction then lands them as
+    # (sender, local expert) segments that are already GEMM-aligned, so the
+    # receive side needs no regroup copy and the return trip restores the
+    # sender's layout exactly (combine reads it through gemm_row).
+    def _exchange_plan(self, ctx, plan) -> ExchangePlan:
         g = self.g
-        all_send = ctx.gather_counts(g.ep, plan.counts.to(torch.int64))  # [ep, E]
+        counts = ctx.gather_counts(g.ep, plan.counts.to(torch.int64))  # [ep, E] host (one sync)
         ep_pos = g.ep.index(self.rank)
-        # this EP group only routes to experts of its own EP coordinate set: E = ep*L
-        lay0 = exchange_layout(all_send, ep_pos, np.zeros((1, self.L), dtype=np.int64), self.L)
-        my_recv_tot = lay0.recv_cnt.sum(axis=0)
+        mine = exchange_plan(counts, ep_pos, self.L, None, ALIGN)
         if len(g.etp) > 1:
-            etp_all = ctx.gather_counts(g.etp, torch.as_tensor(my_recv_tot))
-        else:
-            etp_all = my_recv_tot[None, :]
-        return exchange_layout(all_send, ep_pos, etp_all, self.L)
+            etp_recv = ctx.gather_counts(g.etp, torch.as_tensor(mine.recv_padded.reshape(-1)))
+            return exchange_plan(counts, ep_pos, self.L, etp_recv, ALIGN)
+        return mine
 
-    def _a2a(self, ctx, lay: ExchangeLayout, src: torch.Tensor, dst: torch.Tensor, forward: bool):
-        """forward: send-order rows -> my padded block; else the reverse."""
-        g = self.g
-        sends, recvs = [], []
-        for j, peer in enumerate(g.ep):
-            for le in range(self.L):
-                so, sc = int(lay.send_off[j, le]), int(lay.send_cnt[j, le])
-                ro, rc = int(lay.recv_off[j, le]), int(lay.recv_cnt[j, le])
-                if forward:
-                    sends.append((peer, src[so:so + sc]))
-                    recvs.append((peer, dst[ro:ro + rc]))
-                else:
-                    sends.append((peer, src[ro:ro + rc]))
-                    recvs.append((peer, dst[so:so + sc]))
-        ctx.p2p(g.ep, sends, recvs)
-
-    def _member_blocks(self, lay):
-        off = np.concatenate(([0], np.cumsum(lay.block_rows)))
-        return off
-
-    def _gather_blocks(self, ctx, lay, mine: torch.Tensor, width: int) -> torch.Tensor:
+    def _gather_blocks(self, ctx, xp: ExchangePlan, mine: torch.Tensor) -> torch.Tensor:
         g = self.g
         if len(g.etp) == 1:
             return mine
-        off = self._member_blocks(lay)
-        full = torch.empty((int(off[-1]), width), dtype=mine.dtype, device=mine.device)
-        me = g.etp.index(self.rank)
+        off = xp.block_off
+        full = torch.empty((int(off[-1]), mine.shape[1]), dtype=mine.dtype, device=mine.device)
         sends = [(r, mine) for r in g.etp]
         recvs = [(g.etp[m], full[off[m]:off[m + 1]]) for m in range(len(g.etp))]
         ctx.p2p(g.etp, sends, recvs)
         return full
 
-    def _reduce_blocks(self, ctx, lay, full: torch.Tensor) -> torch.Tensor:
+    def _reduce_blocks(self, ctx, xp: ExchangePlan, full: torch.Tensor) -> torch.Tensor:
         g = self.g
         if len(g.etp) == 1:
             return full
-        off = self._member_blocks(lay)
+        off = xp.block_off
         me = g.etp.index(self.rank)
-        n_me = int(lay.block_rows[me])
+        n_me = int(off[me + 1] - off[me])
         parts = [torch.empty((n_me, full.shape[1]), dtype=full.dtype, device=full.device)
                  for _ in g.etp]
         sends = [(g.etp[m], full[off[m]:off[m + 1]]) for m in range(len(g.etp))]
@@ -393,46 +380,28 @@ class RankLayer:
             acc += q.float()
         return acc.to(full.dtype)
 
-    def _groups_dev(self, lay):
-        etp = len(self.g.etp)
-        off = self._member_blocks(lay)
-        goff = []
-        for m in range(etp):
-            goff.extend((off[m] + lay.member_le_off[m, :-1]).tolist())
-        goff.append(int(off[-1]))
-        gexp = [le for _ in range(etp) for le in range(self.L)]
-        dev = self.device
-        return (torch.tensor(goff, dtype=torch.int32, device=dev),
-                torch.tensor(gexp, dtype=torch.int32, device=dev), len(gexp))
-
-    def _pad_ranges(self, lay, me):
-        starts, ends = [], []
-        for le in range(self.L):
-            base = int(lay.member_le_off[me, le])
-            starts.append(base + int(lay.member_le_cnt[me, le]))
-            ends.append(int(lay.member_le_off[me, le + 1]))
-        return starts, ends
-
     def _forward_exchange(self, ctx, x, dec, plan, saved):
         T, H = x.shape
-        lay = self._layout(ctx, plan)
-        n_send = int(lay.send_cnt.sum())
-        send = K.permute(x, plan.send_row, max(n_send, 1))
-        me_etp = self.g.etp.index(self.rank)
-        my_rows = int(lay.block_rows[me_etp])
-        block = torch.empty((max(my_rows, 1), H), dtype=x.dtype, device=x.device)
-        self._a2a(ctx, lay, send, block, forward=True)
-        _zero_pads(block, *self._pad_ranges(lay, me_etp))
-        xp = self._gather_blocks(ctx, lay, block[:my_rows], H)
-        goff, gexp, G = self._groups_dev(lay)
+        E = self.E
+        xpl = self._exchange_plan(ctx, plan)
+        R_send = int(sum(xpl.send_splits))
+        xs = K.permute(x, plan.gemm_row, max(R_send, 1), poffsets=plan.poffsets, counts=plan.counts, E=E)
+        R_recv = int(sum(xpl.recv_splits))
+        xr = torch.empty((max(R_recv, 1), H), dtype=x.dtype, device=x.device)
+        ctx.a2a_single(self.g.ep, xs, xpl.send_splits, xr, xpl.recv_splits)
+        xp = self._gather_blocks(ctx, xpl, xr[:R_recv])
+        # pinned + non_blocking: a pageable H2D copy would stall the host on the stream
+        goff = torch.tensor(xpl.group_off, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        gexp = torch.tensor(xpl.group_expert, dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        G = len(xpl.group_expert)
         R = xp.shape[0]
         pre, h, y = X.ffn_forward(xp, goff, G, gexp, self.pk, R)
-        y_mine = self._reduce_blocks(ctx, lay, y)
-        y_send = torch.empty((max(n_send, 1), H), dtype=x.dtype, device=x.device)
-        self._a2a(ctx, lay, y_mine, y_send, forward=False)
-        out = K.combine(y_send, plan.send_row, T, gates=dec.gates)
-        saved.update(xp=xp, pre=pre, h=h, y=y_send, goff=goff, G=G, gexp=gexp, R=R, lay=lay,
-                     pair_row=plan.send_row, n_send=n_send, my_rows=my_rows)
+        y_mine = self._reduce_blocks(ctx, xpl, y)
+        ys = torch.empty((max(R_send, 1), H), dtype=x.dtype, device=x.device)
+        ctx.a2a_single(self.g.ep, y_mine, xpl.recv_splits, ys, xpl.send_splits)
+        out = K.combine(ys, plan.gemm_row, T, gates=dec.gates)
+        saved.update(xp=xp, pre=pre, h=h, y=ys, goff=goff, G=G, gexp=gexp, R=R, xpl=xpl,
+                     pair_row=plan.gemm_row, R_send=R_send, R_recv=R_recv)
         return out, saved
 
     # ---------------------------------------------------------------- bwd
@@ -453,22 +422,20 @@ class RankLayer:
             dw1p, dw2p = dw1g, dw2g
             rows = dxp
         else:
-            lay = sv["lay"]
-            dy_send, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"])
-            me_etp = self.g.etp.index(self.rank)
-            my_rows = sv["my_rows"]
-            block = torch.empty((max(my_rows, 1), H), dtype=u.dtype, device=u.device)
-            self._a2a(ctx, lay, dy_send, block, forward=True)
-            _zero_pads(block, *self._pad_ranges(lay, me_etp))
-            dyp = self._gather_blocks(ctx, lay, block[:my_rows], H)
+            xpl = sv["xpl"]
+            dys, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"], poffsets=plan.poffsets,
+                                        counts=plan.counts, E=E)
+            dyr = torch.empty((max(sv["R_recv"], 1), H), dtype=u.dtype, device=u.device)
+            ctx.a2a_single(self.g.ep, dys, xpl.send_splits, dyr, xpl.recv_splits)
+            dyp = self._gather_blocks(ctx, xpl, dyr[:sv["R_recv"]])
             dxp, dw1g, dw2g = X.ffn_backward(dyp, sv["xp"], sv["pre"], sv["h"], sv["goff"], sv["G"],
                                             sv["gexp"], self.pk, sv["R"])
-            # groups (member, le) -> local experts, summed in member order
-            dw1p = dw1g.reshape(len(self.g.etp), self.L, *dw1g.shape[1:]).sum(0)
-            dw2p = dw2g.reshape(len(self.g.etp), self.L, *dw2g.shape[1:]).sum(0)
-            dx_mine = self._reduce_blocks(ctx, lay, dxp)
-            rows = torch.empty((max(sv["n_send"], 1), H), dtype=u.dtype, device=u.device)
-            self._a2a(ctx, lay, dx_mine, rows, forward=False)
+            # groups (member, sender, le) -> local experts, summed in group order
+            dw1p = dw1g.reshape(-1, self.L, *dw1g.shape[1:]).sum(0)
+            dw2p = dw2g.reshape(-1, self.L, *dw2g.shape[1:]).sum(0)
+            dx_mine = self._reduce_blocks(ctx, xpl, dxp)
+            rows = torch.empty((max(sv["R_send"], 1), H), dtype=u.dtype, device=u.device)
+            ctx.a2a_single(self.g.ep, dx_mine, xpl.recv_splits, rows, xpl.send_splits)
         dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
                           p.renormalize_topk)
         dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT)

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from paper_2504_14960_b200 import _lib, errors
-from paper_2504_14960_b200.dispatcher import exchange_layout, token_partition
+from paper_2504_14960_b200.dispatcher import exchange_plan, token_partition
 from paper_2504_14960_b200.topology import (ParallelTopology, check_pp_consistency,
                                             generate_parallel_groups, sequence_group)
 
@@ -61,18 +61,23 @@ def test_topology_validation_errors():
         token_partition(ParallelTopology(world_size=4, tp=4), seq_len=6, batch=1)
 
 
-def test_exchange_layout_arithmetic():
+def test_exchange_plan_arithmetic():
     # EP group of 2, L=2 local experts: member s's counts over 4 global experts
-    all_send = np.array([[3, 1, 2, 0], [1, 4, 0, 5]])
-    lay = exchange_layout(all_send, 1, np.array([[2, 5]]), 2, align=4)
-    # rank at EP position 1 hosts experts 2, 3: receives [2,0] from member 0, [0,5] from 1
-    np.testing.assert_array_equal(lay.recv_cnt, [[2, 0], [0, 5]])
-    np.testing.assert_array_equal(lay.send_off, [[0, 1], [5, 5]])
-    np.testing.assert_array_equal(lay.send_cnt, [[1, 4], [0, 5]])
-    # le segments padded to 4: le0 has 2 rows -> [0,4), le1 has 5 -> [4, 12)
-    np.testing.assert_array_equal(lay.recv_off, [[0, 4], [2, 4]])
-    np.testing.assert_array_equal(lay.member_le_off, [[0, 4, 12]])
-    assert lay.block_rows.tolist() == [12]
+    counts = np.array([[3, 1, 2, 0], [1, 4, 0, 5]])
+    xp = exchange_plan(counts, 1, 2, None, align=4)
+    # rank at EP position 1 (experts 2, 3) sends its padded chunks: to 0 -> pad(1)+pad(4) = 4+4,
+    # to itself -> pad(0)+pad(5) = 0+8
+    assert xp.send_splits == [8, 8]
+    # receives from 0: pad(2)+pad(0) = 4, from 1: pad(0)+pad(5) = 8
+    assert xp.recv_splits == [4, 8]
+    np.testing.assert_array_equal(xp.recv_counts, [[2, 0], [0, 5]])
+    assert xp.group_off == [0, 4, 4, 4, 12]
+    assert xp.group_expert == [0, 1, 0, 1]
+    # ETP of 2: member blocks concatenated, groups member-major
+    xp2 = exchange_plan(counts, 1, 2, np.array([[4, 0, 0, 8], [8, 4, 0, 0]]), align=4)
+    assert xp2.block_off.tolist() == [0, 12, 24]
+    assert xp2.group_off == [0, 4, 4, 4, 12, 20, 24, 24, 24]
+    assert xp2.group_expert == [0, 1, 0, 1, 0, 1, 0, 1]
 
 
 def test_library_exports_every_declared_symbol():

@@ -106,36 +106,29 @@ def prog_gather_reduce(rank, world):
 
 
 def prog_layer_exchange(rank, world):
-    """The layer's count exchange + P2P into the expert-major padded layout."""
+    """The layer's count exchange + all_to_all_single of the padded
+    per-expert layout: (sender, local expert) segments land aligned."""
     from paper_2504_14960_b200.collectives import NcclWorld, NcclRankContext
-    from paper_2504_14960_b200.dispatcher import exchange_layout
+    from paper_2504_14960_b200.dispatcher import exchange_plan
 
     nw = NcclWorld()
     nw.setup_groups([[tuple(range(world))]])
     ctx = NcclRankContext(nw)
-    L_ = 2
+    L_, A = 2, 4
     E = world * L_
     rng = np.random.default_rng(100 + rank)
-    counts = rng.integers(0, 5, size=E)  # my rows per global expert (send order)
-    all_send = ctx.gather_counts(tuple(range(world)), torch.as_tensor(counts))
-    lay = exchange_layout(all_send, rank, all_send[:, rank * L_:(rank + 1) * L_].sum(0)[None, :], L_,
-                          align=4)
-    # rows carry (src rank, global expert, ordinal) so placement is checkable
+    counts = rng.integers(0, 7, size=E)  # my kept pairs per global expert
+    all_counts = ctx.gather_counts(tuple(range(world)), torch.as_tensor(counts))
+    xp = exchange_plan(all_counts, rank, L_, None, align=A)
+    # padded send layout; rows carry (src rank, global expert, ordinal), pads = -1
     send = []
     for e in range(E):
-        for i in range(counts[e]):
-            send.append([rank, e, i])
+        send += [[rank, e, i] for i in range(counts[e])]
+        send += [[-1, -1, -1]] * int((-counts[e]) % A)
     send = torch.tensor(send, dtype=torch.float32).reshape(-1, 3)
-    block = torch.full((int(lay.block_rows[0]), 3), -1.0)
-    sends, recvs = [], []
-    for j in range(world):
-        for le in range(L_):
-            so, sc = int(lay.send_off[j, le]), int(lay.send_cnt[j, le])
-            ro, rc = int(lay.recv_off[j, le]), int(lay.recv_cnt[j, le])
-            sends.append((j, send[so:so + sc]))
-            recvs.append((j, block[ro:ro + rc]))
-    ctx.p2p(tuple(range(world)), sends, recvs)
-    return all_send.tolist(), block.tolist(), lay.member_le_off.tolist()
+    recv = torch.full((sum(xp.recv_splits), 3), -2.0)
+    ctx.a2a_single(tuple(range(world)), send, xp.send_splits, recv, xp.recv_splits)
+    return all_counts.tolist(), recv.tolist(), xp.group_off, xp.group_expert
 
 
 # ---------------------------------------------------------------- tests
@@ -166,18 +159,22 @@ def test_all_gather_reduce_scatter_all_reduce():
     assert out[0][2] == full[:2] and out[1][2] == full[2:]
 
 
-def test_layer_exchange_lands_expert_major_sender_minor():
-    out = _run("prog_layer_exchange")
-    world, L_ = 2, 2
-    all_send = np.array(out[0][0])
+@pytest.mark.parametrize("world", [2, 3])
+def test_layer_exchange_lands_aligned_sender_expert_segments(world):
+    out = _run("prog_layer_exchange", world)
+    L_ = 2
+    counts = np.array(out[0][0])
     for me in range(world):
-        _, block, mle = out[me]
-        block = np.array(block)
-        for le in range(L_):
-            e = me * L_ + le
-            base = mle[0][le]
-            rows = block[base:base + int(all_send[:, e].sum())]
-            want = [[s, e, i] for s in range(world) for i in range(all_send[s, e])]
-            assert rows.tolist() == want, (me, le)
-            pad = block[base + len(want):mle[0][le + 1]]
-            assert (pad == -1).all()
+        _, recv, goff, gexp = out[me]
+        recv = np.array(recv)
+        assert goff[-1] == recv.shape[0]
+        g = 0
+        for s in range(world):
+            for le in range(L_):
+                e = me * L_ + le
+                assert gexp[g] == le and goff[g] % 4 == 0
+                seg = recv[goff[g]:goff[g + 1]]
+                want = [[s, e, i] for i in range(counts[s, e])]
+                assert seg[:len(want)].tolist() == want, (me, s, le)
+                assert (seg[len(want):] == -1).all()
+                g += 1
