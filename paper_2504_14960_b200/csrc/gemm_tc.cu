@@ -60,6 +60,7 @@ struct Params {
   int64_t ldh;
   const void* PRE; // pre-activation input for *_BWD epilogues
   int64_t ldpre;
+  int panel_m;     // raster panel height in m-tiles
 };
 
 // ------------------------------------------------------------------ PTX
@@ -172,21 +173,21 @@ struct Tile {
   int bidx;           // weight/expert index for B (grouped-M)
 };
 
-// Panel rasterisation inside a group: PANEL_M m-tiles x all n-tiles, so the
-// ~148 tiles in flight share A k-slabs across n-tiles and B k-slabs across
-// the panel's m-tiles (keeps the concurrent working set in L2 even when one
-// operand of the group is larger than L2, e.g. wgrad of W1: M = 2F = 28672).
-constexpr int PANEL_M = 8;
-
-__device__ __forceinline__ void raster(int local, int mt, int nt, int& mb, int& nb) {
-  const int full = mt / PANEL_M;
-  if (local < full * PANEL_M * nt) {
-    const int pnl = local / (PANEL_M * nt), r = local % (PANEL_M * nt);
-    mb = pnl * PANEL_M + r % PANEL_M;
-    nb = r / PANEL_M;
+// Panel rasterisation inside a group: panels of `pm` m-tiles x all n-tiles,
+// m fastest inside a panel.  pm is chosen on the host per GEMM (see
+// choose_panel): pm >= mt keeps the whole A operand of a group L2-resident
+// while B streams once; a small pm keeps B resident while A streams once;
+// when neither fits L2, pm ~ sqrt(148 * BN / BM) balances the k-slab reuse of
+// the ~148 concurrent tiles.
+__device__ __forceinline__ void raster(int local, int mt, int nt, int pm, int& mb, int& nb) {
+  const int full = mt / pm;
+  if (local < full * pm * nt) {
+    const int pnl = local / (pm * nt), r = local % (pm * nt);
+    mb = pnl * pm + r % pm;
+    nb = r / pm;
   } else {
-    const int rem = mt - full * PANEL_M, r = local - full * PANEL_M * nt;
-    mb = full * PANEL_M + r % rem;
+    const int rem = mt - full * pm, r = local - full * pm * nt;
+    mb = full * pm + r % rem;
     nb = r / rem;
   }
 }
@@ -207,7 +208,7 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
   int mb, nb;
   if (!p.grouped_k) {
     const int mt = (int)((g1 - g0 + BM - 1) / BM);
-    raster(local, mt, nt, mb, nb);
+    raster(local, mt, nt, p.panel_m, mb, nb);
     r.m0 = g0 + (int64_t)mb * BM;
     r.m_end = g1;
     r.n0 = (int64_t)nb * BN;
@@ -216,7 +217,7 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
     r.bidx = p.gexp ? p.gexp[lo] : lo;
   } else {
     const int mt = (int)((p.M + BM - 1) / BM);
-    raster(local, mt, nt, mb, nb);
+    raster(local, mt, nt, p.panel_m, mb, nb);
     r.m0 = (int64_t)mb * BM;
     r.m_end = p.M;
     r.n0 = (int64_t)nb * BN;
@@ -602,6 +603,20 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, u
   return B200MOE_OK;
 }
 
+// Raster policy from the typical per-group operand footprints (bf16 bytes).
+static int choose_panel(const b200moe_tc_gemm_args* a) {
+  using namespace tc;
+  const double G = a->G > 0 ? a->G : 1;
+  const double Mg = a->grouped_dim == 0 ? (double)a->a_rows / G : (double)a->M;
+  const double Kg = a->grouped_dim == 0 ? (double)a->K : (double)a->a_rows / G;
+  const double a_bytes = Mg * Kg * 2, b_bytes = (double)a->N * Kg * 2;
+  const double resident = 40.0 * 1024 * 1024;  // comfortably inside the 126 MB L2
+  const int mt = (int)((Mg + BM - 1) / BM);
+  if (a_bytes <= resident) return mt > 0 ? mt : 1;  // A resident, B streamed once
+  if (b_bytes <= resident) return 8;                 // B resident, A streamed once
+  return 16;                                         // balanced k-slab reuse
+}
+
 int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   using namespace tc;
   if (a->G < 1 || a->G > MAX_G) {
@@ -660,6 +675,7 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.ldh = a->ldh;
   p.PRE = a->PRE;
   p.ldpre = a->ldpre;
+  p.panel_m = choose_panel(a);
 
   auto kern = a_mn ? (b_mn ? gemm_tc_kernel<true, true> : gemm_tc_kernel<true, false>)
                     : (b_mn ? gemm_tc_kernel<false, true> : gemm_tc_kernel<false, false>);

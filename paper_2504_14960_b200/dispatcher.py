@@ -216,6 +216,8 @@ class BackwardResult:
     input_grads: List[Optional[torch.Tensor]]
     w_g_grad: torch.Tensor
     expert_grads: Dict[Tuple[int, int], Tuple[List[torch.Tensor], List[torch.Tensor]]]
+    # builder-defined shared expert: (dW1 [H, 2F_s], dW2 [F_s, H]) summed over ranks
+    shared_grads: Optional[Tuple[torch.Tensor, torch.Tensor]] = None
 
 
 # =========================================================== rank program
@@ -280,7 +282,9 @@ class RankLayer:
     """Everything one rank needs to run the layer forward and backward."""
 
     def __init__(self, params: GatingParams, weights: X.ExpertWeights, topology: ParallelTopology,
-                 groups: LayerGroups, rank: int, dtype, device, seq_len=None, check=False):
+                 groups: LayerGroups, rank: int, dtype, device, seq_len=None, check=False,
+                 shared: Optional[X.ExpertWeights] = None):
+        self.shared_pk = None if shared is None else shared.packed(dtype, device)
         self.params = params
         self.topo = topology
         self.g = groups
@@ -297,6 +301,28 @@ class RankLayer:
         self.wg = params.device_w_g(device)
         self.wgT = params.device_w_gT(device)
         self.single = len(groups.ep) == 1 and len(groups.etp) == 1
+
+    # ------------------------------------------------------- shared expert
+    # Builder-defined (no reference): a dense FFN over every token whose
+    # output is added to the routed combine (Qwen2-57B-A14B, BASELINE C4).
+    # One GEMM group spanning all T rows; the ragged tail tile reads past
+    # the buffer end, which TMA zero-fills.
+    def _shared_forward(self, x, saved):
+        if self.shared_pk is None:
+            return None
+        T = x.shape[0]
+        goff = torch.tensor([0, T], dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        pre, h, y = X.ffn_forward(x, goff, 1, None, self.shared_pk, T)
+        saved.update(s_pre=pre, s_h=h, s_goff=goff)
+        return y
+
+    def _shared_backward(self, u, sv):
+        if self.shared_pk is None:
+            return None, None
+        T = u.shape[0]
+        dx, dw1, dw2 = X.ffn_backward(u, sv["x"], sv["s_pre"], sv["s_h"], sv["s_goff"], 1, None,
+                                      self.shared_pk, T)
+        return dx, (dw1, dw2)
 
     # ---------------------------------------------------------------- fwd
     def forward(self, ctx: Optional[RankContext], x: torch.Tensor, positions: torch.Tensor) -> Tuple[torch.Tensor, dict]:
@@ -329,7 +355,8 @@ class RankLayer:
             xp = K.permute(x, plan.gemm_row, R, poffsets=plan.poffsets, counts=plan.counts, E=E)
             goff = plan.poffsets
             pre, h, y = X.ffn_forward(xp, goff, E, None, self.pk, R)
-            out = K.combine(y, plan.gemm_row, T, gates=dec.gates)
+            ys = self._shared_forward(x, saved)
+            out = K.combine(y, plan.gemm_row, T, gates=dec.gates, out=ys, accumulate=ys is not None)
             saved.update(xp=xp, pre=pre, h=h, y=y, goff=goff, G=E, gexp=None, R=R,
                          pair_row=plan.gemm_row)
             return out, saved
@@ -399,7 +426,8 @@ class RankLayer:
         y_mine = self._reduce_blocks(ctx, xpl, y)
         ys = torch.empty((max(R_send, 1), H), dtype=x.dtype, device=x.device)
         ctx.a2a_single(self.g.ep, y_mine, xpl.recv_splits, ys, xpl.send_splits)
-        out = K.combine(ys, plan.gemm_row, T, gates=dec.gates)
+        y_sh = self._shared_forward(x, saved)
+        out = K.combine(ys, plan.gemm_row, T, gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
         saved.update(xp=xp, pre=pre, h=h, y=ys, goff=goff, G=G, gexp=gexp, R=R, xpl=xpl,
                      pair_row=plan.gemm_row, R_send=R_send, R_recv=R_recv)
         return out, saved
@@ -438,7 +466,9 @@ class RankLayer:
             ctx.a2a_single(self.g.ep, dx_mine, xpl.recv_splits, rows, xpl.send_splits)
         dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
                           p.renormalize_topk)
-        dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT)
+        dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
+        dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT, out=dx_sh,
+                       accumulate=dx_sh is not None)
         dwg = K.router_wgrad(x, dz)
         return dx, dwg, dw1p, dw2p
 
@@ -471,7 +501,7 @@ def _validate(blocks, topology, params, seq_len):
 
 def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingParams, world,
                 seq_len: Optional[int] = None, workers: Optional[int] = None, *, dtype=None,
-                check_finite_inputs: bool = True):
+                check_finite_inputs: bool = True, shared_weights: Optional[X.ExpertWeights] = None):
     """Run the MoE layer forward on every rank of ``world`` (dispatcher.py:246-384).
 
     ``world`` is a LocalWorld (all ranks in this process) or an NcclWorld
@@ -493,7 +523,7 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
         dev = getattr(world, "device", torch.device("cuda"))
         dt = dtype or (b.values.dtype if b.values.dtype in (torch.float32, torch.bfloat16) else torch.float32)
         layer = RankLayer(params, w, topology, _rank_groups(topology, groups, rank), rank, dt, dev,
-                          seq_len, check=check_finite_inputs)
+                          seq_len, check=check_finite_inputs, shared=shared_weights)
         out, saved = layer.forward(ctx, b.values, b.positions)
         saved["layer"] = layer
         return out, saved
@@ -532,11 +562,19 @@ def moe_backward(upstream, context: ForwardContext, workers: Optional[int] = Non
             red = ctx.all_reduce(layer.g.edp, flat, "sum")
             dw1p = red[: dw1p.numel()].reshape(dw1p.shape)
             dw2p = red[dw1p.numel():].reshape(dw2p.shape)
-        return dx, dwg, dw1p, dw2p, layer.pk.act
+        shared = None
+        if sv.get("shared_grads") is not None:
+            s1, s2 = sv["shared_grads"]
+            if topology.world_size > 1:  # replicated shared expert: data-parallel over all ranks
+                flat = ctx.all_reduce(world_group, torch.cat([s1.reshape(-1), s2.reshape(-1)]), "sum")
+                s1, s2 = flat[: s1.numel()].reshape(s1.shape), flat[s1.numel():].reshape(s2.shape)
+            shared = (X.unpack_w1_grad(s1, layer.shared_pk.act)[0], X.unpack_w2_grad(s2)[0])
+        return dx, dwg, dw1p, dw2p, layer.pk.act, shared
 
     results = context.world.run(program, workers=workers)
     input_grads = [None if r is None else r[0] for r in results]
     w_g_grad = next(r[1] for r in results if r is not None)
+    shared = next(r[5] for r in results if r is not None)
     expert_grads = {}
     for rank, r in enumerate(results):
         if r is None:
@@ -544,4 +582,4 @@ def moe_backward(upstream, context: ForwardContext, workers: Optional[int] = Non
         etp_idx, ep_idx, edp_idx, _ = topology.moe_coords(rank)
         if edp_idx == 0:
             expert_grads[(ep_idx, etp_idx)] = (X.unpack_w1_grad(r[2], r[4]), X.unpack_w2_grad(r[3]))
-    return BackwardResult(input_grads, w_g_grad, expert_grads)
+    return BackwardResult(input_grads, w_g_grad, expert_grads, shared)

@@ -172,6 +172,17 @@ def full_swiglu_matrices(num_experts: int, hidden: int, ffn: int, seed: int):
     return w1, w2
 
 
+def init_shared_expert(hidden: int, ffn: int, seed: int) -> "ExpertWeights":
+    """Builder-defined dense SwiGLU shared expert (BASELINE C4), U(+-1/sqrt(H))
+    from rng([seed, 5]); replicated on every rank."""
+    rng = np.random.default_rng([seed, 5])
+    bound = 1.0 / np.sqrt(hidden)
+    g = rng.uniform(-bound, bound, size=(hidden, ffn))
+    u = rng.uniform(-bound, bound, size=(hidden, ffn))
+    w2 = rng.uniform(-bound, bound, size=(ffn, hidden))
+    return ExpertWeights((0,), [np.concatenate([g, u], axis=1)], [w2], ACT_SWIGLU, 0, 1)
+
+
 def init_gating_matrix(hidden: int, num_experts: int, seed: int) -> np.ndarray:
     """experts.py:78-81."""
     bound = 1.0 / np.sqrt(hidden)

@@ -250,3 +250,38 @@ def test_c1_shape_layer_vs_oracle(act, dtype, tol, cf):
     for e in range(E):
         assert O.rel_err(res.expert_grads[(0, 0)][0][e].cpu().numpy(), g[3][e]) < tol
         assert O.rel_err(res.expert_grads[(0, 0)][1][e].cpu().numpy(), g[4][e]) < tol
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, FP32_TOL), (torch.bfloat16, BF16_TOL)])
+def test_c4_flavour_shared_expert_vs_oracle(dtype, tol):
+    """C4 flavour (many experts, top-8, SwiGLU + dense shared expert; shapes
+    reduced): routed + shared output and all gradients vs the oracle."""
+    from paper_2504_14960_b200.experts import init_shared_expert
+
+    E, k, H, F, Fs, T, seed = 64, 8, 256, 128, 512, 1024, 3
+    wg = O.gating_matrix(H, E, seed)
+    params = B.GatingParams(w_g=wg, k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, activation="swiglu")
+    shared = init_shared_expert(H, Fs, seed)
+    x = O.token_rows(T, H, seed, 2)
+    u = O.token_rows(T, H, seed, 3)
+    outs, ctx = B.moe_forward([B.TokenBlock(t(x, dtype), np.arange(T))], weights,
+                              B.ParallelTopology(world_size=1), params, B.LocalWorld(1),
+                              shared_weights=shared)
+    res = B.moe_backward([t(u, dtype)], ctx)
+    rnd = lambda a: t(a, dtype).double().cpu().numpy()  # noqa: E731
+    lg = ctx.per_rank[0]["logits"].double().cpu().numpy()
+    w0 = weights[(0, 0)]
+    experts = [O.Expert(np.asarray(a), np.asarray(b), "swiglu") for a, b in zip(w0.w1, w0.w2)]
+    sh = O.Expert(np.asarray(shared.w1[0]), np.asarray(shared.w2[0]), "swiglu")
+    cfg = O.LayerConfig(k=k)
+    y, st = O.layer_forward(rnd(x), lg, experts, cfg, shared=sh)
+    g = O.layer_backward(rnd(u), st, experts, cfg, w_g=wg, shared=sh)
+    np.testing.assert_array_equal(ctx.per_rank[0]["decision"].experts.cpu().numpy(), st.routing.experts)
+    assert O.rel_err(outs[0].double().cpu().numpy(), y) < tol
+    assert O.rel_err(res.input_grads[0].double().cpu().numpy(), g[0]) < tol
+    assert O.rel_err(res.w_g_grad.cpu().numpy(), g[2]) < tol
+    assert O.rel_err(res.shared_grads[0].cpu().numpy(), g[5][0]) < tol
+    assert O.rel_err(res.shared_grads[1].cpu().numpy(), g[5][1]) < tol
+    for e in range(0, E, 7):
+        assert O.rel_err(res.expert_grads[(0, 0)][0][e].cpu().numpy(), g[3][e]) < tol
