@@ -30,8 +30,6 @@ constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int TMEM_COLS = 512;  // 2 accumulator buffers of BN fp32 columns
 constexpr int MAX_G = 1024;
 constexpr int NUM_THREADS = 256;
-constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 1024 /*barriers*/ +
-                           (MAX_G + 1) * 4;
 
 enum Epi : int {
   EPI_STORE = 0,       // C = acc (bf16 or fp32, optional accumulate)
@@ -61,6 +59,21 @@ struct Params {
   const void* PRE; // pre-activation input for *_BWD epilogues
   int64_t ldpre;
   int panel_m;     // raster panel height in m-tiles
+  int tile_m;      // rows per tile: 128 (1 CTA) or 256 (CTA pair)
+};
+
+// Per-CTA-group configuration.  CG = 2: a CTA pair (cluster of 2 on one TPC)
+// computes a 256 x 256 tile with tcgen05.mma.cta_group::2; each CTA stages
+// its 128 rows of A and its 128 rows (half of N) of B, so a stage is 32 KB
+// and six stages fit.
+template <int CG>
+struct Cfg {
+  static constexpr int STAGES_ = CG == 1 ? STAGES : 6;
+  static constexpr int B_CTA = BN / CG;  // B rows staged per CTA
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = B_CTA * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int SMEM = 1024 + STAGES_ * STAGE + 1024 + (MAX_G + 1) * 4;
 };
 
 // ------------------------------------------------------------------ PTX
@@ -141,6 +154,89 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ---- CTA-pair (cta_group::2) helpers
+// A cluster-shared address with this bit cleared names the leader CTA's copy
+// of a shared variable (the pair's TMA completions all land on the leader's
+// full barrier).
+constexpr uint32_t PEER_BIT_MASK = 0xFEFFFFFFu;
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t local_bar, uint32_t target_cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_bar), "r"(target_cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load(const CUtensorMap* map, uint32_t dst, uint32_t bar, int c0,
+                                         int c1, int c2) {
+  if (CG == 1) {
+    tma_load_3d(map, dst, bar, c0, c1, c2);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
+  if (CG == 1) {
+    tc_mma(d_tmem, adesc, bdesc, idesc, accum);
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  }
+}
+// commit the issued MMAs to the barrier at this offset in every CTA of the pair
+template <int CG>
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  if (CG == 1) {
+    tc_commit(bar);
+  } else {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            bar),
+        "h"(mask)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void arrive_all(uint32_t bar) {
+  mbar_arrive(bar);
+  if (CG == 2) mbar_arrive_remote(bar, 1);
+}
+template <int CG>
+__device__ __forceinline__ void tmem_alloc(uint32_t slot, uint32_t cols) {
+  if (CG == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot), "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot), "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  if (CG == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start
 // address, leading/stride byte offsets (>>4), version 1, 128B swizzle.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -153,14 +249,14 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   return d;
 }
 
-// Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M=128, N=BN.
-__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn) {
+// Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M (128 or 256), N=BN.
+__host__ __device__ constexpr uint32_t make_idesc(bool a_mn, bool b_mn, int m) {
   return (1u << 4)                     // D format f32
          | (1u << 7) | (1u << 10)      // A, B = bf16
          | ((a_mn ? 1u : 0u) << 15)    // A major
          | ((b_mn ? 1u : 0u) << 16)    // B major
          | ((uint32_t)(BN >> 3) << 17) // N
-         | ((uint32_t)(BM >> 4) << 24); // M
+         | ((uint32_t)(m >> 4) << 24); // M
 }
 
 // ------------------------------------------------------------- scheduling
@@ -207,18 +303,20 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
   const int nt = (int)((p.N + BN - 1) / BN);
   int mb, nb;
   if (!p.grouped_k) {
-    const int mt = (int)((g1 - g0 + BM - 1) / BM);
+    // a 256-row pair tile may run past the group end: those rows are
+    // computed with this group's weights and masked at store
+    const int mt = (int)((g1 - g0 + p.tile_m - 1) / p.tile_m);
     raster(local, mt, nt, p.panel_m, mb, nb);
-    r.m0 = g0 + (int64_t)mb * BM;
+    r.m0 = g0 + (int64_t)mb * p.tile_m;
     r.m_end = g1;
     r.n0 = (int64_t)nb * BN;
     r.kbeg = 0;
     r.nkb = (int)((p.K + BK - 1) / BK);
     r.bidx = p.gexp ? p.gexp[lo] : lo;
   } else {
-    const int mt = (int)((p.M + BM - 1) / BM);
+    const int mt = (int)((p.M + p.tile_m - 1) / p.tile_m);
     raster(local, mt, nt, p.panel_m, mb, nb);
-    r.m0 = (int64_t)mb * BM;
+    r.m0 = (int64_t)mb * p.tile_m;
     r.m_end = p.M;
     r.n0 = (int64_t)nb * BN;
     r.kbeg = g0;
@@ -299,44 +397,48 @@ __device__ __forceinline__ void load_row32_bf16(const void* base, int64_t off, f
 }
 
 // ------------------------------------------------------------------ kernel
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const Params p) {
+  using C = Cfg<CG>;
+  constexpr int S = C::STAGES_;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sA = base;
-  const uint32_t sB = base + STAGES * A_STAGE_BYTES;
-  const uint32_t bars = base + STAGES * STAGE_BYTES;
+  const uint32_t sB = base + S * C::A_BYTES;
+  const uint32_t bars = base + S * C::STAGE;
   // barrier layout: full[S], empty[S], tfull[2], tempty[2], tmem slot
-  const uint32_t full_bar = bars, empty_bar = bars + 8 * STAGES;
-  const uint32_t tfull_bar = bars + 16 * STAGES, tempty_bar = tfull_bar + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * STAGE_BYTES + 16 * STAGES + 32);
-  int32_t* prefix = reinterpret_cast<int32_t*>(gbase + STAGES * STAGE_BYTES + 1024);
+  const uint32_t full_bar = bars, empty_bar = bars + 8 * S;
+  const uint32_t tfull_bar = bars + 16 * S, tempty_bar = tfull_bar + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * C::STAGE + 16 * S + 32);
+  int32_t* prefix = reinterpret_cast<int32_t*>(gbase + S * C::STAGE + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader CTA of the pair
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
   // per-group tile counts -> prefix (smem)
   for (int g = threadIdx.x; g < p.G; g += NUM_THREADS) {
     int tiles;
     if (!p.grouped_k) {
       const int64_t rows = p.goff[g + 1] - p.goff[g];
-      tiles = (int)(((rows + BM - 1) / BM) * ((p.N + BN - 1) / BN));
+      tiles = (int)(((rows + p.tile_m - 1) / p.tile_m) * ((p.N + BN - 1) / BN));
     } else {
-      tiles = (int)(((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN));
+      tiles = (int)(((p.M + p.tile_m - 1) / p.tile_m) * ((p.N + BN - 1) / BN));
     }
     prefix[g + 1] = tiles;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < S; ++i) {
       mbar_init(full_bar + 8 * i, 1);
       mbar_init(empty_bar + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull_bar + 8 * i, 1);
-      mbar_init(tempty_bar + 8 * i, 4);
+      mbar_init(tempty_bar + 8 * i, 4 * CG);  // epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -344,56 +446,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     prefetch_map(&map_a);
     prefetch_map(&map_b);
   }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
+  if (warp == 2) tmem_alloc<CG>(smem_u32(tmem_slot), TMEM_COLS);
   __syncthreads();
   if (threadIdx.x == 0) {
     prefix[0] = 0;
     for (int g = 0; g < p.G; ++g) prefix[g + 1] += prefix[g];
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total = prefix[p.G];
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    // Both CTAs of a pair load their halves; TMA completions of both land on
+    // the leader's full barrier, which the leader arms for both halves.
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cid; t < total; t += ncl) {
         const Tile tl = decode(p, prefix, t);
+        const int m0 = (int)tl.m0 + BM * (int)crank;
+        const int n0 = (int)tl.n0 + C::B_CTA * (int)crank;
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(empty_bar + 8 * stage, phase ^ 1);
           const uint32_t fb = full_bar + 8 * stage;
-          mbar_expect_tx(fb, STAGE_BYTES);
+          if (crank == 0) mbar_expect_tx(fb, C::STAGE * CG);
+          const uint32_t fb_tma = CG == 2 ? (fb & PEER_BIT_MASK) : fb;
           const int kc = (int)(tl.kbeg + (int64_t)kb * BK);
-          const uint32_t a_dst = sA + stage * A_STAGE_BYTES;
-          const uint32_t b_dst = sB + stage * B_STAGE_BYTES;
+          const uint32_t a_dst = sA + stage * C::A_BYTES;
+          const uint32_t b_dst = sB + stage * C::B_BYTES;
           if (!A_MN) {
             // A [rows, K] K-major: box {64 K, 128 rows}
-            tma_load_3d(&map_a, a_dst, fb, kc, (int)tl.m0, 0);
+            tma_load<CG>(&map_a, a_dst, fb_tma, kc, m0, 0);
           } else {
             // A stored [K, M] (M contiguous): 2 boxes {64 M, 64 K}
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i)
-              tma_load_3d(&map_a, a_dst + i * 8192, fb, (int)tl.m0 + 64 * i, kc, 0);
+              tma_load<CG>(&map_a, a_dst + i * 8192, fb_tma, m0 + 64 * i, kc, 0);
           }
           if (!B_MN) {
-            // B stored [L, N, K]: box {64 K, 256 N, 1}
-            tma_load_3d(&map_b, b_dst, fb, kc, (int)tl.n0, tl.bidx);
+            // B stored [L, N, K]: box {64 K, B_CTA N, 1}
+            tma_load<CG>(&map_b, b_dst, fb_tma, kc, n0, tl.bidx);
           } else {
-            // B stored [L, K, N] (N contiguous): 4 boxes {64 N, 64 K, 1}
+            // B stored [L, K, N] (N contiguous): B_CTA/64 boxes {64 N, 64 K, 1}
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_3d(&map_b, b_dst + i * 8192, fb, (int)tl.n0 + 64 * i, kc, tl.bidx);
+            for (int i = 0; i < C::B_CTA / 64; ++i)
+              tma_load<CG>(&map_b, b_dst + i * 8192, fb_tma, n0 + 64 * i, kc, tl.bidx);
           }
-          if (++stage == STAGES) {
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
@@ -402,13 +505,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+    // (leader CTA only for a pair: one tcgen05.mma.cta_group::2 covers 256 x 256)
+    if (lane == 0 && crank == 0) {
+      constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BM * CG);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cid; t < total; t += ncl) {
         const Tile tl = decode(p, prefix, t);
         mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
@@ -416,8 +520,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(full_bar + 8 * stage, phase);
           tc_fence_after();
-          const uint32_t a_s = sA + stage * A_STAGE_BYTES;
-          const uint32_t b_s = sB + stage * B_STAGE_BYTES;
+          const uint32_t a_s = sA + stage * C::A_BYTES;
+          const uint32_t b_s = sB + stage * C::B_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: advance 32 B inside the 128B swizzle atom; MN-major:
@@ -426,16 +530,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                      : smem_desc(a_s + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc(b_s + k * 2048, 8192, 1024)
                                      : smem_desc(b_s + k * 32, 16, 1024);
-            tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            tc_mma<CG>(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          tc_commit(empty_bar + 8 * stage);
-          if (++stage == STAGES) {
+          tc_commit<CG>(empty_bar + 8 * stage);
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (tl.nkb > 0) tc_commit(tfull_bar + 8 * acc);
-        else mbar_arrive(tfull_bar + 8 * acc);
+        if (tl.nkb > 0) tc_commit<CG>(tfull_bar + 8 * acc);
+        else arrive_all<CG>(tfull_bar + 8 * acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -443,10 +547,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
-    const int row_in_tile = 32 * q + lane;
+    const int row_in_tile = BM * (int)crank + 32 * q + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = cid; t < total; t += ncl) {
       const Tile tl = decode(p, prefix, t);
       mbar_wait(tfull_bar + 8 * acc, acc_phase);
       tc_fence_after();
@@ -545,18 +649,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar + 8 * acc);
+      // the leader's MMA warp waits on its own tempty barrier for both CTAs
+      if (lane == 0) {
+        if (CG == 2 && crank != 0) mbar_arrive_remote(tempty_bar + 8 * acc, 0);
+        else mbar_arrive(tempty_bar + 8 * acc);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync();  // the peer may still arrive on our barriers
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS));
-  }
+  if (warp == 2) tmem_dealloc<CG>(tmem_base, TMEM_COLS);
 }
 
 }  // namespace tc
@@ -604,17 +710,17 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, u
 }
 
 // Raster policy from the typical per-group operand footprints (bf16 bytes).
-static int choose_panel(const b200moe_tc_gemm_args* a) {
-  using namespace tc;
+static int choose_panel(const b200moe_tc_gemm_args* a, int tile_m) {
   const double G = a->G > 0 ? a->G : 1;
   const double Mg = a->grouped_dim == 0 ? (double)a->a_rows / G : (double)a->M;
   const double Kg = a->grouped_dim == 0 ? (double)a->K : (double)a->a_rows / G;
   const double a_bytes = Mg * Kg * 2, b_bytes = (double)a->N * Kg * 2;
   const double resident = 40.0 * 1024 * 1024;  // comfortably inside the 126 MB L2
-  const int mt = (int)((Mg + BM - 1) / BM);
+  const int mt = (int)((Mg + tile_m - 1) / tile_m);
+  const int small = tile_m == 256 ? 4 : 8;
   if (a_bytes <= resident) return mt > 0 ? mt : 1;  // A resident, B streamed once
-  if (b_bytes <= resident) return 8;                 // B resident, A streamed once
-  return 16;                                         // balanced k-slab reuse
+  if (b_bytes <= resident) return small;             // B resident, A streamed once
+  return 2 * small;                                  // balanced k-slab reuse
 }
 
 int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
@@ -637,6 +743,14 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
     set_error("gemm_tc: leading dimensions must be multiples of 8 elements (16 B)");
     return B200MOE_EUNSUPPORTED;
   }
+  // CTA pairs (cta_group::2, 256 x 256 tiles) by default; B200MOE_CTA_GROUP=1
+  // selects single-CTA 128 x 256 tiles.  num_ctas must be even for pairs.
+  const char* cg_str = getenv("B200MOE_CTA_GROUP");
+  const int cg_env = (cg_str && cg_str[0] == '1') ? 1 : 2;
+  int grid = a->num_ctas > 0 ? a->num_ctas : num_sms();
+  const int cg = (cg_env == 2 && grid >= 2) ? 2 : 1;
+  if (cg == 2) grid &= ~1;
+  const uint32_t b_box = BN / cg;
   CUtensorMap ma, mb;
   int rc;
   const uint64_t R = (uint64_t)a->a_rows;
@@ -645,9 +759,9 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   else        // A [R(K), M]: box {64 M, 64 K}
     rc = make_map(&ma, a->A, (uint64_t)a->M, R, 1, (uint64_t)a->lda, (uint64_t)a->lda * R, 64);
   if (rc) return rc;
-  if (!b_mn)  // B [batch, N, K]: box {64 K, 256 N, 1}
+  if (!b_mn)  // B [batch, N, K]: box {64 K, BN/cg N, 1}
     rc = make_map(&mb, a->B, (uint64_t)a->K, (uint64_t)a->N, (uint64_t)a->b_batch,
-                  (uint64_t)a->ldb, (uint64_t)a->b_batch_stride, BN);
+                  (uint64_t)a->ldb, (uint64_t)a->b_batch_stride, b_box);
   else {      // B [batch, Kdim, N]: box {64 N, 64 K, 1}
     const uint64_t kdim = a->grouped_dim == 1 ? R : (uint64_t)a->K;
     const uint64_t bstride = a->b_batch > 1 ? (uint64_t)a->b_batch_stride : (uint64_t)a->ldb * kdim;
@@ -675,22 +789,46 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.ldh = a->ldh;
   p.PRE = a->PRE;
   p.ldpre = a->ldpre;
-  p.panel_m = choose_panel(a);
+  p.tile_m = BM * cg;
+  p.panel_m = choose_panel(a, p.tile_m);
 
-  auto kern = a_mn ? (b_mn ? gemm_tc_kernel<true, true> : gemm_tc_kernel<true, false>)
-                    : (b_mn ? gemm_tc_kernel<false, true> : gemm_tc_kernel<false, false>);
-  static bool attr_set[4] = {false, false, false, false};
-  const int ki = (a_mn ? 2 : 0) + (b_mn ? 1 : 0);
+  using KernT = void (*)(const CUtensorMap, const CUtensorMap, const Params);
+  KernT kern;
+  int smem;
+  if (cg == 1) {
+    kern = a_mn ? (b_mn ? gemm_tc_kernel<true, true, 1> : gemm_tc_kernel<true, false, 1>)
+                : (b_mn ? gemm_tc_kernel<false, true, 1> : gemm_tc_kernel<false, false, 1>);
+    smem = Cfg<1>::SMEM;
+  } else {
+    kern = a_mn ? (b_mn ? gemm_tc_kernel<true, true, 2> : gemm_tc_kernel<true, false, 2>)
+                : (b_mn ? gemm_tc_kernel<false, true, 2> : gemm_tc_kernel<false, false, 2>);
+    smem = Cfg<2>::SMEM;
+  }
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  const int ki = (cg == 2 ? 4 : 0) + (a_mn ? 2 : 0) + (b_mn ? 1 : 0);
   if (!attr_set[ki]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
-        cudaSuccess) {
-      set_error("gemm_tc: cannot set %d B dynamic shared memory", SMEM_BYTES);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+      set_error("gemm_tc: cannot set %d B dynamic shared memory", smem);
       return B200MOE_ELAUNCH;
     }
     attr_set[ki] = true;
   }
-  const int grid = a->num_ctas > 0 ? a->num_ctas : num_sms();
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, p) != cudaSuccess) {
+    set_error("gemm_tc: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return B200MOE_ELAUNCH;
+  }
   B200MOE_CHECK_LAUNCH("gemm_tc");
   return B200MOE_OK;
 }

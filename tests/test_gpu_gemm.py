@@ -13,6 +13,14 @@ from paper_2504_14960_b200 import gemm_tc, kernels as K  # noqa: E402
 ALIGN = 128
 
 
+@pytest.fixture(params=["1", "2"], ids=["cta1", "cta2"], autouse=True)
+def cta_group(request, monkeypatch):
+    """Run every test with single-CTA (128x256) and CTA-pair (256x256,
+    tcgen05.mma.cta_group::2) tiles."""
+    monkeypatch.setenv("B200MOE_CTA_GROUP", request.param)
+    return request.param
+
+
 def _layout(counts, align=ALIGN):
     pad = [(c + align - 1) // align * align for c in counts]
     off = np.concatenate(([0], np.cumsum(pad))).astype(np.int32)
