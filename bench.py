@@ -288,6 +288,17 @@ def main():
     for n, m in all_launches:
         if not n.startswith("gemm_tc"):
             other[n] = other.get(n, 0.0) + m
+    # all-to-all bus bandwidth (nccl-tests convention: bytes sent incl. self /
+    # time * (n-1)/n), per direction per GPU, against 900 GB/s NVLink 5
+    a2a = None
+    a2a_events = [(n, m) for n, m in all_launches if n.startswith("nccl:a2a[")]
+    if a2a_events and world > 1:
+        sent = sum(int(n.split("[")[1].split("->")[0]) for n, _ in a2a_events) * H * 2
+        t_a2a = sum(m for _, m in a2a_events) / 1e3
+        busbw = sent / t_a2a * (world - 1) / world / 1e9
+        a2a = {"busbw_gbs": busbw, "nominal_gbs": 900.0, "frac_nominal": busbw / 900.0,
+               "ms_per_step": t_a2a * 1e3, "calls_per_step": len(a2a_events),
+               "bytes_per_step": sent, "impl": "NCCL all_to_all_single (grouped P2P)"}
     P = T * k  # kept pairs per GPU (dropless)
     flops_step = 18.0 * P * H * F  # SwiGLU fwd 6PHF + bwd 12PHF
     gemm_ms = sum(ms_ for _, ms_ in per_launch)
@@ -356,7 +367,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload_config(a),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "a2a": a2a,
             "gpu_launches": launches, "clocks": clk,
         }), flush=True)
     if world > 1:

@@ -24,12 +24,10 @@ namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int STAGES = 4;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int TMEM_COLS = 512;  // 2 accumulator buffers of BN fp32 columns
-constexpr int MAX_G = 1024;
+constexpr int MAX_G = 512;
 constexpr int NUM_THREADS = 256;
+constexpr int STG_BYTES = 128 * 128;  // one epilogue staging tile: 128 rows x 128 B
 
 enum Epi : int {
   EPI_STORE = 0,       // C = acc (bf16 or fp32, optional accumulate)
@@ -60,20 +58,25 @@ struct Params {
   int64_t ldpre;
   int panel_m;     // raster panel height in m-tiles
   int tile_m;      // rows per tile: 128 (1 CTA) or 256 (CTA pair)
+  int debug_nostore;  // perf experiments only: skip epilogue global traffic
+  int use_tma;        // output tensor maps are valid (TMA-store epilogue)
 };
 
 // Per-CTA-group configuration.  CG = 2: a CTA pair (cluster of 2 on one TPC)
 // computes a 256 x 256 tile with tcgen05.mma.cta_group::2; each CTA stages
 // its 128 rows of A and its 128 rows (half of N) of B, so a stage is 32 KB
 // and six stages fit.
+// The epilogue stages 128 B row chunks in NSTG swizzled 16 KB buffers and
+// writes them with TMA bulk tensor stores.
 template <int CG>
 struct Cfg {
-  static constexpr int STAGES_ = CG == 1 ? STAGES : 6;
+  static constexpr int STAGES_ = CG == 1 ? 3 : 5;
+  static constexpr int NSTG = 2;
   static constexpr int B_CTA = BN / CG;  // B rows staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_CTA * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int SMEM = 1024 + STAGES_ * STAGE + 1024 + (MAX_G + 1) * 4;
+  static constexpr int SMEM = 1024 + STAGES_ * STAGE + NSTG * STG_BYTES + 1024 + (MAX_G + 1) * 4;
 };
 
 // ------------------------------------------------------------------ PTX
@@ -153,6 +156,66 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+
+// ---- epilogue: shared-memory staging + TMA bulk tensor stores
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                                  int c2) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// one 128-byte row chunk (8 x 16 B) into a 128B-swizzled staging tile
+__device__ __forceinline__ void st_row_chunk(uint32_t buf, int r, const uint4 (&v)[8]) {
+  const uint32_t row = buf + (uint32_t)r * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) st_shared_v4(row + ((uint32_t)(j ^ (r & 7)) << 4), v[j]);
+}
+
+// Ring of NSTG staging tiles shared by the 128 epilogue threads.
+template <int NSTG>
+struct Stager {
+  uint32_t base;
+  int buf;
+  bool leader;
+  __device__ __forceinline__ uint32_t acquire() {
+    if (leader) bulk_wait_read<NSTG - 1>();  // the store that last used this tile has read it
+    epi_bar();
+    return base + buf * STG_BYTES;
+  }
+  __device__ __forceinline__ void issue(const CUtensorMap* map, int c0, int c1, int c2, bool reduce) {
+    fence_async_smem();  // generic-proxy smem writes -> visible to the TMA (async proxy)
+    epi_bar();
+    if (leader) {
+      const uint32_t src = base + buf * STG_BYTES;
+      if (reduce) tma_reduce_add_3d(map, src, c0, c1, c2);
+      else tma_store_3d(map, src, c0, c1, c2);
+      bulk_commit();
+    }
+    buf = (buf + 1) % NSTG;
+  }
+};
 
 // ---- CTA-pair (cta_group::2) helpers
 // A cluster-shared address with this bit cleared names the leader CTA's copy
@@ -348,6 +411,20 @@ __device__ __forceinline__ float2 unpack_bf16(uint32_t v) {
   __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&v);
   return __bfloat1622float2(h);
 }
+// 32 floats -> 4 x uint4 of bf16 (64 B)
+__device__ __forceinline__ void pack32_bf16(const float* f, uint4* out) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    out[i] = make_uint4(pack_bf16(f[8 * i], f[8 * i + 1]), pack_bf16(f[8 * i + 2], f[8 * i + 3]),
+                        pack_bf16(f[8 * i + 4], f[8 * i + 5]), pack_bf16(f[8 * i + 6], f[8 * i + 7]));
+}
+// 32 floats -> 8 x uint4 of fp32 (128 B)
+__device__ __forceinline__ void pack32_f32(const float* f, uint4* out) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    out[i] = make_uint4(__float_as_uint(f[4 * i]), __float_as_uint(f[4 * i + 1]),
+                        __float_as_uint(f[4 * i + 2]), __float_as_uint(f[4 * i + 3]));
+}
 
 // store 32 consecutive values (fp32 in f[]) of one row at column n (masked by N)
 __device__ __forceinline__ void store_row32(void* base, bool f32, int64_t row_off, int64_t n,
@@ -365,7 +442,9 @@ __device__ __forceinline__ void store_row32(void* base, bool f32, int64_t row_of
         *reinterpret_cast<float4*>(p + i) = v;
       }
     } else {
-      for (int i = 0; i < 32 && n + i < N; ++i) p[i] = accumulate ? p[i] + f[i] : f[i];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (n + i < N) p[i] = accumulate ? p[i] + f[i] : f[i];
     }
   } else {
     __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + row_off + n;
@@ -380,7 +459,9 @@ __device__ __forceinline__ void store_row32(void* base, bool f32, int64_t row_of
         *reinterpret_cast<uint4*>(p + i) = v;
       }
     } else {
-      for (int i = 0; i < 32 && n + i < N; ++i) p[i] = __float2bfloat16_rn(f[i]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (n + i < N) p[i] = __float2bfloat16_rn(f[i]);
     }
   }
 }
@@ -400,6 +481,7 @@ __device__ __forceinline__ void load_row32_bf16(const void* base, int64_t off, f
 template <bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_h,
                    const Params p) {
   using C = Cfg<CG>;
   constexpr int S = C::STAGES_;
@@ -409,12 +491,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sA = base;
   const uint32_t sB = base + S * C::A_BYTES;
-  const uint32_t bars = base + S * C::STAGE;
+  const uint32_t stg = base + S * C::STAGE;  // epilogue staging ring (1024-aligned)
+  const int bars_off = S * C::STAGE + C::NSTG * STG_BYTES;
+  const uint32_t bars = base + bars_off;
   // barrier layout: full[S], empty[S], tfull[2], tempty[2], tmem slot
   const uint32_t full_bar = bars, empty_bar = bars + 8 * S;
   const uint32_t tfull_bar = bars + 16 * S, tempty_bar = tfull_bar + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * C::STAGE + 16 * S + 32);
-  int32_t* prefix = reinterpret_cast<int32_t*>(gbase + S * C::STAGE + 1024);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + bars_off + 16 * S + 32);
+  int32_t* prefix = reinterpret_cast<int32_t*>(gbase + bars_off + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader CTA of the pair
@@ -548,6 +632,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
     const int row_in_tile = BM * (int)crank + 32 * q + lane;
+    Stager<C::NSTG> stgr{stg, 0, threadIdx.x == 128};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < total; t += ncl) {
@@ -555,11 +640,126 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(tfull_bar + 8 * acc, acc_phase);
       tc_fence_after();
       const int64_t row = tl.m0 + row_in_tile;
-      const bool live = row < tl.m_end;
+      const bool live = row < tl.m_end && !p.debug_nostore;
       const bool zero = tl.nkb == 0;
       const int64_t c_off = p.grouped_k ? (int64_t)tl.g * p.c_sg : 0;
       const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
-      if (p.epi == EPI_STORE) {
+      // This CTA's 128-row block is either entirely inside the group (TMA
+      // store path), entirely past it (nothing to do) or -- only for
+      // unaligned groups -- ragged (direct masked stores).
+      const int64_t row0 = tl.m0 + BM * (int64_t)crank;
+      const bool cta_live = row0 < tl.m_end && !p.debug_nostore;
+      const bool tma_path = p.use_tma && row0 + BM <= tl.m_end && p.epi <= EPI_SWIGLU_BWD;
+      const int r = 32 * q + lane;
+      if (!cta_live) {
+        // this CTA half holds no rows of the group
+      } else if (tma_path) {
+        const int crow = (int)row0;
+        if (p.epi == EPI_STORE && p.out_f32) {
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            const int64_t n = tl.n0 + c * 32;
+            if (n >= p.N) break;
+            uint32_t v[32];
+            tmem_ld32(t_row + c * 32, v);
+            float f[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = zero ? 0.f : __uint_as_float(v[i]);
+            uint4 o[8];
+            pack32_f32(f, o);
+            st_row_chunk(stgr.acquire(), r, o);
+            stgr.issue(&map_c, (int)n, crow, p.grouped_k ? tl.g : 0, p.accumulate);
+          }
+        } else if (p.epi == EPI_STORE) {
+#pragma unroll 1
+          for (int c = 0; c < BN / 64; ++c) {
+            const int64_t n = tl.n0 + c * 64;
+            if (n >= p.N) break;
+            uint32_t v0[32], v1[32];
+            tmem_ld32(t_row + c * 64, v0);
+            tmem_ld32(t_row + c * 64 + 32, v1);
+            float f0[32], f1[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              f0[i] = zero ? 0.f : __uint_as_float(v0[i]);
+              f1[i] = zero ? 0.f : __uint_as_float(v1[i]);
+            }
+            uint4 o[8];
+            pack32_bf16(f0, o);
+            pack32_bf16(f1, o + 4);
+            st_row_chunk(stgr.acquire(), r, o);
+            stgr.issue(&map_c, (int)n, crow, p.grouped_k ? tl.g : 0, false);
+          }
+        } else if (p.epi == EPI_SWIGLU_FWD) {
+          uint4 hb[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) hb[i] = make_uint4(0, 0, 0, 0);
+          int b = 0;
+#pragma unroll 1
+          for (; b < BN / 64; ++b) {
+            const int64_t n = tl.n0 + b * 64;
+            if (n >= p.N) break;
+            uint32_t vg[32], vu[32];
+            tmem_ld32(t_row + b * 64, vg);
+            tmem_ld32(t_row + b * 64 + 32, vu);
+            float g[32], u[32], h[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              // round the pre-activations to bf16 first so the saved `pre`
+              // and `h` agree exactly with what the backward recomputes
+              g[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(vg[i])));
+              u[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(vu[i])));
+              h[i] = silu_f(g[i]) * u[i];
+            }
+            uint4 o[8];
+            pack32_bf16(g, o);
+            pack32_bf16(u, o + 4);
+            st_row_chunk(stgr.acquire(), r, o);
+            stgr.issue(&map_c, (int)n, crow, 0, false);
+            uint4 hq[4];
+            pack32_bf16(h, hq);
+            if (b & 1) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) hb[4 + i] = hq[i];
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) hb[i] = hq[i];
+            }
+            if (b & 1) {  // two blocks of h = one 64-column (128 B) chunk
+              st_row_chunk(stgr.acquire(), r, hb);
+              stgr.issue(&map_h, (int)((tl.n0 + (b - 1) * 64) / 2), crow, 0, false);
+            }
+          }
+          if (b & 1) {  // odd number of blocks: flush the half chunk (TMA clips at F)
+            st_row_chunk(stgr.acquire(), r, hb);
+            stgr.issue(&map_h, (int)((tl.n0 + (b - 1) * 64) / 2), crow, 0, false);
+          }
+        } else {  // EPI_SWIGLU_BWD: acc = dh over F columns; pre/dpre [.., 2F] interleaved
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            const int64_t n = tl.n0 + c * 32;
+            if (n >= p.N) break;
+            uint32_t v[32];
+            tmem_ld32(t_row + c * 32, v);
+            const int64_t pc = (n / 32) * 64;
+            float g[32], u[32], dg[32], du[32];
+            load_row32_bf16(p.PRE, row * p.ldpre + pc, g);
+            load_row32_bf16(p.PRE, row * p.ldpre + pc + 32, u);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float d = __uint_as_float(v[i]);
+              const float s = 1.f / (1.f + __expf(-g[i]));
+              dg[i] = d * u[i] * s * (1.f + g[i] * (1.f - s));
+              du[i] = d * g[i] * s;
+            }
+            uint4 o[8];
+            pack32_bf16(dg, o);
+            pack32_bf16(du, o + 4);
+            st_row_chunk(stgr.acquire(), r, o);
+            stgr.issue(&map_c, (int)pc, crow, 0, false);
+          }
+        }
+      } else if (p.epi == EPI_STORE) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t v[32];
@@ -657,6 +857,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (threadIdx.x == 128) bulk_wait_all();  // staged stores done before smem is released
   }
   tc_fence_before();
   if (CG == 2) cluster_sync();  // the peer may still arrive on our barriers
@@ -686,21 +887,24 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-// 3-D bf16 tensor map {d0 (contiguous), d1, d2} with box {64, box1, 1}, 128B swizzle.
+// 3-D tensor map {d0 (contiguous), d1, d2} with box {128 B of d0, box1, 1},
+// 128B swizzle; f32 = false: bf16 elements (box0 = 64), true: fp32 (box0 = 32).
 static int make_map(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
-                    uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box1) {
+                    uint64_t stride1_elems, uint64_t stride2_elems, uint32_t box1, bool f32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     set_error("gemm_tc: cuTensorMapEncodeTiled unavailable");
     return B200MOE_ELAUNCH;
   }
+  const uint64_t es = f32 ? 4 : 2;
   cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {stride1_elems * 2, stride2_elems * 2};
-  cuuint32_t box[3] = {64, box1, 1};
+  cuuint64_t strides[2] = {stride1_elems * es, stride2_elems * es};
+  cuuint32_t box[3] = {f32 ? 32u : 64u, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("gemm_tc: cuTensorMapEncodeTiled failed (%d) dims=%llu,%llu,%llu", (int)r,
               (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2);
@@ -769,7 +973,29 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   }
   if (rc) return rc;
 
+  // Output maps for the TMA-store epilogue (row dim = a_rows for grouped M,
+  // M for grouped K; 3rd dim = per-group output for grouped K).
+  CUtensorMap mc, mh;
+  int use_tma = 0;
+  if (a->epilogue <= 2) {
+    const bool of32 = a->out_dtype == B200MOE_F32;
+    const uint64_t crows = a->grouped_dim == 0 ? R : (uint64_t)a->M;
+    const uint64_t cg_n = a->grouped_dim == 0 ? 1 : (uint64_t)a->G;
+    const uint64_t ccols = a->epilogue == 2 ? 2 * (uint64_t)a->N : (uint64_t)a->N;
+    const uint64_t csg = a->grouped_dim == 0 ? (uint64_t)a->ldc * crows : (uint64_t)a->c_sg;
+    rc = make_map(&mc, a->C, ccols, crows, cg_n, (uint64_t)a->ldc, csg, BM, of32);
+    if (rc == B200MOE_OK && a->epilogue == 1)
+      rc = make_map(&mh, a->H, (uint64_t)a->N / 2, R, 1, (uint64_t)a->ldh, (uint64_t)a->ldh * R, BM);
+    else
+      mh = mc;
+    use_tma = rc == B200MOE_OK && (a->ldc % 8 == 0) && (a->epilogue != 1 || a->ldh % 8 == 0);
+    if (rc != B200MOE_OK) mc = mh = ma;  // fall back to direct stores
+  } else {
+    mc = mh = ma;
+  }
+
   Params p{};
+  p.use_tma = use_tma;
   p.G = a->G;
   p.grouped_k = a->grouped_dim;
   p.M = a->M;
@@ -790,9 +1016,12 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.PRE = a->PRE;
   p.ldpre = a->ldpre;
   p.tile_m = BM * cg;
+  const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
+  p.debug_nostore = (ns && ns[0] == '1') ? 1 : 0;
   p.panel_m = choose_panel(a, p.tile_m);
 
-  using KernT = void (*)(const CUtensorMap, const CUtensorMap, const Params);
+  using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                         const Params);
   KernT kern;
   int smem;
   if (cg == 1) {
@@ -825,7 +1054,7 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, p) != cudaSuccess) {
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mh, p) != cudaSuccess) {
     set_error("gemm_tc: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return B200MOE_ELAUNCH;
   }
