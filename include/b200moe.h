@@ -80,7 +80,10 @@ B200MOE_API size_t b200moe_dispatch_plan_ws(int64_t T, int E);
  * order     [T] i32, nullable: token admission order for capacity (identity
  *           when positions are increasing in row order).
  * cap       per-expert capacity; <= 0 means dropless.
- * align     row alignment of each expert segment in the padded (GEMM) layout.
+ * align     > 0: each expert segment of the padded (GEMM) layout is rounded up
+ *           to a multiple of align rows; < 0: pad-to-capacity, every segment
+ *           has exactly -align rows (requires 0 < cap <= -align), so all
+ *           exchange sizes are static.
  * Outputs: kept_out[T*k] u8; expert_counts[E] (kept pairs);
  *   expert_offsets[E+1] (unpadded, send order); padded_offsets[E+1];
  *   send_row[T*k] (row of the pair in reference permutation order, -1 when
@@ -120,7 +123,9 @@ B200MOE_API int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz
 /* out[row_of(t,s)] = x[t] (* scale[t,s] when scale != NULL) for every kept
  * pair (pair_row >= 0).                                 -- dispatcher.py:134-142
  * When padded_offsets/expert_counts are given, rows
- * [padded_offsets[e]+expert_counts[e], padded_offsets[e+1]) are zeroed. */
+ * [padded_offsets[e]+expert_counts[e], padded_offsets[e+1]) are zeroed
+ * (align: the plan's align; at most align-1, or -align when negative, pad
+ * rows per segment). */
 B200MOE_API int b200moe_permute(const void* x, int dtype, int64_t T, int64_t H, int k, const int32_t* pair_row,
                     const float* scale, void* out, const int32_t* padded_offsets,
                     const int32_t* expert_counts, int E, int align, void* stream);

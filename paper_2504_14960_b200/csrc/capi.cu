@@ -110,7 +110,9 @@ int b200moe_dispatch_plan(const int32_t* topk_idx, const float* gates, const uin
                           int32_t* send_row, int32_t* gemm_row, int64_t* perm, float* perm_gates,
                           void* stream) {
   REQUIRE(E >= 1 && E <= 4096 && k >= 1 && k <= 16 && k <= E, "dispatch_plan: bad E=%d k=%d", E, k);
-  REQUIRE(align >= 1, "dispatch_plan: align must be >= 1");
+  REQUIRE(align != 0, "dispatch_plan: align must be non-zero");
+  REQUIRE(align > 0 || (cap > 0 && cap <= -(int64_t)align),
+          "dispatch_plan: pad-to-capacity (align < 0) needs 0 < cap <= -align");
   REQUIRE(T >= 0 && T * k < (int64_t)INT32_MAX, "dispatch_plan: T*k must fit int32");
   REQUIRE(workspace_bytes >= plan_ws_bytes(T, E), "dispatch_plan: workspace too small");
   REQUIRE(expert_counts && expert_offsets && padded_offsets && workspace,
@@ -160,7 +162,9 @@ int b200moe_permute(const void* x, int dtype, int64_t T, int64_t H, int k, const
   REQUIRE(dt_ok(dtype) && H >= 1 && k >= 1 && T >= 0, "permute: bad args");
   REQUIRE(out, "permute: null output");
   if (T > 0) REQUIRE(x && pair_row, "permute: null pointer");
-  const int64_t max_pad = (padded_offsets && expert_counts) ? (align > 1 ? align - 1 : 0) : 0;
+  // align > 0: at most align-1 pad rows per segment; align < 0: fixed segments
+  // of -align rows (pad-to-capacity), up to -align pad rows
+  const int64_t max_pad = (padded_offsets && expert_counts) ? (align > 1 ? align - 1 : (align < 0 ? -(int64_t)align : 0)) : 0;
   return permute(x, dtype, T, H, k, pair_row, scale, out, padded_offsets, expert_counts, E,
                  max_pad, S(stream));
 }
@@ -171,7 +175,9 @@ int b200moe_permute_bwd(const void* u, int dtype, int64_t T, int64_t H, int k,
                         const int32_t* expert_counts, int E, int align, void* stream) {
   REQUIRE(dt_ok(dtype) && H >= 1 && k >= 1 && T >= 0, "permute_bwd: bad args");
   if (T > 0) REQUIRE(u && pair_row && gates && y_rows && dy_rows && dgates, "permute_bwd: null pointer");
-  const int64_t max_pad = (padded_offsets && expert_counts) ? (align > 1 ? align - 1 : 0) : 0;
+  // align > 0: at most align-1 pad rows per segment; align < 0: fixed segments
+  // of -align rows (pad-to-capacity), up to -align pad rows
+  const int64_t max_pad = (padded_offsets && expert_counts) ? (align > 1 ? align - 1 : (align < 0 ? -(int64_t)align : 0)) : 0;
   return permute_bwd(u, dtype, T, H, k, pair_row, gates, y_rows, dy_rows, dgates, padded_offsets,
                      expert_counts, E, max_pad, S(stream));
 }

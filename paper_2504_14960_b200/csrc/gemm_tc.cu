@@ -71,7 +71,7 @@ struct Params {
 template <int CG>
 struct Cfg {
   static constexpr int STAGES_ = CG == 1 ? 3 : 5;
-  static constexpr int NSTG = 2;
+  static constexpr int NSTG = 3;
   static constexpr int B_CTA = BN / CG;  // B rows staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_CTA * BK * 2;
@@ -185,6 +185,14 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
 }
 // one 128-byte row chunk (8 x 16 B) into a 128B-swizzled staging tile
 __device__ __forceinline__ void st_row_chunk(uint32_t buf, int r, const uint4 (&v)[8]) {
@@ -494,10 +502,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t stg = base + S * C::STAGE;  // epilogue staging ring (1024-aligned)
   const int bars_off = S * C::STAGE + C::NSTG * STG_BYTES;
   const uint32_t bars = base + bars_off;
-  // barrier layout: full[S], empty[S], tfull[2], tempty[2], tmem slot
+  // barrier layout: full[S], empty[S], tfull[2], tempty[2], ldb[NSTG], tmem slot
   const uint32_t full_bar = bars, empty_bar = bars + 8 * S;
   const uint32_t tfull_bar = bars + 16 * S, tempty_bar = tfull_bar + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + bars_off + 16 * S + 32);
+  const uint32_t ld_bar = tfull_bar + 32;  // epilogue TMA loads into the staging ring
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + bars_off + 16 * S + 32 + 8 * C::NSTG + 8);
   int32_t* prefix = reinterpret_cast<int32_t*>(gbase + bars_off + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -524,6 +533,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(tfull_bar + 8 * i, 1);
       mbar_init(tempty_bar + 8 * i, 4 * CG);  // epilogue warps of both CTAs
     }
+    for (int i = 0; i < C::NSTG; ++i) mbar_init(ld_bar + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -633,6 +643,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
     const int row_in_tile = BM * (int)crank + 32 * q + lane;
     Stager<C::NSTG> stgr{stg, 0, threadIdx.x == 128};
+    uint32_t ld_par = 0;  // phase bits of the staging-ring load barriers
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < total; t += ncl) {
@@ -735,16 +746,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             stgr.issue(&map_h, (int)((tl.n0 + (b - 1) * 64) / 2), crow, 0, false);
           }
         } else {  // EPI_SWIGLU_BWD: acc = dh over F columns; pre/dpre [.., 2F] interleaved
+          // The matching 64-column pre chunk (32 gate | 32 up, 128 B per row)
+          // is TMA-loaded into the staging tile, transformed in place into
+          // d[gate|up] and TMA-stored: pre and dpre share the layout.  The
+          // load of chunk c+1 is issued before chunk c is processed.
+          int nch = 0;
+          while (nch < BN / 32 && tl.n0 + nch * 32 < p.N) ++nch;
+          auto load_pre = [&](int c, uint32_t ctr, bool prologue) {
+            if (threadIdx.x == 128) {
+              if (prologue) bulk_wait_read<C::NSTG - 1>();
+              else bulk_wait_read<C::NSTG - 2>();
+              const uint32_t sl = ctr % C::NSTG;
+              mbar_expect_tx(ld_bar + 8 * sl, STG_BYTES);
+              tma_load_3d(&map_h, stg + sl * STG_BYTES, ld_bar + 8 * sl,
+                          (int)(((tl.n0 + c * 32) / 32) * 64), crow, 0);
+            }
+          };
+          if (nch > 0) load_pre(0, (uint32_t)stgr.buf, true);
 #pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            const int64_t n = tl.n0 + c * 32;
-            if (n >= p.N) break;
+          for (int c = 0; c < nch; ++c) {
+            const uint32_t ctr = (uint32_t)stgr.buf;
+            if (c + 1 < nch) load_pre(c + 1, ctr + 1, false);
             uint32_t v[32];
             tmem_ld32(t_row + c * 32, v);
-            const int64_t pc = (n / 32) * 64;
+            const uint32_t sl = ctr % C::NSTG;
+            mbar_wait(ld_bar + 8 * sl, (ld_par >> sl) & 1u);
+            ld_par ^= 1u << sl;
+            const uint32_t rowp = stg + sl * STG_BYTES + (uint32_t)r * 128;
+            uint4 o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = ld_shared_v4(rowp + ((uint32_t)(j ^ (r & 7)) << 4));
             float g[32], u[32], dg[32], du[32];
-            load_row32_bf16(p.PRE, row * p.ldpre + pc, g);
-            load_row32_bf16(p.PRE, row * p.ldpre + pc + 32, u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t* gw = reinterpret_cast<const uint32_t*>(&o[j]);
+              const uint32_t* uw = reinterpret_cast<const uint32_t*>(&o[4 + j]);
+#pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                const float2 a = unpack_bf16(gw[w]), b = unpack_bf16(uw[w]);
+                g[8 * j + 2 * w] = a.x; g[8 * j + 2 * w + 1] = a.y;
+                u[8 * j + 2 * w] = b.x; u[8 * j + 2 * w + 1] = b.y;
+              }
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float d = __uint_as_float(v[i]);
@@ -752,11 +795,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               dg[i] = d * u[i] * s * (1.f + g[i] * (1.f - s));
               du[i] = d * g[i] * s;
             }
-            uint4 o[8];
             pack32_bf16(dg, o);
             pack32_bf16(du, o + 4);
-            st_row_chunk(stgr.acquire(), r, o);
-            stgr.issue(&map_c, (int)pc, crow, 0, false);
+            st_row_chunk(stg + sl * STG_BYTES, r, o);
+            stgr.issue(&map_c, (int)(((tl.n0 + c * 32) / 32) * 64), crow, 0, false);
           }
         }
       } else if (p.epi == EPI_STORE) {
@@ -984,11 +1026,14 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
     const uint64_t ccols = a->epilogue == 2 ? 2 * (uint64_t)a->N : (uint64_t)a->N;
     const uint64_t csg = a->grouped_dim == 0 ? (uint64_t)a->ldc * crows : (uint64_t)a->c_sg;
     rc = make_map(&mc, a->C, ccols, crows, cg_n, (uint64_t)a->ldc, csg, BM, of32);
-    if (rc == B200MOE_OK && a->epilogue == 1)
+    if (rc == B200MOE_OK && a->epilogue == 1)  // h [R, F]
       rc = make_map(&mh, a->H, (uint64_t)a->N / 2, R, 1, (uint64_t)a->ldh, (uint64_t)a->ldh * R, BM);
+    else if (rc == B200MOE_OK && a->epilogue == 2)  // pre [R, 2F], read by the epilogue
+      rc = make_map(&mh, a->PRE, 2 * (uint64_t)a->N, R, 1, (uint64_t)a->ldpre, (uint64_t)a->ldpre * R, BM);
     else
       mh = mc;
-    use_tma = rc == B200MOE_OK && (a->ldc % 8 == 0) && (a->epilogue != 1 || a->ldh % 8 == 0);
+    use_tma = rc == B200MOE_OK && (a->ldc % 8 == 0) && (a->epilogue != 1 || a->ldh % 8 == 0) &&
+              (a->epilogue != 2 || a->ldpre % 8 == 0);
     if (rc != B200MOE_OK) mc = mh = ma;  // fall back to direct stores
   } else {
     mc = mh = ma;

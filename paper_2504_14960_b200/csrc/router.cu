@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(1024) plan_scan_kernel(int32_t* __restrict__ c
       offsets[e] = o;
       poffsets[e] = po;
       o += kept_cnt[e];
-      po += (kept_cnt[e] + align - 1) / align * align;
+      // align < 0: pad-to-capacity, every segment has exactly -align rows
+      po += align > 0 ? (kept_cnt[e] + align - 1) / align * align : -align;
     }
     offsets[E] = o;
     poffsets[E] = po;

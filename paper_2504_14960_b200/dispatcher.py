@@ -283,8 +283,13 @@ class RankLayer:
 
     def __init__(self, params: GatingParams, weights: X.ExpertWeights, topology: ParallelTopology,
                  groups: LayerGroups, rank: int, dtype, device, seq_len=None, check=False,
-                 shared: Optional[X.ExpertWeights] = None):
+                 shared: Optional[X.ExpertWeights] = None, pad_to_capacity: bool = False):
         self.shared_pk = None if shared is None else shared.packed(dtype, device)
+        # pad-to-capacity (BASELINE C3): every expert segment holds exactly
+        # round_up(cap, ALIGN) rows, so all exchange sizes are static and the
+        # layer never synchronises with the host.  Sub-sequence dropping only
+        # (the per-rank capacity bounds every segment).
+        self.pad_to_capacity = pad_to_capacity
         self.params = params
         self.topo = topology
         self.g = groups
@@ -346,13 +351,25 @@ class RankLayer:
             else:
                 dec.kept = kept_mask(dec, T, E, p).bool()
         kept_in = None if p.dropless else dec.kept.to(torch.uint8).contiguous()
-        plan = K.dispatch_plan(dec.experts, dec.gates, E, cap=0, kept_in=kept_in)
+        seg = 0
+        if self.pad_to_capacity and not p.dropless and p.drop_mode != DROP_FULLSEQUENCE:
+            cap = capacity_limit(p.capacity_factor, T, E)
+            seg = (cap + ALIGN - 1) // ALIGN * ALIGN
+            plan = K.dispatch_plan(dec.experts, dec.gates, E, cap=cap, kept_in=kept_in, align=-seg)
+        else:
+            plan = K.dispatch_plan(dec.experts, dec.gates, E, cap=0, kept_in=kept_in)
+        self.seg = seg
+        self.align = -seg if seg else ALIGN
         saved = {"x": x, "dec": dec, "plan": plan, "logits": logits}
         if self.single:
             # padded expert-major layout straight from the plan; group sizes stay on device
-            R = T * k + E * (ALIGN - 1)
-            R = (R + ALIGN - 1) // ALIGN * ALIGN
-            xp = K.permute(x, plan.gemm_row, R, poffsets=plan.poffsets, counts=plan.counts, E=E)
+            if seg:
+                R = E * seg
+            else:
+                R = T * k + E * (ALIGN - 1)
+                R = (R + ALIGN - 1) // ALIGN * ALIGN
+            xp = K.permute(x, plan.gemm_row, R, poffsets=plan.poffsets, counts=plan.counts, E=E,
+                           align=self.align)
             goff = plan.poffsets
             pre, h, y = X.ffn_forward(xp, goff, E, None, self.pk, R)
             ys = self._shared_forward(x, saved)
@@ -371,8 +388,15 @@ class RankLayer:
     # sender's layout exactly (combine reads it through gemm_row).
     def _exchange_plan(self, ctx, plan) -> ExchangePlan:
         g = self.g
-        counts = ctx.gather_counts(g.ep, plan.counts.to(torch.int64))  # [ep, E] host (one sync)
         ep_pos = g.ep.index(self.rank)
+        if self.seg:
+            # pad-to-capacity: static sizes, no count exchange, no host sync
+            counts = np.full((len(g.ep), self.E), self.seg, dtype=np.int64)
+            etp_recv = None
+            if len(g.etp) > 1:
+                etp_recv = np.full((len(g.etp), len(g.ep) * self.L), self.seg, dtype=np.int64)
+            return exchange_plan(counts, ep_pos, self.L, etp_recv, ALIGN)
+        counts = ctx.gather_counts(g.ep, plan.counts.to(torch.int64))  # [ep, E] host (one sync)
         mine = exchange_plan(counts, ep_pos, self.L, None, ALIGN)
         if len(g.etp) > 1:
             etp_recv = ctx.gather_counts(g.etp, torch.as_tensor(mine.recv_padded.reshape(-1)))
@@ -412,7 +436,8 @@ class RankLayer:
         E = self.E
         xpl = self._exchange_plan(ctx, plan)
         R_send = int(sum(xpl.send_splits))
-        xs = K.permute(x, plan.gemm_row, max(R_send, 1), poffsets=plan.poffsets, counts=plan.counts, E=E)
+        xs = K.permute(x, plan.gemm_row, max(R_send, 1), poffsets=plan.poffsets, counts=plan.counts, E=E,
+                       align=self.align)
         R_recv = int(sum(xpl.recv_splits))
         xr = torch.empty((max(R_recv, 1), H), dtype=x.dtype, device=x.device)
         ctx.a2a_single(self.g.ep, xs, xpl.send_splits, xr, xpl.recv_splits)
@@ -444,7 +469,7 @@ class RankLayer:
         E = self.E
         if self.single:
             dyp, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"], poffsets=plan.poffsets,
-                                        counts=plan.counts, E=E)
+                                        counts=plan.counts, E=E, align=self.align)
             dxp, dw1g, dw2g = X.ffn_backward(dyp, sv["xp"], sv["pre"], sv["h"], sv["goff"], sv["G"],
                                             None, self.pk, sv["R"])
             dw1p, dw2p = dw1g, dw2g
@@ -452,7 +477,7 @@ class RankLayer:
         else:
             xpl = sv["xpl"]
             dys, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"], poffsets=plan.poffsets,
-                                        counts=plan.counts, E=E)
+                                        counts=plan.counts, E=E, align=self.align)
             dyr = torch.empty((max(sv["R_recv"], 1), H), dtype=u.dtype, device=u.device)
             ctx.a2a_single(self.g.ep, dys, xpl.send_splits, dyr, xpl.recv_splits)
             dyp = self._gather_blocks(ctx, xpl, dyr[:sv["R_recv"]])
@@ -501,7 +526,8 @@ def _validate(blocks, topology, params, seq_len):
 
 def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingParams, world,
                 seq_len: Optional[int] = None, workers: Optional[int] = None, *, dtype=None,
-                check_finite_inputs: bool = True, shared_weights: Optional[X.ExpertWeights] = None):
+                check_finite_inputs: bool = True, shared_weights: Optional[X.ExpertWeights] = None,
+                pad_to_capacity: bool = False):
     """Run the MoE layer forward on every rank of ``world`` (dispatcher.py:246-384).
 
     ``world`` is a LocalWorld (all ranks in this process) or an NcclWorld
@@ -523,7 +549,8 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
         dev = getattr(world, "device", torch.device("cuda"))
         dt = dtype or (b.values.dtype if b.values.dtype in (torch.float32, torch.bfloat16) else torch.float32)
         layer = RankLayer(params, w, topology, _rank_groups(topology, groups, rank), rank, dt, dev,
-                          seq_len, check=check_finite_inputs, shared=shared_weights)
+                          seq_len, check=check_finite_inputs, shared=shared_weights,
+                          pad_to_capacity=pad_to_capacity)
         out, saved = layer.forward(ctx, b.values, b.positions)
         saved["layer"] = layer
         return out, saved

@@ -285,3 +285,34 @@ def test_c4_flavour_shared_expert_vs_oracle(dtype, tol):
     assert O.rel_err(res.shared_grads[1].cpu().numpy(), g[5][1]) < tol
     for e in range(0, E, 7):
         assert O.rel_err(res.expert_grads[(0, 0)][0][e].cpu().numpy(), g[3][e]) < tol
+
+
+@pytest.mark.parametrize("world,ep,etp,tp", [(1, 1, 1, 1), (4, 2, 2, 2), (2, 2, 1, 1)])
+def test_pad_to_capacity_equals_unpadded(world, ep, etp, tp):
+    """C3 flavour: CF=1 dropping with pad-to-capacity (static segment sizes,
+    no count exchange) gives the same outputs and gradients as the
+    count-driven layout (no reference exists for padding; results must not
+    change) -- fp32, emulated ranks."""
+    E, k, H, F, seq, seed = 8, 2, 128, 256, 512, 21
+    topo = B.ParallelTopology(world_size=world, tp=tp, ep=ep, etp=etp)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=1.0)
+    weights = B.init_expert_weights(E, H, F, etp, seed, ep_size=ep, activation="swiglu")
+    _, blocks = B.fabricate_token_blocks(topo, seq, topo.dp, H, seed)
+    _, ups = B.fabricate_upstream(topo, seq, topo.dp, H, seed)
+    runs = []
+    for pad in (False, True):
+        outs, ctx = B.moe_forward(blocks, weights, topo, params, B.LocalWorld(world), seq_len=seq,
+                                  pad_to_capacity=pad)
+        res = B.moe_backward(ups, ctx)
+        runs.append((outs, res, ctx))
+    (o0, r0, c0), (o1, r1, c1) = runs
+    for r in range(world):
+        np.testing.assert_array_equal(c0.per_rank[r]["decision"].kept.cpu().numpy(),
+                                      c1.per_rank[r]["decision"].kept.cpu().numpy())
+        assert c1.per_rank[r]["layer"].seg > 0
+        assert O.rel_err(o1[r].cpu().numpy(), o0[r].cpu().numpy()) < 1e-6
+        assert O.rel_err(r1.input_grads[r].cpu().numpy(), r0.input_grads[r].cpu().numpy()) < 1e-6
+    assert O.rel_err(r1.w_g_grad.cpu().numpy(), r0.w_g_grad.cpu().numpy()) < 1e-6
+    for key in r0.expert_grads:
+        for a, b in zip(r0.expert_grads[key][0], r1.expert_grads[key][0]):
+            assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-6
