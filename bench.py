@@ -28,6 +28,19 @@ sys.path.insert(0, ROOT)
 METRIC = "MoE-layer fwd+bwd tokens/s"
 UNIT = "tokens/s"
 
+# BASELINE.json configs[1..4] (configs[0] is the CPU-oracle case); per-GPU
+# token counts from SURVEY.md §8.  etp applies when n_gpus >= 2.
+CONFIGS = {
+    "c2": dict(name="Mixtral-8x7B MoE layer (C2)", E=8, k=2, H=4096, F=14336, T=16384, cf=None,
+               shared=0, etp=1, pad=False),
+    "c3": dict(name="Mixtral-8x7B, CF=1.0 pad-to-capacity, EP x ETP2 (C3)", E=8, k=2, H=4096,
+               F=14336, T=16384, cf=1.0, shared=0, etp=2, pad=True),
+    "c4": dict(name="Qwen2-57B-A14B MoE layer + shared expert (C4)", E=64, k=8, H=3584, F=2560,
+               T=16384, cf=None, shared=20480, etp=1, pad=False),
+    "c5": dict(name="Mixtral-8x22B MoE layer, seq 32K over TP2xCP2 (C5)", E=8, k=2, H=6144,
+               F=16384, T=8192, cf=None, shared=0, etp=1, pad=False),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -35,11 +48,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--tokens", type=int, default=16384, help="tokens per GPU")
-    ap.add_argument("--hidden", type=int, default=4096)
-    ap.add_argument("--ffn", type=int, default=14336)
-    ap.add_argument("--experts", type=int, default=8)
-    ap.add_argument("--topk", type=int, default=2)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default c2, the metric's headline)")
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per GPU (override)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
@@ -166,17 +177,36 @@ def run_reference(a):
     }), flush=True)
 
 
+def resolve(a):
+    c = dict(CONFIGS[a.config])
+    if a.tokens:
+        c["T"] = a.tokens
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    c["etp_eff"] = c["etp"] if world >= 2 else 1
+    c["ep_eff"] = max(1, world // c["etp_eff"])
+    a.experts, a.topk, a.hidden, a.ffn = c["E"], c["k"], c["H"], c["F"]
+    a.tokens = c["T"]
+    a.cfg = c
+    return c
+
+
 def workload_config(a):
-    return {"workload": f"Mixtral-8x7B MoE layer (C2 shape): E{a.experts} top-{a.topk} H{a.hidden} "
-                        f"F{a.ffn} SwiGLU, {a.tokens} tokens/GPU, dropless",
-            "tokens_per_gpu": a.tokens, "experts": a.experts, "top_k": a.topk,
-            "hidden": a.hidden, "ffn": a.ffn, "activation": "swiglu",
-            "parallelism": f"ep{a.gpus}", "l2": "per-step working set >10 GB (>> 126 MB L2)"}
+    c = a.cfg
+    drop = "dropless" if c["cf"] is None else f"CF={c['cf']}" + (" pad-to-capacity" if c["pad"] else "")
+    sh = f" + shared expert F={c['shared']}" if c["shared"] else ""
+    return {"workload": f"{c['name']}: E{c['E']} top-{c['k']} H{c['H']} F{c['F']} SwiGLU{sh}, "
+                        f"{c['T']} tokens/GPU, {drop}",
+            "config": a.config, "tokens_per_gpu": c["T"], "experts": c["E"], "top_k": c["k"],
+            "hidden": c["H"], "ffn": c["F"], "shared_ffn": c["shared"], "activation": "swiglu",
+            "capacity_factor": c["cf"], "pad_to_capacity": c["pad"],
+            "parallelism": f"ep{c['ep_eff']}" + (f"xetp{c['etp_eff']}" if c["etp_eff"] > 1 else ""),
+            "l2": "per-step working set >10 GB (>> 126 MB L2); L2 also flushed between steps"}
 
 
 # --------------------------------------------------------------- GPU arm
 def main():
     a = parse()
+    resolve(a)
     if a.impl == "reference":
         run_reference(a)
         return
@@ -198,22 +228,33 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     _lib.load()
 
-    E, k, H, F, T = a.experts, a.topk, a.hidden, a.ffn, a.tokens
-    topo = B.ParallelTopology(world_size=world, ep=world)
+    c = a.cfg
+    E, k, H, F, T = c["E"], c["k"], c["H"], c["F"], c["T"]
+    ep, etp = c["ep_eff"], c["etp_eff"]
+    topo = B.ParallelTopology(world_size=world, ep=ep, etp=etp, tp=etp)
     seed = 0
     rng = np.random.default_rng([seed, 0])
     bnd = 1.0 / np.sqrt(H)
     wg = torch.as_tensor(rng.uniform(-bnd, bnd, size=(H, E)), dtype=torch.float32)
-    params = B.GatingParams(w_g=wg, k=k)
-    L_ = E // world
-    # random-init local experts directly on the device (U(+-1/sqrt(H)))
+    params = B.GatingParams(w_g=wg, k=k, capacity_factor=c["cf"])
+    L_ = E // ep
+    etp_idx, ep_idx, _, _ = topo.moe_coords(rank)
+    Fs = F // etp
+    # random-init this rank's expert shards directly on the device (U(+-1/sqrt(H)))
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
-    w1 = [((torch.rand((H, 2 * F), generator=g, device=dev) * 2 - 1) * bnd) for _ in range(L_)]
-    w2 = [((torch.rand((F, H), generator=g, device=dev) * 2 - 1) * bnd) for _ in range(L_)]
-    ep_idx = rank
-    weights = B.ExpertWeights(tuple(range(ep_idx * L_, (ep_idx + 1) * L_)), w1, w2, "swiglu", 0, 1)
+    w1 = [((torch.rand((H, 2 * Fs), generator=g, device=dev) * 2 - 1) * bnd) for _ in range(L_)]
+    w2 = [((torch.rand((Fs, H), generator=g, device=dev) * 2 - 1) * bnd) for _ in range(L_)]
+    weights = B.ExpertWeights(tuple(range(ep_idx * L_, (ep_idx + 1) * L_)), w1, w2, "swiglu",
+                              etp_idx, etp)
     weights.packed(torch.bfloat16, dev)
     del w1, w2
+    shared = None
+    if c["shared"]:
+        S_ = c["shared"]
+        shared = B.ExpertWeights((0,), [(torch.rand((H, 2 * S_), generator=g, device=dev) * 2 - 1) * bnd],
+                                 [(torch.rand((S_, H), generator=g, device=dev) * 2 - 1) * bnd],
+                                 "swiglu", 0, 1)
+        shared.packed(torch.bfloat16, dev)
     groups = B.generate_parallel_groups(topo)
     if world > 1:
         nw = B.NcclWorld()
@@ -223,7 +264,7 @@ def main():
         nw = B.LocalWorld(1, dev)
         ctx = B.collectives.LocalRankContext(nw, 0)
     layer = D.RankLayer(params, weights, topo, D._rank_groups(topo, groups, rank), rank,
-                        torch.bfloat16, dev)
+                        torch.bfloat16, dev, shared=shared, pad_to_capacity=c["pad"])
     x = torch.randn((T, H), generator=g, device=dev).to(torch.bfloat16)
     u = torch.randn((T, H), generator=g, device=dev).to(torch.bfloat16)
     positions = torch.arange(T, dtype=torch.int64) + rank * T
@@ -299,8 +340,15 @@ def main():
         a2a = {"busbw_gbs": busbw, "nominal_gbs": 900.0, "frac_nominal": busbw / 900.0,
                "ms_per_step": t_a2a * 1e3, "calls_per_step": len(a2a_events),
                "bytes_per_step": sent, "impl": "NCCL all_to_all_single (grouped P2P)"}
-    P = T * k  # kept pairs per GPU (dropless)
-    flops_step = 18.0 * P * H * F  # SwiGLU fwd 6PHF + bwd 12PHF
+    # kept (token, expert) pairs of the last step, summed over ranks; each
+    # pair costs 18*H*F flop fwd+bwd with SwiGLU (6PHF + 12PHF),
+    # shared expert 18*T*H*Fs; per-GPU share of the whole job
+    _, sv_last = layer.forward(ctx, x, positions)
+    kept = torch.tensor([float(sv_last["plan"].counts.sum())], device=dev)
+    if world > 1:
+        dist.all_reduce(kept)
+    P = float(kept) / world
+    flops_step = 18.0 * P * H * F + 18.0 * T * H * c["shared"]
     gemm_ms = sum(ms_ for _, ms_ in per_launch)
     achieved = flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     roof = {"bound": "tensor", "kernel": "gemm_tc (grouped SwiGLU FFN, 6 launches/step)",
@@ -326,12 +374,13 @@ def main():
         blocks[rank] = B.TokenBlock(xh, positions)
         ups = [None] * world
         ups[rank] = uh
-        wmap = {(rank, 0): weights}
+        wmap = {(ep_idx, etp_idx): weights}
         api_world = nw
 
         def e2e_step():
             outs, fctx = B.moe_forward(blocks, wmap, topo, params, api_world, dtype=torch.bfloat16,
-                                       check_finite_inputs=False)
+                                       check_finite_inputs=False, shared_weights=shared,
+                                       pad_to_capacity=c["pad"])
             yh.copy_(outs[rank], non_blocking=True)
             res = B.moe_backward(ups, fctx)
             dxh.copy_(res.input_grads[rank], non_blocking=True)
