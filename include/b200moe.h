@@ -170,6 +170,7 @@ typedef struct {
   const int32_t* group_off;
   const int32_t* group_expert;
   int64_t max_rows;  /* upper bound of group_off[G] (buffer capacity) */
+  int dtype_b;       /* dtype of B (may differ from A's dtype_in) */
 } b200moe_gemm_args;
 
 /* Portable SIMT implementation (fp32 parity mode and cross-check). */

@@ -36,7 +36,7 @@ class GemmArgs(ctypes.Structure):
         ("A", P), ("a_sm", I64), ("a_sk", I64),
         ("B", P), ("b_sg", I64), ("b_sk", I64), ("b_sn", I64),
         ("C", P), ("c_sg", I64), ("ldc", I64),
-        ("group_off", P), ("group_expert", P), ("max_rows", I64),
+        ("group_off", P), ("group_expert", P), ("max_rows", I64), ("dtype_b", I32),
     ]
 
 

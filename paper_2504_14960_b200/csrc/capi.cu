@@ -195,10 +195,9 @@ int b200moe_combine(const void* rows, int dtype, int64_t T, int64_t H, int k,
 
 int b200moe_gemm_simt(const b200moe_gemm_args* a, void* stream) {
   REQUIRE(a, "gemm_simt: null args");
-  REQUIRE(dt_ok(a->dtype_in) && dt_ok(a->dtype_out), "gemm_simt: bad dtype");
+  REQUIRE(dt_ok(a->dtype_in) && dt_ok(a->dtype_out) && dt_ok(a->dtype_b), "gemm_simt: bad dtype");
   REQUIRE(a->grouped_dim == 0 || a->grouped_dim == 1, "gemm_simt: bad grouped_dim");
   REQUIRE(a->G >= 1 && a->N >= 1, "gemm_simt: bad G/N");
-  REQUIRE(!a->accumulate || a->dtype_out == B200MOE_F32, "gemm_simt: accumulate needs fp32 out");
   REQUIRE(a->A && a->B && a->C && a->group_off, "gemm_simt: null pointer");
   if (a->grouped_dim == 0) REQUIRE(a->K >= 1 && a->max_rows >= 0, "gemm_simt: bad K/max_rows");
   else REQUIRE(a->M >= 1, "gemm_simt: bad M");

@@ -9,12 +9,12 @@ namespace b200moe {
 
 constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
 
-template <typename Tin, typename Tout>
+template <typename Tin, typename TinB, typename Tout>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(b200moe_gemm_args a) {
   __shared__ float As[SB_K][SB_M + 4];
   __shared__ float Bs[SB_K][SB_N + 4];
   const Tin* A = static_cast<const Tin*>(a.A);
-  const Tin* B = static_cast<const Tin*>(a.B);
+  const TinB* B = static_cast<const TinB*>(a.B);
   Tout* C = static_cast<Tout*>(a.C);
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -126,17 +126,21 @@ int gemm_simt(const b200moe_gemm_args* a, cudaStream_t st) {
     grid.y = (unsigned)ceil_div(a->M, SB_M);
     grid.z = (unsigned)a->G;
   }
-  if (a->dtype_in == B200MOE_BF16) {
-    if (a->dtype_out == B200MOE_BF16)
-      gemm_simt_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, st>>>(*a);
-    else
-      gemm_simt_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(*a);
-  } else {
-    if (a->dtype_out == B200MOE_BF16)
-      gemm_simt_kernel<float, __nv_bfloat16><<<grid, 256, 0, st>>>(*a);
-    else
-      gemm_simt_kernel<float, float><<<grid, 256, 0, st>>>(*a);
+  using bf = __nv_bfloat16;
+  const int ka = a->dtype_in == B200MOE_BF16, kb = a->dtype_b == B200MOE_BF16,
+            kc = a->dtype_out == B200MOE_BF16;
+#define GS(TA, TB, TC) gemm_simt_kernel<TA, TB, TC><<<grid, 256, 0, st>>>(*a)
+  switch (ka * 4 + kb * 2 + kc) {
+    case 0: GS(float, float, float); break;
+    case 1: GS(float, float, bf); break;
+    case 2: GS(float, bf, float); break;
+    case 3: GS(float, bf, bf); break;
+    case 4: GS(bf, float, float); break;
+    case 5: GS(bf, float, bf); break;
+    case 6: GS(bf, bf, float); break;
+    default: GS(bf, bf, bf); break;
   }
+#undef GS
   B200MOE_CHECK_LAUNCH("gemm_simt");
   return B200MOE_OK;
 }

@@ -492,8 +492,12 @@ class RankLayer:
         dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
                           p.renormalize_topk)
         dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
-        dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT, out=dx_sh,
-                       accumulate=dx_sh is not None)
+        if E <= 8:  # router term fused into the combine (w_g^T chunks reused per warp)
+            dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT, out=dx_sh,
+                           accumulate=dx_sh is not None)
+        else:
+            dx = K.combine(rows, sv["pair_row"], T, gates=None, out=dx_sh, accumulate=dx_sh is not None)
+            K.router_term(dz, self.wg, dx)
         dwg = K.router_wgrad(x, dz)
         return dx, dwg, dw1p, dw2p
 

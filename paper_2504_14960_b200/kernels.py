@@ -30,15 +30,50 @@ def _sp():
     return L.stream_ptr()
 
 
+_ROWS_CACHE = {}
+
+
+def _single_group(rows: int, device) -> torch.Tensor:
+    """Device [0, rows] int32 (one GEMM group spanning all rows), cached."""
+    key = (rows, str(device))
+    t = _ROWS_CACHE.get(key)
+    if t is None:
+        t = torch.tensor([0, rows], dtype=torch.int32).pin_memory().to(device, non_blocking=True)
+        _ROWS_CACHE[key] = t
+    return t
+
+
+def dense_gemm(A, B, C, *, M: int, N: int, K: int, a_sm, a_sk, b_sk, b_sn, ldc, accumulate=False):
+    """C (+)= A @ B on CUDA cores in fp32 (mixed input dtypes allowed): the
+    skinny router GEMMs (x W_g, dz W_g^T) when E is too large for the fused
+    warp kernels."""
+    return gemm_simt(A, B, C, grouped_dim=0, G=1, M=M, N=N, K=K, a_sm=a_sm, a_sk=a_sk, b_sg=0,
+                     b_sk=b_sk, b_sn=b_sn, c_sg=0, ldc=ldc, group_off=_single_group(M, A.device),
+                     max_rows=M, accumulate=accumulate)
+
+
 def router_logits(x: torch.Tensor, w_g: torch.Tensor) -> torch.Tensor:
     T, H = x.shape
     E = w_g.shape[1]
     _cuda(x, "x")
     _cuda(w_g, "w_g", torch.float32)
     out = torch.empty((T, E), dtype=torch.float32, device=x.device)
+    if E > 8 and T > 0:
+        # tiled fp32 GEMM (64x64 tiles) instead of the per-token warp kernel
+        return dense_gemm(x, w_g, out, M=T, N=E, K=H, a_sm=H, a_sk=1, b_sk=E, b_sn=1, ldc=E)
     L.call("b200moe_router_logits", L.ptr(x), L.dtype_code(x.dtype), L.ptr(w_g), T, H, E,
            L.ptr(out), _sp())
     return out
+
+
+def router_term(dz: torch.Tensor, w_g: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """out += dz @ w_g^T  (dispatcher.py:490) as a tiled GEMM."""
+    T, E = dz.shape
+    H = w_g.shape[0]
+    if T == 0:
+        return out
+    return dense_gemm(dz, w_g, out, M=T, N=H, K=E, a_sm=E, a_sk=1, b_sk=1, b_sn=E, ldc=H,
+                      accumulate=True)
 
 
 def router_topk(logits: torch.Tensor, k: int, gate_fn: int, renorm: bool, want_f64: bool = False):
@@ -170,7 +205,7 @@ def gemm_simt(A, B, C, *, grouped_dim: int, G: int, M: int, N: int, K: int, a_sm
         accumulate=int(accumulate), G=G, M=M, N=N, K=K,
         A=L.ptr(A), a_sm=a_sm, a_sk=a_sk, B=L.ptr(B), b_sg=b_sg, b_sk=b_sk, b_sn=b_sn,
         C=L.ptr(C), c_sg=c_sg, ldc=ldc, group_off=L.ptr(group_off),
-        group_expert=L.ptr(group_expert), max_rows=max_rows)
+        group_expert=L.ptr(group_expert), max_rows=max_rows, dtype_b=L.dtype_code(B.dtype))
     L.call("b200moe_gemm_simt", ctypes.byref(args), _sp())
     return C
 
