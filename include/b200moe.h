@@ -171,6 +171,7 @@ typedef struct {
   const int32_t* group_expert;
   int64_t max_rows;  /* upper bound of group_off[G] (buffer capacity) */
   int dtype_b;       /* dtype of B (may differ from A's dtype_in) */
+  const int32_t* group_end; /* nullable: group g = [group_off[g], group_end[g]) (gaps allowed) */
 } b200moe_gemm_args;
 
 /* Portable SIMT implementation (fp32 parity mode and cross-check). */
@@ -202,6 +203,7 @@ typedef struct {
   void* H; int64_t ldh;
   const void* PRE; int64_t ldpre;
   int num_ctas;
+  const int32_t* group_end; /* nullable: group g = [group_off[g], group_end[g]) (gaps allowed) */
 } b200moe_tc_gemm_args;
 
 B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);

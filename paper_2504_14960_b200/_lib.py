@@ -37,6 +37,7 @@ class GemmArgs(ctypes.Structure):
         ("B", P), ("b_sg", I64), ("b_sk", I64), ("b_sn", I64),
         ("C", P), ("c_sg", I64), ("ldc", I64),
         ("group_off", P), ("group_expert", P), ("max_rows", I64), ("dtype_b", I32),
+        ("group_end", P),
     ]
 
 

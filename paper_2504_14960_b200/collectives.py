@@ -172,6 +172,29 @@ class _Aborted(BaseException):
     pass
 
 
+class _Done:
+    """Handle of an already-completed (emulated) collective."""
+
+    def wait(self):
+        return None
+
+
+class _Work:
+    """Handle of an in-flight NCCL collective; wait() makes the current
+    stream wait for it (no host synchronisation)."""
+
+    def __init__(self, work, prof=None):
+        self.work = work
+        self.prof = prof
+
+    def wait(self):
+        self.work.wait()
+        if self.prof is not None:
+            from . import _lib
+
+            _lib.PROFILE.end(*self.prof)
+
+
 class RankContext:
     """Per-rank handle (collectives.py:249-327 analogue)."""
 
@@ -244,14 +267,17 @@ class RankContext:
         raise NotImplementedError
 
     def a2a_single(self, group: Group, send: torch.Tensor, send_splits: Sequence[int],
-                   recv: torch.Tensor, recv_splits: Sequence[int]) -> None:
+                   recv: torch.Tensor, recv_splits: Sequence[int], async_op: bool = False):
         """Rows [sum(send_splits[:j]), +send_splits[j]) of ``send`` go to
-        member j; ``recv`` receives members' rows in ascending member order."""
+        member j; ``recv`` receives members' rows in ascending member order.
+        With async_op the call returns a handle whose wait() orders the
+        current stream after the transfer (emulated worlds complete eagerly)."""
         so = np.concatenate(([0], np.cumsum(send_splits))).astype(np.int64)
         ro = np.concatenate(([0], np.cumsum(recv_splits))).astype(np.int64)
         sends = [(group[j], send[so[j]:so[j + 1]]) for j in range(len(group))]
         recvs = [(group[j], recv[ro[j]:ro[j + 1]]) for j in range(len(group))]
         self.p2p(group, sends, recvs)
+        return _Done() if async_op else None
 
     def gather_counts(self, group: Group, counts: torch.Tensor) -> np.ndarray:
         """[len(group), n] int64 on the host: row i = member i's vector."""
@@ -399,7 +425,7 @@ class NcclRankContext(RankContext):
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
 
-    def a2a_single(self, group, send, send_splits, recv, recv_splits):
+    def a2a_single(self, group, send, send_splits, recv, recv_splits, async_op=False):
         from . import _lib
 
         _check_group(self.rank, group)
@@ -407,12 +433,17 @@ class NcclRankContext(RankContext):
         if len(group) == 1:
             if ns:
                 recv[:nr].copy_(send[:ns])
-            return
+            return _Done() if async_op else None
         e0 = _lib.PROFILE.begin() if _lib.PROFILE.on else None
-        self.world.dist.all_to_all_single(recv[:nr], send[:ns], [int(v) for v in recv_splits],
-                                          [int(v) for v in send_splits], group=self.world.pg(group))
+        work = self.world.dist.all_to_all_single(
+            recv[:nr], send[:ns], [int(v) for v in recv_splits], [int(v) for v in send_splits],
+            group=self.world.pg(group), async_op=async_op)
+        if async_op:
+            # (profiled span = issue .. wait, i.e. including overlapped compute)
+            return _Work(work, None if e0 is None else (f"nccl:a2a_async[{ns}->{nr} rows]", e0))
         if e0 is not None:
             _lib.PROFILE.end(f"nccl:a2a[{ns}->{nr} rows]", e0)
+        return None
 
     def _all_reduce(self, group, values, op):
         _check_group(self.rank, group)

@@ -293,6 +293,71 @@ __global__ void __launch_bounds__(256) combine_vec_kernel(
   }
 }
 
+// Gather-sum without the router term: one warp per token (high occupancy),
+// each lane owns 8 columns per step and keeps UNR steps x k row loads in
+// flight.
+template <typename Tin, typename Tout, int KMAX, int UNR>
+__global__ void __launch_bounds__(256) combine_gather_kernel(
+    const Tin* __restrict__ rows, int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_row,
+    const float* __restrict__ gates, Tout* __restrict__ out, int accumulate) {
+  static_assert(sizeof(Tin) == 2, "bf16 rows");
+  constexpr int V = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  int32_t r[KMAX];
+  float w[KMAX];
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    r[s] = s < k ? pair_row[t * k + s] : -1;
+    w[s] = (s < k && gates) ? gates[t * k + s] : 1.f;
+  }
+  for (int64_t h0 = (int64_t)lane * V; h0 < H; h0 += 32 * V * UNR) {
+    Vec16<Tin> v[UNR][KMAX];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t h = h0 + (int64_t)u * 32 * V;
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s)
+        if (r[s] >= 0 && h < H) v[u][s].raw = ld_nc_v4(rows + (int64_t)r[s] * H + h);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t h = h0 + (int64_t)u * 32 * V;
+      if (h >= H) break;
+      float acc[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = 0.f;
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (r[s] < 0) continue;
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = fmaf(w[s], to_f32(v[u][s].v[j]), acc[j]);
+      }
+      Tout* o = out + t * H + h;
+      if (accumulate) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] += to_f32(o[j]);
+      }
+      if (sizeof(Tout) == 2) {
+        Vec16<Tout> q;
+#pragma unroll
+        for (int j = 0; j < V; ++j) q.v[j] = from_f32<Tout>(acc[j]);
+        st_v4(o, q.raw);
+      } else {
+        Vec16<Tout> a, b;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          a.v[j] = from_f32<Tout>(acc[j]);
+          b.v[j] = from_f32<Tout>(acc[4 + j]);
+        }
+        st_v4(o, a.raw);
+        st_v4(o + 4, b.raw);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 #define KDISPATCH(k, MACRO)            \
   if (k <= 1) { MACRO(1); }            \
@@ -376,7 +441,18 @@ static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const i
                           int acc, cudaStream_t st) {
   constexpr int TPW = 4;
   const unsigned grid = (unsigned)ceil_div(ceil_div(Tn, TPW), 8);
-  if (H % 8 == 0) {
+  bool done = false;
+  if constexpr (sizeof(Tin) == 2) {
+    if (!dz && H % 8 == 0) {
+      const unsigned g1 = (unsigned)ceil_div(Tn, 8);
+#define CG1(KM) combine_gather_kernel<Tin, Tout, KM, (KM <= 2 ? 4 : (KM <= 4 ? 2 : 1))><<<g1, 256, 0, st>>>(rows, Tn, H, k, pr, gates, out, acc)
+      if (Tn > 0) { KDISPATCH(k, CG1) }
+#undef CG1
+      done = true;
+    }
+  }
+  if (done) {
+  } else if (H % 8 == 0) {
 #define CV(KM) combine_vec_kernel<Tin, Tout, KM, TPW><<<grid, 256, 0, st>>>(rows, Tn, H, k, pr, gates, dz, wgT, E, out, acc)
     if (Tn > 0) { KDISPATCH(k, CV) }
 #undef CV

@@ -27,11 +27,16 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(b200moe_gemm_args a) {
   if (a.grouped_dim == 0) {
     m_lo = (int64_t)blockIdx.y * SB_M;
     m_hi = m_lo + SB_M;
-    if (m_lo >= a.group_off[a.G]) return;
-    g_begin = 0;
-    while (g_begin < a.G && a.group_off[g_begin + 1] <= m_lo) ++g_begin;
-    g_end = g_begin;
-    while (g_end < a.G && a.group_off[g_end] < m_hi) ++g_end;
+    if (a.group_end) {  // explicit [begin, end) per group, possibly with gaps
+      g_begin = 0;
+      g_end = a.G;
+    } else {
+      if (m_lo >= a.group_off[a.G]) return;
+      g_begin = 0;
+      while (g_begin < a.G && a.group_off[g_begin + 1] <= m_lo) ++g_begin;
+      g_end = g_begin;
+      while (g_end < a.G && a.group_off[g_end] < m_hi) ++g_end;
+    }
   } else {
     g_begin = blockIdx.z;
     g_end = g_begin + 1;
@@ -41,9 +46,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(b200moe_gemm_args a) {
   }
   for (int g = g_begin; g < g_end; ++g) {
     int64_t mbase, mcount, kbase, K, b_off, c_off;
+    const int64_t gend = a.group_end ? a.group_end[g] : a.group_off[g + 1];
     if (a.grouped_dim == 0) {
       const int64_t lo = max(m_lo, (int64_t)a.group_off[g]);
-      const int64_t hi = min(m_hi, (int64_t)a.group_off[g + 1]);
+      const int64_t hi = min(m_hi, gend);
       if (hi <= lo) continue;
       mbase = lo;
       mcount = hi - lo;
@@ -56,7 +62,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(b200moe_gemm_args a) {
       mbase = m_lo;
       mcount = min((int64_t)SB_M, a.M - m_lo);
       kbase = a.group_off[g];
-      K = a.group_off[g + 1] - kbase;
+      K = gend - kbase;
       b_off = 0;
       c_off = (int64_t)g * a.c_sg;
     }

@@ -43,6 +43,7 @@ struct Params {
   int64_t M, N, K; // fixed extents (M for grouped-K, K for grouped-M)
   const int32_t* goff;
   const int32_t* gexp;
+  const int32_t* gend;  // nullable: explicit group ends (gaps between groups)
   int64_t max_rows;
   // epilogue
   int epi;
@@ -370,7 +371,7 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
   Tile r;
   r.g = lo;
   const int local = t - prefix[lo];
-  const int64_t g0 = p.goff[lo], g1 = p.goff[lo + 1];
+  const int64_t g0 = p.goff[lo], g1 = p.gend ? p.gend[lo] : p.goff[lo + 1];
   const int nt = (int)((p.N + BN - 1) / BN);
   int mb, nb;
   if (!p.grouped_k) {
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   for (int g = threadIdx.x; g < p.G; g += NUM_THREADS) {
     int tiles;
     if (!p.grouped_k) {
-      const int64_t rows = p.goff[g + 1] - p.goff[g];
+      const int64_t rows = (p.gend ? p.gend[g] : p.goff[g + 1]) - p.goff[g];
       tiles = (int)(((rows + p.tile_m - 1) / p.tile_m) * ((p.N + BN - 1) / BN));
     } else {
       tiles = (int)(((p.M + p.tile_m - 1) / p.tile_m) * ((p.N + BN - 1) / BN));
@@ -1048,6 +1049,7 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.K = a->K;
   p.goff = a->group_off;
   p.gexp = a->group_expert;
+  p.gend = a->group_end;
   p.max_rows = a->a_rows;
   p.epi = a->epilogue;
   p.act = a->act;

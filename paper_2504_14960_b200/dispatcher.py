@@ -290,6 +290,11 @@ class RankLayer:
         # layer never synchronises with the host.  Sub-sequence dropping only
         # (the per-rank capacity bounds every segment).
         self.pad_to_capacity = pad_to_capacity
+        # overlap the EP all-to-all with the FFN of the rank's own rows
+        # (B200MOE_OVERLAP=0 selects the serial exchange)
+        import os
+
+        self.overlap = os.environ.get("B200MOE_OVERLAP", "1") != "0"
         self.params = params
         self.topo = topology
         self.g = groups
@@ -431,9 +436,85 @@ class RankLayer:
             acc += q.float()
         return acc.to(full.dtype)
 
+    # ---- overlapped EP exchange (ETP = 1): while NCCL moves the remote rows,
+    # the rank's own rows (its self segment of the send buffer) run through
+    # the FFN; the remote segments follow once they land.
+    def _overlap_groups(self, xpl: ExchangePlan):
+        me = self.g.ep.index(self.rank)
+        L_ = self.L
+        dev = self.device
+        so_me = int(sum(xpl.send_splits[:me]))
+        n_self = int(xpl.send_splits[me])
+        self_pad = xpl.recv_padded[me]
+        soff = np.concatenate(([0], np.cumsum(self_pad))).astype(np.int64)
+        go, ge, gx = [], [], []
+        for s in range(len(self.g.ep)):
+            if s == me:
+                continue
+            for le in range(L_):
+                i = s * L_ + le
+                go.append(xpl.group_off[i])
+                ge.append(xpl.group_off[i + 1])
+                gx.append(le)
+        go.append(xpl.group_off[-1])  # bound for the elementwise kernels
+        pin = lambda v: torch.tensor(v, dtype=torch.int32).pin_memory().to(dev, non_blocking=True)  # noqa: E731
+        return dict(me=me, so_me=so_me, n_self=n_self, s_off=pin(soff.tolist()), G_self=L_,
+                    r_off=pin(go), r_end=pin(ge), r_exp=pin(gx), G_rem=len(gx))
+
+    def _forward_overlap(self, ctx, x, dec, plan, saved):
+        T, H = x.shape
+        E = self.E
+        xpl = self._exchange_plan(ctx, plan)
+        R_send, R_recv = int(sum(xpl.send_splits)), int(sum(xpl.recv_splits))
+        xs = K.permute(x, plan.gemm_row, max(R_send, 1), poffsets=plan.poffsets, counts=plan.counts, E=E,
+                       align=self.align)
+        xr = torch.empty((max(R_recv, 1), H), dtype=x.dtype, device=x.device)
+        work = ctx.a2a_single(self.g.ep, xs, xpl.send_splits, xr, xpl.recv_splits, async_op=True)
+        og = self._overlap_groups(xpl)
+        xs_self = xs[og["so_me"]:og["so_me"] + og["n_self"]]
+        s_pre, s_h, s_y = X.ffn_forward(xs_self, og["s_off"], og["G_self"], None, self.pk, og["n_self"])
+        work.wait()
+        r_pre, r_h, r_y = X.ffn_forward(xr, og["r_off"], og["G_rem"], og["r_exp"], self.pk, R_recv,
+                                        gend=og["r_end"])
+        ys = torch.empty((max(R_send, 1), H), dtype=x.dtype, device=x.device)
+        work = ctx.a2a_single(self.g.ep, r_y, xpl.recv_splits, ys, xpl.send_splits, async_op=True)
+        y_sh = self._shared_forward(x, saved)  # overlaps the return transfer
+        work.wait()
+        ys[og["so_me"]:og["so_me"] + og["n_self"]].copy_(s_y)  # self rows never left the GPU
+        out = K.combine(ys, plan.gemm_row, T, gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
+        saved.update(xs=xs, xr=xr, s_pre=s_pre, s_h=s_h, r_pre=r_pre, r_h=r_h, y=ys, og=og, xpl=xpl,
+                     pair_row=plan.gemm_row, R_send=R_send, R_recv=R_recv, overlap=True)
+        return out, saved
+
+    def _backward_overlap(self, ctx, u, sv, dec, plan):
+        H = u.shape[1]
+        E = self.E
+        xpl, og = sv["xpl"], sv["og"]
+        dys, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"], poffsets=plan.poffsets,
+                                    counts=plan.counts, E=E, align=self.align)
+        dyr = torch.empty((max(sv["R_recv"], 1), H), dtype=u.dtype, device=u.device)
+        work = ctx.a2a_single(self.g.ep, dys, xpl.send_splits, dyr, xpl.recv_splits, async_op=True)
+        a, n = og["so_me"], og["n_self"]
+        s_dx, s_dw1, s_dw2 = X.ffn_backward(dys[a:a + n], sv["xs"][a:a + n], sv["s_pre"], sv["s_h"],
+                                            og["s_off"], og["G_self"], None, self.pk, n)
+        work.wait()
+        r_dx, r_dw1, r_dw2 = X.ffn_backward(dyr, sv["xr"], sv["r_pre"], sv["r_h"], og["r_off"],
+                                            og["G_rem"], og["r_exp"], self.pk, sv["R_recv"],
+                                            gend=og["r_end"])
+        rows = torch.empty((max(sv["R_send"], 1), H), dtype=u.dtype, device=u.device)
+        work = ctx.a2a_single(self.g.ep, r_dx, xpl.recv_splits, rows, xpl.send_splits, async_op=True)
+        # per-expert weight grads: self groups are experts 0..L-1, remote groups cycle le
+        dw1p = s_dw1 + r_dw1.reshape(-1, self.L, *r_dw1.shape[1:]).sum(0)
+        dw2p = s_dw2 + r_dw2.reshape(-1, self.L, *r_dw2.shape[1:]).sum(0)
+        work.wait()
+        rows[a:a + n].copy_(s_dx)
+        return rows, dgates, dw1p, dw2p
+
     def _forward_exchange(self, ctx, x, dec, plan, saved):
         T, H = x.shape
         E = self.E
+        if len(self.g.etp) == 1 and self.overlap:
+            return self._forward_overlap(ctx, x, dec, plan, saved)
         xpl = self._exchange_plan(ctx, plan)
         R_send = int(sum(xpl.send_splits))
         xs = K.permute(x, plan.gemm_row, max(R_send, 1), poffsets=plan.poffsets, counts=plan.counts, E=E,
@@ -474,6 +555,8 @@ class RankLayer:
                                             None, self.pk, sv["R"])
             dw1p, dw2p = dw1g, dw2g
             rows = dxp
+        elif sv.get("overlap"):
+            rows, dgates, dw1p, dw2p = self._backward_overlap(ctx, u, sv, dec, plan)
         else:
             xpl = sv["xpl"]
             dys, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"], poffsets=plan.poffsets,

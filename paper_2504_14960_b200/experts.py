@@ -234,9 +234,11 @@ def _gemm(A, B, C, **kw):
 
 
 def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor],
-                pk: PackedExperts, max_rows: int):
+                pk: PackedExperts, max_rows: int, gend: Optional[torch.Tensor] = None):
     """pre = xp W1_g ; h = act(pre) ; y = h W2_g  for every group g
-    (experts.py:130-143 batched over groups).  Returns (pre, h, y)."""
+    (experts.py:130-143 batched over groups).  Returns (pre, h, y).
+    ``gend`` (optional) gives explicit group ends so groups may skip rows;
+    then goff[G] must bound the last end."""
     from . import gemm_tc
 
     R = xp.shape[0]
@@ -246,21 +248,22 @@ def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[tor
     h = torch.empty((R, F), dtype=dt, device=xp.device)
     pre = torch.empty((R, N1), dtype=dt, device=xp.device)
     if dt == torch.bfloat16 and gemm_tc.available() and gemm_tc.fused_act_ok(pk):
-        gemm_tc.ffn1_fused(xp, pk, pre, h, goff, G, gexp, max_rows)
+        gemm_tc.ffn1_fused(xp, pk, pre, h, goff, G, gexp, max_rows, gend)
     else:
         _gemm(xp, pk.w1p, pre, grouped_dim=0, G=G, M=0, N=N1, K=H, a_sm=H, a_sk=1,
               b_sg=N1 * H, b_sk=1, b_sn=H, c_sg=0, ldc=N1, group_off=goff, group_expert=gexp,
-              max_rows=max_rows)
+              max_rows=max_rows, group_end=gend)
         K.act_fwd(pre, act, goff, G, F, out=h)
     y = torch.empty((R, H), dtype=dt, device=xp.device)
     _gemm(h, pk.w2p, y, grouped_dim=0, G=G, M=0, N=H, K=F, a_sm=F, a_sk=1, b_sg=H * F, b_sk=1,
-          b_sn=F, c_sg=0, ldc=H, group_off=goff, group_expert=gexp, max_rows=max_rows)
+          b_sn=F, c_sg=0, ldc=H, group_off=goff, group_expert=gexp, max_rows=max_rows,
+          group_end=gend)
     return pre, h, y
 
 
 def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torch.Tensor,
                  goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor], pk: PackedExperts,
-                 max_rows: int, want_dx: bool = True):
+                 max_rows: int, want_dx: bool = True, gend: Optional[torch.Tensor] = None):
     """experts.py:146-172 batched over groups: returns (dxp, dw1p, dw2p) with
     dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert)."""
     from . import gemm_tc
@@ -272,24 +275,25 @@ def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torc
     dev = dyp.device
     dpre = torch.empty((R, N1), dtype=dt, device=dev)
     if dt == torch.bfloat16 and gemm_tc.available() and gemm_tc.fused_act_ok(pk):
-        gemm_tc.dgrad2_fused(dyp, pk, pre, dpre, goff, G, gexp, max_rows)
+        gemm_tc.dgrad2_fused(dyp, pk, pre, dpre, goff, G, gexp, max_rows, gend)
     else:
         dh = torch.empty((R, F), dtype=dt, device=dev)
         _gemm(dyp, pk.w2p, dh, grouped_dim=0, G=G, M=0, N=F, K=H, a_sm=H, a_sk=1, b_sg=H * F,
-              b_sk=F, b_sn=1, c_sg=0, ldc=F, group_off=goff, group_expert=gexp, max_rows=max_rows)
+              b_sk=F, b_sn=1, c_sg=0, ldc=F, group_off=goff, group_expert=gexp, max_rows=max_rows,
+              group_end=gend)
         K.act_bwd(dh, pre, act, goff, G, F, out=dpre)
     dxp = None
     if want_dx:
         dxp = torch.empty((R, H), dtype=dt, device=dev)
         _gemm(dpre, pk.w1p, dxp, grouped_dim=0, G=G, M=0, N=H, K=N1, a_sm=N1, a_sk=1,
               b_sg=N1 * H, b_sk=H, b_sn=1, c_sg=0, ldc=H, group_off=goff, group_expert=gexp,
-              max_rows=max_rows)
+              max_rows=max_rows, group_end=gend)
     dw2p = torch.empty((G, H, F), dtype=torch.float32, device=dev)
     _gemm(dyp, h, dw2p, grouped_dim=1, G=G, M=H, N=F, K=0, a_sm=1, a_sk=H, b_sg=0, b_sk=F,
-          b_sn=1, c_sg=H * F, ldc=F, group_off=goff, max_rows=max_rows)
+          b_sn=1, c_sg=H * F, ldc=F, group_off=goff, max_rows=max_rows, group_end=gend)
     dw1p = torch.empty((G, N1, H), dtype=torch.float32, device=dev)
     _gemm(dpre, xp, dw1p, grouped_dim=1, G=G, M=N1, N=H, K=0, a_sm=1, a_sk=N1, b_sg=0, b_sk=H,
-          b_sn=1, c_sg=N1 * H, ldc=H, group_off=goff, max_rows=max_rows)
+          b_sn=1, c_sg=N1 * H, ldc=H, group_off=goff, max_rows=max_rows, group_end=gend)
     return dxp, dw1p, dw2p
 
 

@@ -29,7 +29,7 @@ class TcGemmArgs(ctypes.Structure):
         ("C", P), ("ldc", I64), ("c_sg", I64), ("out_dtype", I32), ("accumulate", I32),
         ("group_off", P), ("group_expert", P),
         ("epilogue", I32), ("act", I32), ("H", P), ("ldh", I64), ("PRE", P), ("ldpre", I64),
-        ("num_ctas", I32),
+        ("num_ctas", I32), ("group_end", P),
     ]
 
 
@@ -85,7 +85,7 @@ def _run(args: TcGemmArgs) -> None:
 
 
 def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg, ldc, group_off,
-         group_expert=None, max_rows=0, accumulate=False):
+         group_expert=None, max_rows=0, accumulate=False, group_end=None):
     """Same argument convention as kernels.gemm_simt."""
     a = TcGemmArgs()
     a.G, a.grouped_dim, a.M, a.N, a.K = G, grouped_dim, M, N, K
@@ -106,6 +106,7 @@ def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg
     a.out_dtype = L.dtype_code(C.dtype)
     a.accumulate = int(accumulate)
     a.group_off, a.group_expert = L.ptr(group_off), L.ptr(group_expert)
+    a.group_end = L.ptr(group_end)
     a.epilogue = EPI_STORE
     _run(a)
     return C
@@ -120,7 +121,7 @@ def fused_act_ok(pk) -> bool:
     return True
 
 
-def ffn1_fused(xp, pk, pre, h, goff, G, gexp, max_rows):
+def ffn1_fused(xp, pk, pre, h, goff, G, gexp, max_rows, gend=None):
     """pre = xp W1_g (bf16) and h = act(pre) in one tensor-core pass."""
     a = TcGemmArgs()
     H, F, N1 = pk.hidden, pk.ffn, pk.n1
@@ -130,6 +131,7 @@ def ffn1_fused(xp, pk, pre, h, goff, G, gexp, max_rows):
     a.b_batch, a.b_batch_stride = pk.w1p.shape[0], N1 * H
     a.C, a.ldc, a.c_sg, a.out_dtype = L.ptr(pre), N1, 0, L.BF16
     a.group_off, a.group_expert = L.ptr(goff), L.ptr(gexp)
+    a.group_end = L.ptr(gend)
     if pk.act == "swiglu":
         a.epilogue = EPI_SWIGLU_FWD
     else:
@@ -138,7 +140,7 @@ def ffn1_fused(xp, pk, pre, h, goff, G, gexp, max_rows):
     _run(a)
 
 
-def dgrad2_fused(dyp, pk, pre, dpre, goff, G, gexp, max_rows):
+def dgrad2_fused(dyp, pk, pre, dpre, goff, G, gexp, max_rows, gend=None):
     """dpre = (dy W2_g^T) * act'(pre) in one tensor-core pass."""
     a = TcGemmArgs()
     H, F, N1 = pk.hidden, pk.ffn, pk.n1
@@ -149,6 +151,7 @@ def dgrad2_fused(dyp, pk, pre, dpre, goff, G, gexp, max_rows):
     a.b_batch, a.b_batch_stride = pk.w2p.shape[0], H * F
     a.C, a.ldc, a.c_sg, a.out_dtype = L.ptr(dpre), N1, 0, L.BF16
     a.group_off, a.group_expert = L.ptr(goff), L.ptr(gexp)
+    a.group_end = L.ptr(gend)
     if pk.act == "swiglu":
         a.epilogue = EPI_SWIGLU_BWD
     else:

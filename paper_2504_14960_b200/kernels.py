@@ -199,13 +199,14 @@ def router_wgrad(x: torch.Tensor, dz: torch.Tensor) -> torch.Tensor:
 
 def gemm_simt(A, B, C, *, grouped_dim: int, G: int, M: int, N: int, K: int, a_sm, a_sk, b_sg,
               b_sk, b_sn, c_sg, ldc, group_off, group_expert=None, max_rows: int = 0,
-              accumulate: bool = False):
+              accumulate: bool = False, group_end=None):
     args = L.GemmArgs(
         dtype_in=L.dtype_code(A.dtype), dtype_out=L.dtype_code(C.dtype), grouped_dim=grouped_dim,
         accumulate=int(accumulate), G=G, M=M, N=N, K=K,
         A=L.ptr(A), a_sm=a_sm, a_sk=a_sk, B=L.ptr(B), b_sg=b_sg, b_sk=b_sk, b_sn=b_sn,
         C=L.ptr(C), c_sg=c_sg, ldc=ldc, group_off=L.ptr(group_off),
-        group_expert=L.ptr(group_expert), max_rows=max_rows, dtype_b=L.dtype_code(B.dtype))
+        group_expert=L.ptr(group_expert), max_rows=max_rows, dtype_b=L.dtype_code(B.dtype),
+        group_end=L.ptr(group_end))
     L.call("b200moe_gemm_simt", ctypes.byref(args), _sp())
     return C
 
