@@ -471,8 +471,11 @@ class RankLayer:
         xr = torch.empty((max(R_recv, 1), H), dtype=x.dtype, device=x.device)
         work = ctx.a2a_single(self.g.ep, xs, xpl.send_splits, xr, xpl.recv_splits, async_op=True)
         og = self._overlap_groups(xpl)
-        xs_self = xs[og["so_me"]:og["so_me"] + og["n_self"]]
-        s_pre, s_h, s_y = X.ffn_forward(xs_self, og["s_off"], og["G_self"], None, self.pk, og["n_self"])
+        s_pre = s_h = s_y = None
+        if og["n_self"]:
+            xs_self = xs[og["so_me"]:og["so_me"] + og["n_self"]]
+            s_pre, s_h, s_y = X.ffn_forward(xs_self, og["s_off"], og["G_self"], None, self.pk,
+                                            og["n_self"])
         work.wait()
         r_pre, r_h, r_y = X.ffn_forward(xr, og["r_off"], og["G_rem"], og["r_exp"], self.pk, R_recv,
                                         gend=og["r_end"])
@@ -480,7 +483,8 @@ class RankLayer:
         work = ctx.a2a_single(self.g.ep, r_y, xpl.recv_splits, ys, xpl.send_splits, async_op=True)
         y_sh = self._shared_forward(x, saved)  # overlaps the return transfer
         work.wait()
-        ys[og["so_me"]:og["so_me"] + og["n_self"]].copy_(s_y)  # self rows never left the GPU
+        if s_y is not None:  # self rows never left the GPU
+            ys[og["so_me"]:og["so_me"] + og["n_self"]].copy_(s_y)
         out = K.combine(ys, plan.gemm_row, T, gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
         saved.update(xs=xs, xr=xr, s_pre=s_pre, s_h=s_h, r_pre=r_pre, r_h=r_h, y=ys, og=og, xpl=xpl,
                      pair_row=plan.gemm_row, R_send=R_send, R_recv=R_recv, overlap=True)
@@ -495,8 +499,10 @@ class RankLayer:
         dyr = torch.empty((max(sv["R_recv"], 1), H), dtype=u.dtype, device=u.device)
         work = ctx.a2a_single(self.g.ep, dys, xpl.send_splits, dyr, xpl.recv_splits, async_op=True)
         a, n = og["so_me"], og["n_self"]
-        s_dx, s_dw1, s_dw2 = X.ffn_backward(dys[a:a + n], sv["xs"][a:a + n], sv["s_pre"], sv["s_h"],
-                                            og["s_off"], og["G_self"], None, self.pk, n)
+        s_dx = None
+        if n:
+            s_dx, s_dw1, s_dw2 = X.ffn_backward(dys[a:a + n], sv["xs"][a:a + n], sv["s_pre"],
+                                                sv["s_h"], og["s_off"], og["G_self"], None, self.pk, n)
         work.wait()
         r_dx, r_dw1, r_dw2 = X.ffn_backward(dyr, sv["xr"], sv["r_pre"], sv["r_h"], og["r_off"],
                                             og["G_rem"], og["r_exp"], self.pk, sv["R_recv"],
@@ -504,10 +510,14 @@ class RankLayer:
         rows = torch.empty((max(sv["R_send"], 1), H), dtype=u.dtype, device=u.device)
         work = ctx.a2a_single(self.g.ep, r_dx, xpl.recv_splits, rows, xpl.send_splits, async_op=True)
         # per-expert weight grads: self groups are experts 0..L-1, remote groups cycle le
-        dw1p = s_dw1 + r_dw1.reshape(-1, self.L, *r_dw1.shape[1:]).sum(0)
-        dw2p = s_dw2 + r_dw2.reshape(-1, self.L, *r_dw2.shape[1:]).sum(0)
+        dw1p = r_dw1.reshape(-1, self.L, *r_dw1.shape[1:]).sum(0)
+        dw2p = r_dw2.reshape(-1, self.L, *r_dw2.shape[1:]).sum(0)
+        if s_dx is not None:
+            dw1p += s_dw1
+            dw2p += s_dw2
         work.wait()
-        rows[a:a + n].copy_(s_dx)
+        if s_dx is not None:
+            rows[a:a + n].copy_(s_dx)
         return rows, dgates, dw1p, dw2p
 
     def _forward_exchange(self, ctx, x, dec, plan, saved):
