@@ -284,6 +284,16 @@ def main():
     for _ in range(a.warmup):
         step()
     barrier()
+    if os.environ.get("B200MOE_NCU_RANGE") == "1":
+        # exactly one step between cudaProfilerStart/Stop, for
+        # `ncu --profile-from-start off` launch lists and captures
+        torch.cuda.cudart().cudaProfilerStart()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        if world > 1:
+            dist.destroy_process_group()
+        return
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     clocks = ClockSampler(local)
     clocks.start()

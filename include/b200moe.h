@@ -208,6 +208,46 @@ typedef struct {
 
 B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);
 
+/* ------------------------------------- EP all-to-all over NVLink peer memory
+ * Device-side replacement of all_to_all_v + exchange_meta
+ * (dispatcher.py:310-361, 430-466).  peer_base[ep] (device array) holds the
+ * base address of the same symmetric buffer on every rank of the EP group;
+ * regions are addressed by byte offsets.  No call synchronises the host. */
+
+/* row `me` of every peer's [ep, E] int32 count matrix := counts[E] */
+B200MOE_API int b200moe_ep_counts_push(const int32_t* counts, int me, int ep, int E,
+                                       const uint64_t* peer_base, int64_t cnt_off, void* stream);
+/* cross-GPU barrier: flag exchange at flag_off with system-scope
+ * release/acquire; epoch must increase by one per call (bounded spin, traps
+ * if a peer never arrives). */
+B200MOE_API int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep,
+                                   uint32_t epoch, void* stream);
+/* from this rank's copy of the count matrix: seg_off[ep*L] (first row of
+ * (me, le) in rank d's receive buffer), goff[L+1] / gcount[L] (this rank's
+ * GEMM groups: one per local expert, senders contiguous in rank order, the
+ * group padded to align rows).  Traps if a layout exceeds cap_rows. */
+B200MOE_API int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align,
+                                  int64_t cap_rows, int32_t* seg_off, int32_t* goff, int32_t* gcount,
+                                  void* stream);
+/* zero the pad rows of this rank's receive buffer (bf16 [rows, H]) */
+B200MOE_API int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount,
+                                     int G, int align, void* stream);
+/* fused permute + push: x[t] (bwd: gates*u[t]) -> row seg_off[d,le] +
+ * (gemm_row - poff[e]) of rank d's buffer at dst_off; bwd also pulls the
+ * expert output row at y_off for dgates; fwd records pair_dst/pair_rrow. */
+B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L,
+                                    const int32_t* topk_idx, const int32_t* gemm_row,
+                                    const int32_t* poff, const int32_t* seg_off,
+                                    const uint64_t* peer_base, int64_t dst_off, int64_t y_off,
+                                    const float* gates, float* dgates, int32_t* pair_dst,
+                                    int32_t* pair_rrow, int bwd, void* stream);
+/* pull-combine: out[t] (+)= sum_s w_s * row(pair_dst, pair_rrow) read from
+ * the peers' buffer at src_off (w = gates or 1). */
+B200MOE_API int b200moe_ep_combine(int64_t T, int64_t H, int k, const int32_t* pair_dst,
+                                   const int32_t* pair_rrow, const uint64_t* peer_base,
+                                   int64_t src_off, const float* gates, void* out, int out_dtype,
+                                   int accumulate, void* stream);
+
 /* Elementwise expert activations in the padded row layout, rows < group_off[G].
  * SwiGLU layout: pre has 2F columns, 64-column blocks of [32 gate | 32 up]. */
 B200MOE_API int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,

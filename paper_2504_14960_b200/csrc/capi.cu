@@ -38,6 +38,15 @@ int combine(const void*, int, int64_t, int64_t, int, const int32_t*, const float
             const float*, int, void*, int, int, cudaStream_t);
 int gemm_simt(const b200moe_gemm_args*, cudaStream_t);
 int gemm_tc(const b200moe_tc_gemm_args*, cudaStream_t);
+int ep_barrier(const uint64_t*, int64_t, int, int, uint32_t, cudaStream_t);
+int ep_counts_push(const int32_t*, int, int, int, const uint64_t*, int64_t, cudaStream_t);
+int ep_layout(const int32_t*, int, int, int, int, int64_t, int32_t*, int32_t*, int32_t*, cudaStream_t);
+int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, cudaStream_t);
+int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
+                const int32_t*, const int32_t*, const uint64_t*, int64_t, int64_t, const float*,
+                float*, int32_t*, int32_t*, int, cudaStream_t);
+int ep_combine(int64_t, int64_t, int, const int32_t*, const int32_t*, const uint64_t*, int64_t,
+               const float*, void*, int, int, cudaStream_t);
 int act_fwd(const void*, int, int, const int32_t*, int, int64_t, int64_t, void*, cudaStream_t);
 int act_bwd(const void*, const void*, int, int, const int32_t*, int, int64_t, int64_t, void*,
             cudaStream_t);
@@ -221,6 +230,55 @@ int b200moe_gemm_tc(const b200moe_tc_gemm_args* a, void* stream) {
   REQUIRE(a->epilogue != 2 || a->N % 32 == 0, "gemm_tc: SwiGLU bwd needs N %% 32 == 0");
   if (a->a_rows == 0) return B200MOE_OK;
   return gemm_tc(a, S(stream));
+}
+
+int b200moe_ep_counts_push(const int32_t* counts, int me, int ep, int E, const uint64_t* peer_base,
+                           int64_t cnt_off, void* stream) {
+  REQUIRE(counts && peer_base && ep >= 1 && ep <= 32 && me >= 0 && me < ep && E >= 1,
+          "ep_counts_push: bad args");
+  return ep_counts_push(counts, me, ep, E, peer_base, cnt_off, S(stream));
+}
+
+int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep, uint32_t epoch,
+                       void* stream) {
+  REQUIRE(peer_base && ep >= 1 && ep <= 32 && me >= 0 && me < ep, "ep_barrier: bad args");
+  return ep_barrier(peer_base, flag_off, me, ep, epoch, S(stream));
+}
+
+int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align, int64_t cap_rows,
+                      int32_t* seg_off, int32_t* goff, int32_t* gcount, void* stream) {
+  REQUIRE(cnt_local && seg_off && goff && gcount && ep >= 1 && ep <= 32 && L >= 1 && align >= 1 &&
+              cap_rows >= 0 && cap_rows < (1ll << 31),
+          "ep_layout: bad args");
+  return ep_layout(cnt_local, me, ep, L, align, cap_rows, seg_off, goff, gcount, S(stream));
+}
+
+int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G,
+                         int align, void* stream) {
+  REQUIRE(buf && goff && gcount && H >= 1, "ep_zero_pads: bad args");
+  return ep_zero_pads(buf, H, goff, gcount, G, align, S(stream));
+}
+
+int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const int32_t* topk_idx,
+                        const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
+                        const uint64_t* peer_base, int64_t dst_off, int64_t y_off, const float* gates,
+                        float* dgates, int32_t* pair_dst, int32_t* pair_rrow, int bwd, void* stream) {
+  REQUIRE(H % 8 == 0 && k >= 1 && L >= 1, "ep_dispatch: H %% 8 and k >= 1 required");
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(x && topk_idx && gemm_row && poff && seg_off && peer_base, "ep_dispatch: null pointer");
+  REQUIRE(bwd ? (gates && dgates) : (pair_dst && pair_rrow), "ep_dispatch: null pointer");
+  return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, dst_off, y_off, gates,
+                     dgates, pair_dst, pair_rrow, bwd, S(stream));
+}
+
+int b200moe_ep_combine(int64_t T, int64_t H, int k, const int32_t* pair_dst, const int32_t* pair_rrow,
+                       const uint64_t* peer_base, int64_t src_off, const float* gates, void* out,
+                       int out_dtype, int accumulate, void* stream) {
+  REQUIRE(H % 8 == 0 && dt_ok(out_dtype), "ep_combine: bad args");
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(pair_dst && pair_rrow && peer_base && out, "ep_combine: null pointer");
+  return ep_combine(T, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, out, out_dtype, accumulate,
+                    S(stream));
 }
 
 int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,

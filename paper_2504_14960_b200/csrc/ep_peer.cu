@@ -1,0 +1,311 @@
+// EP all-to-all over NVLink peer memory (symmetric buffers), fused with the
+// permute / combine work -- the device-side replacement of the reference's
+// all_to_all_v + exchange_meta pair (dispatcher.py:310-361, 430-466).
+//
+// Every rank of an EP group maps the same symmetric buffer layout; peer
+// addresses are  peer_base[d] + region offset.  Per forward step:
+//   counts_push   each rank writes its per-expert kept counts into row `me` of
+//                 every peer's count matrix                      (+ barrier)
+//   layout        every rank derives, from the full count matrix, the
+//                 receive layout of each destination: segments (sender s,
+//                 local expert le), s-major, each padded to `align` rows; it
+//                 keeps its own push offsets and its own GEMM group offsets
+//   dispatch      one warp per token reads x[t] once and stores it straight
+//                 into the destination ranks' receive buffers    (+ barrier)
+//   ... grouped GEMM on the local receive buffer ...             (+ barrier)
+//   combine       one warp per token pulls its k expert rows from the peers
+//                 and gate-combines them
+// Split sizes never leave the device.  The barrier is a flag exchange in the
+// symmetric buffer with system-scope release/acquire and a bounded spin
+// (a missing peer traps instead of hanging the GPU).
+#include "common.cuh"
+
+namespace b200moe {
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------------ barrier
+// flags[p] on rank r = last epoch rank p announced to r.
+__global__ void ep_barrier_kernel(const uint64_t* __restrict__ peer_base, int64_t flag_off, int me,
+                                  int ep, uint32_t epoch) {
+  const int p = threadIdx.x;
+  __threadfence_system();  // this rank's prior writes (local and remote) before the flags
+  __syncthreads();
+  if (p < ep) {
+    uint32_t* remote = reinterpret_cast<uint32_t*>(peer_base[p] + flag_off) + me;
+    st_release_sys(remote, epoch);
+  }
+  if (p < ep) {
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(peer_base[me] + flag_off) + p;
+    uint64_t spins = 0;
+    while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
+      if (++spins > (1ull << 31)) {
+        printf("b200moe ep_barrier: rank %d timed out waiting for rank %d (epoch %u)\n", me, p, epoch);
+        __trap();
+      }
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+// ------------------------------------------------------------------ counts
+__global__ void ep_counts_push_kernel(const int32_t* __restrict__ counts, int me, int ep, int E,
+                                      const uint64_t* __restrict__ peer_base, int64_t cnt_off) {
+  for (int i = threadIdx.x; i < ep * E; i += blockDim.x) {
+    const int p = i / E, e = i % E;
+    int32_t* dst = reinterpret_cast<int32_t*>(peer_base[p] + cnt_off) + me * E + e;
+    *dst = counts[e];
+  }
+}
+
+// ------------------------------------------------------------------ layout
+// cnt: this rank's copy of the [ep, E] matrix (row s = sender s's counts).
+// Receive buffers are expert-major: local expert le's rows from all senders
+// are contiguous (sender order), and only the expert's group is padded to
+// `align` rows -- so one GEMM group per local expert, no per-sender padding.
+// seg_off[d*L + le] = first row of (me, le) in rank d's receive buffer;
+// goff[le] / gcount[le] = group start / real rows in this rank's buffer,
+// goff[L] = end.  A layout beyond cap_rows (the buffer size) traps.
+__global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int me, int ep, int L, int align,
+                                 int64_t cap_rows, int32_t* __restrict__ seg_off,
+                                 int32_t* __restrict__ goff, int32_t* __restrict__ gcount) {
+  const int E = ep * L;
+  const int d = threadIdx.x;  // one thread per destination layout
+  if (d >= ep) return;
+  int64_t run = 0;
+  for (int le = 0; le < L; ++le) {
+    int64_t tot = 0;
+    for (int s = 0; s < ep; ++s) {
+      if (s == me) seg_off[d * L + le] = (int32_t)(run + tot);
+      tot += cnt[s * E + d * L + le];
+    }
+    if (d == me) {
+      goff[le] = (int32_t)run;
+      gcount[le] = (int32_t)tot;
+    }
+    run += (tot + align - 1) / align * align;
+  }
+  if (run > cap_rows) {
+    printf("b200moe ep_layout: rank %d receive layout needs %lld rows > capacity %lld\n", d,
+           (long long)run, (long long)cap_rows);
+    __trap();
+  }
+  if (d == me) goff[L] = (int32_t)run;
+}
+
+// zero the alignment pad rows of this rank's receive buffer
+__global__ void ep_zero_pads_kernel(__nv_bfloat16* __restrict__ buf, int64_t H,
+                                    const int32_t* __restrict__ goff, const int32_t* __restrict__ gcount) {
+  const int g = blockIdx.y;
+  const int64_t row = (int64_t)goff[g] + gcount[g] + blockIdx.x;
+  if (row >= goff[g + 1]) return;
+  __nv_bfloat16* p = buf + row * H;
+  for (int64_t c = threadIdx.x; c < H; c += blockDim.x) p[c] = __float2bfloat16_rn(0.f);
+}
+
+// ------------------------------------------------------------------ dispatch
+// Forward: rows x[t] -> dest receive buffers.  Backward (scale != NULL):
+// rows g*u[t] -> dest, and dgate = <u[t], y_row> with y pulled from the
+// dest's output buffer at the same row.  Also records, per pair, the
+// (dest, remote row) that the combines use.
+template <int KMAX, bool BWD>
+__global__ void __launch_bounds__(256) ep_dispatch_kernel(
+    const __nv_bfloat16* __restrict__ x, int64_t Tn, int64_t H, int k, int L,
+    const int32_t* __restrict__ topk, const int32_t* __restrict__ gemm_row,
+    const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
+    const uint64_t* __restrict__ peer_base, int64_t dst_off, int64_t y_off,
+    const float* __restrict__ gates, float* __restrict__ dgates, int32_t* __restrict__ pair_dst,
+    int32_t* __restrict__ pair_rrow) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  __nv_bfloat16* dst[KMAX];
+  const __nv_bfloat16* ysrc[KMAX];
+  float g[KMAX], dot[KMAX];
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    dst[s] = nullptr;
+    ysrc[s] = nullptr;
+    g[s] = 1.f;
+    dot[s] = 0.f;
+    if (s >= k) continue;
+    const int32_t gr = gemm_row[t * k + s];
+    if (gr < 0) {
+      if (!BWD && lane == 0) {
+        pair_dst[t * k + s] = -1;
+        pair_rrow[t * k + s] = -1;
+      }
+      continue;
+    }
+    const int e = topk[t * k + s];
+    const int d = e / L, le = e % L;
+    const int32_t rr = seg_off[d * L + le] + (gr - poff[e]);
+    dst[s] = reinterpret_cast<__nv_bfloat16*>(peer_base[d] + dst_off) + (int64_t)rr * H;
+    if (BWD) {
+      ysrc[s] = reinterpret_cast<const __nv_bfloat16*>(peer_base[d] + y_off) + (int64_t)rr * H;
+      g[s] = gates[t * k + s];
+    } else if (lane == 0) {
+      pair_dst[t * k + s] = d;
+      pair_rrow[t * k + s] = rr;
+    }
+  }
+  const __nv_bfloat16* src = x + t * H;
+  for (int64_t c = (int64_t)lane * 8; c < H; c += 256) {
+    Vec16<__nv_bfloat16> v;
+    v.raw = ld_nc_v4(src + c);
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (!dst[s]) continue;
+      if (BWD) {
+        Vec16<__nv_bfloat16> y, o;
+        y.raw = ld_v4(ysrc[s] + c);  // NVLink pull (peer L2)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float uv = __bfloat162float(v.v[i]);
+          dot[s] = fmaf(uv, __bfloat162float(y.v[i]), dot[s]);
+          o.v[i] = __float2bfloat16_rn(uv * g[s]);
+        }
+        st_v4(dst[s] + c, o.raw);
+      } else {
+        st_v4(dst[s] + c, v.raw);  // NVLink push
+      }
+    }
+  }
+  if (BWD) {
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (s >= k) break;
+      const float d = warp_sum(dot[s]);
+      if (lane == 0) dgates[t * k + s] = dst[s] ? d : 0.f;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ combine
+// out[t] = sum_s w_s * row(pair_dst[s], pair_rrow[s]) pulled from the peers'
+// buffer at src_off (w = gates, or 1); accumulate adds to out.
+template <typename Tout, int KMAX>
+__global__ void __launch_bounds__(256) ep_combine_kernel(
+    int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_dst,
+    const int32_t* __restrict__ pair_rrow, const uint64_t* __restrict__ peer_base, int64_t src_off,
+    const float* __restrict__ gates, Tout* __restrict__ out, int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= Tn) return;
+  const __nv_bfloat16* src[KMAX];
+  float w[KMAX];
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    src[s] = nullptr;
+    w[s] = 1.f;
+    if (s >= k) continue;
+    const int32_t d = pair_dst[t * k + s];
+    if (d < 0) continue;
+    src[s] = reinterpret_cast<const __nv_bfloat16*>(peer_base[d] + src_off) + (int64_t)pair_rrow[t * k + s] * H;
+    if (gates) w[s] = gates[t * k + s];
+  }
+  for (int64_t c = (int64_t)lane * 8; c < H; c += 256) {
+    Vec16<__nv_bfloat16> v[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s)
+      if (src[s]) v[s].raw = ld_v4(src[s] + c);
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (!src[s]) continue;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fmaf(w[s], __bfloat162float(v[s].v[i]), acc[i]);
+    }
+    Tout* o = out + t * H + c;
+    if (accumulate) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += to_f32(o[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = from_f32<Tout>(acc[i]);
+  }
+}
+
+// ------------------------------------------------------------------ host
+#define KSW(k, M)                       \
+  if (k <= 1) { M(1); }                 \
+  else if (k <= 2) { M(2); }            \
+  else if (k <= 4) { M(4); }            \
+  else if (k <= 8) { M(8); }            \
+  else { set_error("ep: k=%d > 8 unsupported", k); return B200MOE_EUNSUPPORTED; }
+
+int ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep, uint32_t epoch,
+               cudaStream_t st) {
+  ep_barrier_kernel<<<1, 32, 0, st>>>(peer_base, flag_off, me, ep, epoch);
+  B200MOE_CHECK_LAUNCH("ep_barrier");
+  return B200MOE_OK;
+}
+
+int ep_counts_push(const int32_t* counts, int me, int ep, int E, const uint64_t* peer_base,
+                   int64_t cnt_off, cudaStream_t st) {
+  ep_counts_push_kernel<<<1, 256, 0, st>>>(counts, me, ep, E, peer_base, cnt_off);
+  B200MOE_CHECK_LAUNCH("ep_counts_push");
+  return B200MOE_OK;
+}
+
+int ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align, int64_t cap_rows,
+              int32_t* seg_off, int32_t* goff, int32_t* gcount, cudaStream_t st) {
+  ep_layout_kernel<<<1, 32, 0, st>>>(cnt_local, me, ep, L, align, cap_rows, seg_off, goff, gcount);
+  B200MOE_CHECK_LAUNCH("ep_layout");
+  return B200MOE_OK;
+}
+
+int ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G, int align,
+                 cudaStream_t st) {
+  if (align <= 1 || G <= 0) return B200MOE_OK;
+  dim3 grid((unsigned)(align - 1), (unsigned)G);
+  ep_zero_pads_kernel<<<grid, 128, 0, st>>>(static_cast<__nv_bfloat16*>(buf), H, goff, gcount);
+  B200MOE_CHECK_LAUNCH("ep_zero_pads");
+  return B200MOE_OK;
+}
+
+int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_t* topk,
+                const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
+                const uint64_t* peer_base, int64_t dst_off, int64_t y_off, const float* gates,
+                float* dgates, int32_t* pair_dst, int32_t* pair_rrow, int bwd, cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(Tn, 8);
+  const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, dst_off, y_off, gates, dgates, pair_dst, pair_rrow)
+#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, dst_off, y_off, gates, dgates, pair_dst, pair_rrow)
+  if (Tn > 0) {
+    if (bwd) { KSW(k, DB) }
+    else { KSW(k, DF) }
+  }
+#undef DF
+#undef DB
+  B200MOE_CHECK_LAUNCH("ep_dispatch");
+  return B200MOE_OK;
+}
+
+int ep_combine(int64_t Tn, int64_t H, int k, const int32_t* pair_dst, const int32_t* pair_rrow,
+               const uint64_t* peer_base, int64_t src_off, const float* gates, void* out, int out_dtype,
+               int accumulate, cudaStream_t st) {
+  const unsigned grid = (unsigned)ceil_div(Tn, 8);
+#define CBF(KM) ep_combine_kernel<__nv_bfloat16, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, static_cast<__nv_bfloat16*>(out), accumulate)
+#define CF(KM) ep_combine_kernel<float, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, static_cast<float*>(out), accumulate)
+  if (Tn > 0) {
+    if (out_dtype == B200MOE_BF16) { KSW(k, CBF) }
+    else { KSW(k, CF) }
+  }
+#undef CBF
+#undef CF
+  B200MOE_CHECK_LAUNCH("ep_combine");
+  return B200MOE_OK;
+}
+
+}  // namespace b200moe

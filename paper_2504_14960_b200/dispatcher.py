@@ -283,7 +283,8 @@ class RankLayer:
 
     def __init__(self, params: GatingParams, weights: X.ExpertWeights, topology: ParallelTopology,
                  groups: LayerGroups, rank: int, dtype, device, seq_len=None, check=False,
-                 shared: Optional[X.ExpertWeights] = None, pad_to_capacity: bool = False):
+                 shared: Optional[X.ExpertWeights] = None, pad_to_capacity: bool = False,
+                 exchange: Optional[str] = None, peer_tokens: Optional[int] = None, peer_tag=0):
         self.shared_pk = None if shared is None else shared.packed(dtype, device)
         # pad-to-capacity (BASELINE C3): every expert segment holds exactly
         # round_up(cap, ALIGN) rows, so all exchange sizes are static and the
@@ -311,6 +312,15 @@ class RankLayer:
         self.wg = params.device_w_g(device)
         self.wgT = params.device_w_gT(device)
         self.single = len(groups.ep) == 1 and len(groups.etp) == 1
+        # EP exchange: device-side over NVLink peer memory (bf16, ETP = 1), or
+        # NCCL all_to_all_single (B200MOE_EP_EXCHANGE=nccl, fp32, ETP > 1)
+        self.peer_tokens = peer_tokens
+        self.peer_tag = peer_tag
+        want = exchange or os.environ.get("B200MOE_EP_EXCHANGE", "peer")
+        if want not in ("peer", "nccl"):
+            raise ValidationError(f"unknown EP exchange {want!r}", constraint="exchange")
+        self.use_peer = (want == "peer" and not self.single and len(groups.etp) == 1
+                         and dtype == torch.bfloat16 and self.k <= 8 and self.pk.hidden % 8 == 0)
 
     # ------------------------------------------------------- shared expert
     # Builder-defined (no reference): a dense FFN over every token whose
@@ -520,9 +530,66 @@ class RankLayer:
             rows[a:a + n].copy_(s_dx)
         return rows, dgates, dw1p, dw2p
 
+    # ---- device-side EP exchange over NVLink peer memory (peer.py).  Tokens
+    # are pushed straight from the token block into the owners' receive
+    # buffers (no send buffer, no host sync), the GEMMs run on the receive
+    # buffer with one group per local expert, and the combines pull the rows
+    # back from the peers.
+    def _peer(self, ctx, T: int):
+        from . import peer as PX
+
+        H = self.pk.hidden
+        cache = ctx.world.__dict__.setdefault("_peer_exchanges", {})
+        key = (ctx.rank, self.g.ep, self.E, self.k, H, self.peer_tag)
+        px = cache.get(key)
+        if px is None:
+            # buffer layout must be identical on every member: agree on the
+            # largest token block once, when the buffers are created
+            T_max = max(int(self.peer_tokens or 0), T)
+            T_max = max(int(v) for v in ctx.exchange_meta(self.g.ep, T_max).values())
+            cap = PX.capacity_rows(len(self.g.ep), T_max, self.k, self.L, ALIGN)
+            px = PX.PeerExchange(ctx, self.g.ep, self.E, self.L, H, cap, self.device)
+            px.tokens = T_max
+            cache[key] = px
+        elif T > px.tokens:
+            raise ValidationError(f"token block of {T} rows exceeds the peer buffers' {px.tokens}: "
+                                  "pass peer_tokens >= the largest block on first use",
+                                  constraint="peer-capacity")
+        return px
+
+    def _forward_peer(self, ctx, x, dec, plan, saved):
+        H = x.shape[1]
+        px = self._peer(ctx, x.shape[0])
+        st = px.forward_dispatch(x, dec.experts, plan, ALIGN)
+        pre, h, _ = X.ffn_forward(px.region("xr"), st["goff"], self.L, None, self.pk, px.cap,
+                                  y_out=px.region("yr"))
+        y_sh = self._shared_forward(x, saved)
+        px.barrier()  # every expert output row is in place
+        out = K.ep_combine(st["pair_dst"], st["pair_rrow"], H, px.peer_base, px.off["yr"],
+                           gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
+        saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row)
+        return out, saved
+
+    def _backward_peer(self, ctx, u, sv, dec, plan):
+        px, st = sv["peer"], sv["pst"]
+        px.check_generation(st)
+        H = u.shape[1]
+        dyr = px.region("dyr")
+        K.ep_zero_pads(dyr, st["goff"], st["gcount"], self.L, ALIGN)
+        dgates = K.ep_dispatch(u, dec.experts, plan.gemm_row, plan.poffsets, st["seg_off"], self.L,
+                               px.peer_base, px.off["dyr"], bwd=True, y_off=px.off["yr"],
+                               gates=dec.gates)
+        px.barrier()  # every upstream row is in place
+        _, dw1p, dw2p = X.ffn_backward(dyr, px.region("xr"), sv["pre"], sv["h"], st["goff"], self.L,
+                                       None, self.pk, px.cap, dx_out=px.region("dxr"))
+        px.barrier()  # every input-gradient row is in place
+        return st, dgates, dw1p, dw2p
+
     def _forward_exchange(self, ctx, x, dec, plan, saved):
         T, H = x.shape
         E = self.E
+        if self.use_peer:
+            return self._forward_peer(ctx, x, dec, plan, saved)
         if len(self.g.etp) == 1 and self.overlap:
             return self._forward_overlap(ctx, x, dec, plan, saved)
         xpl = self._exchange_plan(ctx, plan)
@@ -565,6 +632,16 @@ class RankLayer:
                                             None, self.pk, sv["R"])
             dw1p, dw2p = dw1g, dw2g
             rows = dxp
+        elif sv.get("peer") is not None:
+            st, dgates, dw1p, dw2p = self._backward_peer(ctx, u, sv, dec, plan)
+            dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
+                              p.renormalize_topk)
+            dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
+            px = sv["peer"]
+            dx = K.ep_combine(st["pair_dst"], st["pair_rrow"], H, px.peer_base, px.off["dxr"],
+                              out=dx_sh, accumulate=dx_sh is not None)
+            K.router_term(dz, self.wg, dx)
+            return dx, K.router_wgrad(x, dz), dw1p, dw2p
         elif sv.get("overlap"):
             rows, dgates, dw1p, dw2p = self._backward_overlap(ctx, u, sv, dec, plan)
         else:
@@ -624,13 +701,15 @@ def _validate(blocks, topology, params, seq_len):
 def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingParams, world,
                 seq_len: Optional[int] = None, workers: Optional[int] = None, *, dtype=None,
                 check_finite_inputs: bool = True, shared_weights: Optional[X.ExpertWeights] = None,
-                pad_to_capacity: bool = False):
+                pad_to_capacity: bool = False, exchange: Optional[str] = None):
     """Run the MoE layer forward on every rank of ``world`` (dispatcher.py:246-384).
 
     ``world`` is a LocalWorld (all ranks in this process) or an NcclWorld
     (this process's rank only; other entries of the returned list are None).
     ``dtype`` selects the compute precision (torch.float32 parity mode or
     torch.bfloat16); default: the dtype of the blocks' values (fp64 -> fp32).
+    ``exchange`` picks the EP all-to-all: "peer" (device-side over NVLink
+    peer memory; bf16, ETP = 1) or "nccl"; default $B200MOE_EP_EXCHANGE or "peer".
     """
     groups = _validate(blocks, topology, params, seq_len)
     if hasattr(world, "setup_groups"):
@@ -647,7 +726,9 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
         dt = dtype or (b.values.dtype if b.values.dtype in (torch.float32, torch.bfloat16) else torch.float32)
         layer = RankLayer(params, w, topology, _rank_groups(topology, groups, rank), rank, dt, dev,
                           seq_len, check=check_finite_inputs, shared=shared_weights,
-                          pad_to_capacity=pad_to_capacity)
+                          pad_to_capacity=pad_to_capacity, exchange=exchange,
+                          peer_tokens=max((b_.values.shape[0] for b_ in blocks if b_ is not None),
+                                          default=0))
         out, saved = layer.forward(ctx, b.values, b.positions)
         saved["layer"] = layer
         return out, saved

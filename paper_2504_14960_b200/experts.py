@@ -234,7 +234,8 @@ def _gemm(A, B, C, **kw):
 
 
 def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor],
-                pk: PackedExperts, max_rows: int, gend: Optional[torch.Tensor] = None):
+                pk: PackedExperts, max_rows: int, gend: Optional[torch.Tensor] = None,
+                y_out: Optional[torch.Tensor] = None):
     """pre = xp W1_g ; h = act(pre) ; y = h W2_g  for every group g
     (experts.py:130-143 batched over groups).  Returns (pre, h, y).
     ``gend`` (optional) gives explicit group ends so groups may skip rows;
@@ -254,7 +255,7 @@ def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[tor
               b_sg=N1 * H, b_sk=1, b_sn=H, c_sg=0, ldc=N1, group_off=goff, group_expert=gexp,
               max_rows=max_rows, group_end=gend)
         K.act_fwd(pre, act, goff, G, F, out=h)
-    y = torch.empty((R, H), dtype=dt, device=xp.device)
+    y = torch.empty((R, H), dtype=dt, device=xp.device) if y_out is None else y_out
     _gemm(h, pk.w2p, y, grouped_dim=0, G=G, M=0, N=H, K=F, a_sm=F, a_sk=1, b_sg=H * F, b_sk=1,
           b_sn=F, c_sg=0, ldc=H, group_off=goff, group_expert=gexp, max_rows=max_rows,
           group_end=gend)
@@ -263,7 +264,8 @@ def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[tor
 
 def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torch.Tensor,
                  goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor], pk: PackedExperts,
-                 max_rows: int, want_dx: bool = True, gend: Optional[torch.Tensor] = None):
+                 max_rows: int, want_dx: bool = True, gend: Optional[torch.Tensor] = None,
+                 dx_out: Optional[torch.Tensor] = None):
     """experts.py:146-172 batched over groups: returns (dxp, dw1p, dw2p) with
     dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert)."""
     from . import gemm_tc
@@ -284,7 +286,7 @@ def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torc
         K.act_bwd(dh, pre, act, goff, G, F, out=dpre)
     dxp = None
     if want_dx:
-        dxp = torch.empty((R, H), dtype=dt, device=dev)
+        dxp = torch.empty((R, H), dtype=dt, device=dev) if dx_out is None else dx_out
         _gemm(dpre, pk.w1p, dxp, grouped_dim=0, G=G, M=0, N=H, K=N1, a_sm=N1, a_sk=1,
               b_sg=N1 * H, b_sk=H, b_sn=1, c_sg=0, ldc=H, group_off=goff, group_expert=gexp,
               max_rows=max_rows, group_end=gend)

@@ -220,6 +220,68 @@ def act_fwd(pre, act: int, group_off, G: int, F: int, out=None):
     return out
 
 
+# ------------------------------------------------ EP exchange over peer memory
+# peer_base: int64 device tensor [ep] with the base address of every EP
+# member's symmetric buffer (peer.PeerExchange owns it and the region offsets).
+def ep_counts_push(counts: torch.Tensor, me: int, ep: int, peer_base, cnt_off: int):
+    _cuda(counts, "counts", torch.int32)
+    L.call("b200moe_ep_counts_push", L.ptr(counts), me, ep, counts.numel(), L.ptr(peer_base),
+           cnt_off, _sp())
+
+
+def ep_barrier(peer_base, flag_off: int, me: int, ep: int, epoch: int):
+    L.call("b200moe_ep_barrier", L.ptr(peer_base), flag_off, me, ep, epoch & 0xFFFFFFFF, _sp())
+
+
+def ep_layout(cnt: torch.Tensor, me: int, ep: int, L_: int, align: int, cap_rows: int):
+    """-> (seg_off [ep*L], goff [L+1], gcount [L]) int32 on the device."""
+    dev = cnt.device
+    seg_off = torch.empty((ep * L_,), dtype=torch.int32, device=dev)
+    goff = torch.empty((L_ + 1,), dtype=torch.int32, device=dev)
+    gcount = torch.empty((L_,), dtype=torch.int32, device=dev)
+    L.call("b200moe_ep_layout", L.ptr(cnt), me, ep, L_, align, cap_rows, L.ptr(seg_off), L.ptr(goff),
+           L.ptr(gcount), _sp())
+    return seg_off, goff, gcount
+
+
+def ep_zero_pads(buf: torch.Tensor, goff, gcount, G: int, align: int):
+    _cuda(buf, "receive buffer", torch.bfloat16)
+    L.call("b200moe_ep_zero_pads", L.ptr(buf), buf.shape[1], L.ptr(goff), L.ptr(gcount), G, align,
+           _sp())
+
+
+def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int, peer_base,
+                dst_off: int, bwd: bool = False, y_off: int = 0, gates=None):
+    """Forward: push x rows to the owners' receive buffers -> (pair_dst, pair_rrow).
+    Backward: push gates*u rows, pull y rows -> dgates [T, k] fp32."""
+    T, H = x.shape
+    k = topk_idx.shape[1]
+    _cuda(x, "x", torch.bfloat16)
+    dev = x.device
+    if bwd:
+        dg = torch.empty((T, k), dtype=torch.float32, device=dev)
+        L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
+               L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), dst_off, y_off, L.ptr(gates),
+               L.ptr(dg), None, None, 1, _sp())
+        return dg
+    pd = torch.empty((T, k), dtype=torch.int32, device=dev)
+    pr = torch.empty((T, k), dtype=torch.int32, device=dev)
+    L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
+           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), dst_off, 0, None, None, L.ptr(pd),
+           L.ptr(pr), 0, _sp())
+    return pd, pr
+
+
+def ep_combine(pair_dst, pair_rrow, H: int, peer_base, src_off: int, gates=None, out=None,
+               out_dtype=torch.bfloat16, accumulate: bool = False):
+    T, k = pair_dst.shape
+    if out is None:
+        out = torch.empty((T, H), dtype=out_dtype, device=pair_dst.device)
+    L.call("b200moe_ep_combine", T, H, k, L.ptr(pair_dst), L.ptr(pair_rrow), L.ptr(peer_base),
+           src_off, L.ptr(gates), L.ptr(out), L.dtype_code(out.dtype), int(accumulate), _sp())
+    return out
+
+
 def act_bwd(dh, pre, act: int, group_off, G: int, F: int, out=None):
     rows = pre.shape[0]
     if out is None:

@@ -1,4 +1,4 @@
-"""Multi-GPU parity check of the NCCL path (run under torchrun, >= 2 GPUs).
+"""Multi-GPU parity check of the NCCL and NVLink peer-memory paths (run under torchrun, >= 2 GPUs).
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port 29511 tests/dist_layer_check.py
@@ -47,7 +47,8 @@ def main():
     E, k, H, F, seq = 8, 2, 128, 256, 256
     failures = []
     for ci, (tp, cp, ep, etp, cf, mode, act) in enumerate(cases(world)):
-        for dtype, tol in ((torch.float32, 1e-5), (torch.bfloat16, 2e-2)):
+        for dtype, tol, xch in ((torch.float32, 1e-5, "nccl"), (torch.bfloat16, 2e-2, "peer"),
+                                (torch.bfloat16, 2e-2, "nccl")):
             seed = 40 + ci
             topo = B.ParallelTopology(world_size=world, tp=tp, cp=cp, ep=ep, etp=etp)
             params = B.GatingParams(w_g=B.init_gating_matrix(H, E, seed), k=k, capacity_factor=cf,
@@ -56,13 +57,14 @@ def main():
             _, blocks = B.fabricate_token_blocks(topo, seq, topo.dp, H, seed, dtype=dtype, device=dev)
             _, ups = B.fabricate_upstream(topo, seq, topo.dp, H, seed, dtype=dtype, device=dev)
             nw = B.NcclWorld()
-            outs, fctx = B.moe_forward(blocks, weights, topo, params, nw, seq_len=seq)
+            outs, fctx = B.moe_forward(blocks, weights, topo, params, nw, seq_len=seq, exchange=xch)
             res = B.moe_backward(ups, fctx)
             lw = B.LocalWorld(world, dev)
-            outs2, fctx2 = B.moe_forward(blocks, weights, topo, params, lw, seq_len=seq)
+            outs2, fctx2 = B.moe_forward(blocks, weights, topo, params, lw, seq_len=seq, exchange=xch)
             res2 = B.moe_backward(ups, fctx2)
             torch.cuda.synchronize()
-            tag = f"case{ci} {topo} cf={cf} {mode} {act} {dtype}"
+            peer = fctx.per_rank[rank].get("peer") is not None
+            tag = f"case{ci} {topo} cf={cf} {mode} {act} {dtype} {'peer' if peer else 'nccl'}"
             d1 = fctx.per_rank[rank]["decision"]
             d2 = fctx2.per_rank[rank]["decision"]
             if not (torch.equal(d1.experts, d2.experts) and torch.equal(d1.kept, d2.kept)):

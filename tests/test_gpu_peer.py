@@ -1,0 +1,131 @@
+"""GPU: the device-side EP exchange over peer memory (peer.py, csrc/ep_peer.cu)
+against the NCCL-style exchange and the oracle.
+
+Ranks are threads on one GPU (LocalWorld): the same dispatch / combine /
+layout kernels run, with a host rendezvous in place of the flag barrier
+(which tests/dist_layer_check.py exercises across real GPUs).  Expert rows
+are computed by the same GEMM whatever their position in the receive buffer,
+so forward outputs must match the NCCL path bit for bit; gradients differ
+only in fp32 summation order."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import moe_oracle as O  # noqa: E402
+
+import paper_2504_14960_b200 as B  # noqa: E402
+from paper_2504_14960_b200.errors import ProtocolError, ValidationError  # noqa: E402
+
+BF16_TOL = 2e-2
+
+
+def _blocks(sizes, H, seed):
+    rng = np.random.default_rng(seed)
+    out, ups, start = [], [], 0
+    for n in sizes:
+        pos = np.arange(start, start + n)
+        start += n
+        out.append(B.TokenBlock(torch.as_tensor(rng.standard_normal((n, H)), dtype=torch.float32)
+                                .to("cuda", torch.bfloat16), pos))
+        ups.append(torch.as_tensor(rng.standard_normal((n, H)), dtype=torch.float32)
+                   .to("cuda", torch.bfloat16))
+    return out, ups
+
+
+def _run(exchange, topo, params, weights, blocks, ups, shared=None):
+    world = B.LocalWorld(topo.world_size)
+    outs, ctx = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16,
+                              exchange=exchange, shared_weights=shared)
+    res = B.moe_backward(ups, ctx)
+    return outs, ctx, res
+
+
+CASES = [
+    # world, ep, E, k, H, F, sizes, cf, act
+    (2, 2, 8, 2, 256, 512, (384, 384), None, "swiglu"),
+    (2, 2, 8, 2, 128, 256, (96, 300), 1.0, "swiglu"),  # ragged blocks, dropping
+    (4, 4, 4, 2, 128, 192, (64, 128, 0, 200), None, "gelu"),  # k > L, an empty rank
+    (4, 2, 8, 4, 64, 128, (160, 96, 128, 64), 1.25, "swiglu"),  # ep < world (EDP = 2)
+    (4, 4, 16, 8, 64, 64, (256, 256, 256, 256), None, "swiglu"),  # k = 8
+]
+
+
+@pytest.mark.parametrize("world,ep,E,k,H,F,sizes,cf,act", CASES)
+def test_peer_exchange_matches_nccl_exchange(world, ep, E, k, H, F, sizes, cf, act):
+    seed = 11
+    topo = B.ParallelTopology(world_size=world, ep=ep)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=cf)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=ep, activation=act)
+    blocks, ups = _blocks(sizes, H, seed)
+    o0, c0, r0 = _run("nccl", topo, params, weights, blocks, ups)
+    o1, c1, r1 = _run("peer", topo, params, weights, blocks, ups)
+    for r in range(world):
+        assert c1.per_rank[r].get("peer") is not None
+        assert c0.per_rank[r].get("peer") is None
+        np.testing.assert_array_equal(c0.per_rank[r]["decision"].kept.cpu().numpy(),
+                                      c1.per_rank[r]["decision"].kept.cpu().numpy())
+        if sizes[r]:
+            torch.testing.assert_close(o1[r], o0[r], rtol=0, atol=0)
+            assert O.rel_err(r1.input_grads[r].float().cpu().numpy(),
+                             r0.input_grads[r].float().cpu().numpy()) < 1e-2
+    assert O.rel_err(r1.w_g_grad.cpu().numpy(), r0.w_g_grad.cpu().numpy()) < 1e-3
+    for key in r0.expert_grads:
+        for a, b in zip(r0.expert_grads[key][0] + r0.expert_grads[key][1],
+                        r1.expert_grads[key][0] + r1.expert_grads[key][1]):
+            assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-3
+
+
+def test_peer_exchange_with_shared_expert_vs_oracle():
+    """2 emulated ranks, E16 top-4 SwiGLU + shared expert, bf16, vs the oracle
+    fed the GPU's logits and bf16-rounded inputs."""
+    from paper_2504_14960_b200.experts import init_shared_expert
+
+    E, k, H, F, Fs, seed = 16, 4, 256, 256, 512, 5
+    sizes = (512, 320)
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    wg = O.gating_matrix(H, E, seed)
+    params = B.GatingParams(w_g=wg, k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
+    shared = init_shared_expert(H, Fs, seed)
+    blocks, ups = _blocks(sizes, H, seed)
+    outs, ctx, res = _run("peer", topo, params, weights, blocks, ups, shared)
+    experts = []
+    for ei in range(2):
+        w = weights[(ei, 0)]
+        experts += [O.Expert(np.asarray(a), np.asarray(b), "swiglu") for a, b in zip(w.w1, w.w2)]
+    sh = O.Expert(np.asarray(shared.w1[0]), np.asarray(shared.w2[0]), "swiglu")
+    cfg = O.LayerConfig(k=k)
+    dwg = np.zeros_like(wg)
+    for r in range(2):
+        assert ctx.per_rank[r].get("peer") is not None
+        lg = ctx.per_rank[r]["logits"].double().cpu().numpy()
+        x = blocks[r].values.double().cpu().numpy()
+        u = ups[r].double().cpu().numpy()
+        y, st = O.layer_forward(x, lg, experts, cfg, shared=sh)
+        g = O.layer_backward(u, st, experts, cfg, w_g=wg, shared=sh)
+        np.testing.assert_array_equal(ctx.per_rank[r]["decision"].experts.cpu().numpy(),
+                                      st.routing.experts)
+        assert O.rel_err(outs[r].double().cpu().numpy(), y) < BF16_TOL
+        assert O.rel_err(res.input_grads[r].double().cpu().numpy(), g[0]) < BF16_TOL
+        dwg += g[2]
+    assert O.rel_err(res.w_g_grad.cpu().numpy(), dwg) < BF16_TOL
+
+
+def test_peer_buffers_reused_before_backward_fail_loudly():
+    E, k, H, F = 8, 2, 64, 64
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, 1), k=k)
+    weights = B.init_expert_weights(E, H, F, 1, 1, ep_size=2, activation="swiglu")
+    blocks, ups = _blocks((64, 64), H, 1)
+    world = B.LocalWorld(2)
+    _, ctx_a = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16)
+    _, ctx_b = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16)
+    B.moe_backward(ups, ctx_b)
+    with pytest.raises(ProtocolError, match="reused"):
+        B.moe_backward(ups, ctx_a)
+    # a later, larger token block than the buffers were sized for
+    big, _ = _blocks((128, 64), H, 2)
+    with pytest.raises(ValidationError, match="peer buffers"):
+        B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
