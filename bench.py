@@ -3,7 +3,8 @@
 Workload (N=1): Mixtral-8x7B MoE layer shape -- 8 experts top-2, hidden 4096,
 expert FFN 14336 (SwiGLU), 16384 tokens per GPU, dropless, bf16 -- all 8
 experts on the one GPU (EP=1).  N>1 (torchrun, one rank per GPU): EP=N with
-16384 tokens per GPU (weak scaling), NCCL all-to-all-v dispatch/combine.
+16384 tokens per GPU (weak scaling); dispatch/combine are device-side pushes
+and pulls over NVLink peer memory (B200MOE_EP_EXCHANGE=nccl: NCCL all-to-all-v).
 
 A step = router -> dispatch -> grouped SwiGLU FFN -> combine, then the full
 backward (input, router and expert weight gradients).  Synthetic N(0,1)
@@ -339,6 +340,7 @@ def main():
     for n, m in all_launches:
         if not n.startswith("gemm_tc"):
             other[n] = other.get(n, 0.0) + m
+    _, sv_last = layer.forward(ctx, x, positions)
     # all-to-all bus bandwidth (nccl-tests convention: bytes sent incl. self /
     # time * (n-1)/n), per direction per GPU, against 900 GB/s NVLink 5
     a2a = None
@@ -350,10 +352,23 @@ def main():
         a2a = {"busbw_gbs": busbw, "nominal_gbs": 900.0, "frac_nominal": busbw / 900.0,
                "ms_per_step": t_a2a * 1e3, "calls_per_step": len(a2a_events),
                "bytes_per_step": sent, "impl": "NCCL all_to_all_single (grouped P2P)"}
+    peer_events = [(n, m) for n, m in all_launches if n in ("ep_dispatch", "ep_combine")]
+    if peer_events and world > 1:
+        # device-side exchange: per step the kept pairs' rows cross the fabric
+        # 5 times (fwd push, fwd pull, bwd push + y pull, bwd pull); the
+        # (ep-1)/ep remote share of those bytes over the dispatch+combine time
+        # is the per-GPU, per-direction NVLink rate
+        pairs = float(sv_last["plan"].counts.sum())
+        moved = 5 * pairs * H * 2
+        t_x = sum(m for _, m in peer_events) / 1e3
+        remote = moved * (ep - 1) / ep
+        a2a = {"busbw_gbs": remote / t_x / 1e9, "nominal_gbs": 900.0,
+               "frac_nominal": remote / t_x / 1e9 / 900.0, "ms_per_step": t_x * 1e3,
+               "bytes_per_step": moved, "remote_bytes_per_step": remote,
+               "impl": "NVLink peer memory: ep_dispatch push / ep_combine pull kernels (peer.py)"}
     # kept (token, expert) pairs of the last step, summed over ranks; each
     # pair costs 18*H*F flop fwd+bwd with SwiGLU (6PHF + 12PHF),
     # shared expert 18*T*H*Fs; per-GPU share of the whole job
-    _, sv_last = layer.forward(ctx, x, positions)
     kept = torch.tensor([float(sv_last["plan"].counts.sum())], device=dev)
     if world > 1:
         dist.all_reduce(kept)
