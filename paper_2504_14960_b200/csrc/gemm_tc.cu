@@ -59,7 +59,7 @@ struct Params {
   int64_t ldpre;
   int panel_m;     // raster panel height in m-tiles
   int tile_m;      // rows per tile: 128 (1 CTA) or 256 (CTA pair)
-  int debug_nostore;  // perf experiments only: skip epilogue global traffic
+  int debug_nostore;  // perf experiments only: 1 = no epilogue global traffic, 2 = no bulk stores
   int use_tma;        // output tensor maps are valid (TMA-store epilogue)
 };
 
@@ -208,6 +208,7 @@ struct Stager {
   uint32_t base;
   int buf;
   bool leader;
+  bool skip;  // perf experiments: everything but the bulk store itself
   __device__ __forceinline__ uint32_t acquire() {
     if (leader) bulk_wait_read<NSTG - 1>();  // the store that last used this tile has read it
     epi_bar();
@@ -216,7 +217,7 @@ struct Stager {
   __device__ __forceinline__ void issue(const CUtensorMap* map, int c0, int c1, int c2, bool reduce) {
     fence_async_smem();  // generic-proxy smem writes -> visible to the TMA (async proxy)
     epi_bar();
-    if (leader) {
+    if (leader && !skip) {
       const uint32_t src = base + buf * STG_BYTES;
       if (reduce) tma_reduce_add_3d(map, src, c0, c1, c2);
       else tma_store_3d(map, src, c0, c1, c2);
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
     const int row_in_tile = BM * (int)crank + 32 * q + lane;
-    Stager<C::NSTG> stgr{stg, 0, threadIdx.x == 128};
+    Stager<C::NSTG> stgr{stg, 0, threadIdx.x == 128, p.debug_nostore == 2};
     uint32_t ld_par = 0;  // phase bits of the staging-ring load barriers
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -652,7 +653,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(tfull_bar + 8 * acc, acc_phase);
       tc_fence_after();
       const int64_t row = tl.m0 + row_in_tile;
-      const bool live = row < tl.m_end && !p.debug_nostore;
+      const bool live = row < tl.m_end && p.debug_nostore != 1;
       const bool zero = tl.nkb == 0;
       const int64_t c_off = p.grouped_k ? (int64_t)tl.g * p.c_sg : 0;
       const uint32_t t_row = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
@@ -660,7 +661,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // store path), entirely past it (nothing to do) or -- only for
       // unaligned groups -- ragged (direct masked stores).
       const int64_t row0 = tl.m0 + BM * (int64_t)crank;
-      const bool cta_live = row0 < tl.m_end && !p.debug_nostore;
+      const bool cta_live = row0 < tl.m_end && p.debug_nostore != 1;
       const bool tma_path = p.use_tma && row0 + BM <= tl.m_end && p.epi <= EPI_SWIGLU_BWD;
       const int r = 32 * q + lane;
       if (!cta_live) {
@@ -1064,7 +1065,7 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.ldpre = a->ldpre;
   p.tile_m = BM * cg;
   const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
-  p.debug_nostore = (ns && ns[0] == '1') ? 1 : 0;
+  p.debug_nostore = (ns && (ns[0] == '1' || ns[0] == '2')) ? ns[0] - '0' : 0;
   p.panel_m = choose_panel(a, p.tile_m);
 
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
