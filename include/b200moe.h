@@ -242,10 +242,12 @@ B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, 
                                     const float* gates, float* dgates, int32_t* pair_dst,
                                     int32_t* pair_rrow, int bwd, void* stream);
 /* pull-combine: out[t] (+)= sum_s w_s * row(pair_dst, pair_rrow) read from
- * the peers' buffer at src_off (w = gates or 1). */
+ * the peers' buffer at src_off (w = gates or 1) [+ dz[t] . w_gT, E <= 8:
+ * the router term of the input gradient, as in b200moe_combine]. */
 B200MOE_API int b200moe_ep_combine(int64_t T, int64_t H, int k, const int32_t* pair_dst,
                                    const int32_t* pair_rrow, const uint64_t* peer_base,
-                                   int64_t src_off, const float* gates, void* out, int out_dtype,
+                                   int64_t src_off, const float* gates, const float* dz,
+                                   const float* w_gT, int E, void* out, int out_dtype,
                                    int accumulate, void* stream);
 
 /* Elementwise expert activations in the padded row layout, rows < group_off[G].

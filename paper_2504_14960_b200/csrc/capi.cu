@@ -46,7 +46,7 @@ int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const i
                 const int32_t*, const int32_t*, const uint64_t*, int64_t, int64_t, const float*,
                 float*, int32_t*, int32_t*, int, cudaStream_t);
 int ep_combine(int64_t, int64_t, int, const int32_t*, const int32_t*, const uint64_t*, int64_t,
-               const float*, void*, int, int, cudaStream_t);
+               const float*, const float*, const float*, int, void*, int, int, cudaStream_t);
 int act_fwd(const void*, int, int, const int32_t*, int, int64_t, int64_t, void*, cudaStream_t);
 int act_bwd(const void*, const void*, int, int, const int32_t*, int, int64_t, int64_t, void*,
             cudaStream_t);
@@ -272,13 +272,14 @@ int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const
 }
 
 int b200moe_ep_combine(int64_t T, int64_t H, int k, const int32_t* pair_dst, const int32_t* pair_rrow,
-                       const uint64_t* peer_base, int64_t src_off, const float* gates, void* out,
-                       int out_dtype, int accumulate, void* stream) {
+                       const uint64_t* peer_base, int64_t src_off, const float* gates, const float* dz,
+                       const float* w_gT, int E, void* out, int out_dtype, int accumulate, void* stream) {
   REQUIRE(H % 8 == 0 && dt_ok(out_dtype), "ep_combine: bad args");
+  REQUIRE(!dz || (w_gT && E >= 1 && E <= 8), "ep_combine: the fused router term needs w_gT and E <= 8");
   if (T == 0) return B200MOE_OK;
   REQUIRE(pair_dst && pair_rrow && peer_base && out, "ep_combine: null pointer");
-  return ep_combine(T, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, out, out_dtype, accumulate,
-                    S(stream));
+  return ep_combine(T, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, dz, w_gT, E, out, out_dtype,
+                    accumulate, S(stream));
 }
 
 int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,

@@ -157,25 +157,42 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       pair_rrow[t * k + s] = rr;
     }
   }
+  // U column chunks per iteration keep several 16 B loads (local x, remote
+  // y) in flight per lane
+  constexpr int U = KMAX >= 4 ? 2 : 4;
   const __nv_bfloat16* src = x + t * H;
-  for (int64_t c = (int64_t)lane * 8; c < H; c += 256) {
-    Vec16<__nv_bfloat16> v;
-    v.raw = ld_nc_v4(src + c);
+  for (int64_t c0 = (int64_t)lane * 8; c0 < H; c0 += 256 * U) {
+    Vec16<__nv_bfloat16> v[U];
+    Vec16<__nv_bfloat16> y[BWD ? U : 1][BWD ? KMAX : 1];
 #pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-      if (!dst[s]) continue;
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + u * 256;
+      if (c < H) v[u].raw = ld_nc_v4(src + c);
       if (BWD) {
-        Vec16<__nv_bfloat16> y, o;
-        y.raw = ld_v4(ysrc[s] + c);  // NVLink pull (peer L2)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float uv = __bfloat162float(v.v[i]);
-          dot[s] = fmaf(uv, __bfloat162float(y.v[i]), dot[s]);
-          o.v[i] = __float2bfloat16_rn(uv * g[s]);
+        for (int s = 0; s < KMAX; ++s)
+          if (dst[s] && c < H) y[u][s].raw = ld_v4(ysrc[s] + c);  // NVLink pull (peer L2)
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + u * 256;
+      if (c >= H) break;
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (!dst[s]) continue;
+        if (BWD) {
+          Vec16<__nv_bfloat16> o;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float uv = __bfloat162float(v[u].v[i]);
+            dot[s] = fmaf(uv, __bfloat162float(y[BWD ? u : 0][BWD ? s : 0].v[i]), dot[s]);
+            o.v[i] = __float2bfloat16_rn(uv * g[s]);
+          }
+          st_v4(dst[s] + c, o.raw);
+        } else {
+          st_v4(dst[s] + c, v[u].raw);  // NVLink push
         }
-        st_v4(dst[s] + c, o.raw);
-      } else {
-        st_v4(dst[s] + c, v.raw);  // NVLink push
       }
     }
   }
@@ -191,12 +208,14 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
 
 // ------------------------------------------------------------------ combine
 // out[t] = sum_s w_s * row(pair_dst[s], pair_rrow[s]) pulled from the peers'
-// buffer at src_off (w = gates, or 1); accumulate adds to out.
+// buffer at src_off (w = gates, or 1) [+ dz[t] . w_g^T, the router term of the
+// input gradient, for E <= 8]; accumulate adds to out.
 template <typename Tout, int KMAX>
 __global__ void __launch_bounds__(256) ep_combine_kernel(
     int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_dst,
     const int32_t* __restrict__ pair_rrow, const uint64_t* __restrict__ peer_base, int64_t src_off,
-    const float* __restrict__ gates, Tout* __restrict__ out, int accumulate) {
+    const float* __restrict__ gates, const float* __restrict__ dz, const float* __restrict__ wgT, int E,
+    Tout* __restrict__ out, int accumulate) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -212,27 +231,45 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(
     src[s] = reinterpret_cast<const __nv_bfloat16*>(peer_base[d] + src_off) + (int64_t)pair_rrow[t * k + s] * H;
     if (gates) w[s] = gates[t * k + s];
   }
-  for (int64_t c = (int64_t)lane * 8; c < H; c += 256) {
-    Vec16<__nv_bfloat16> v[KMAX];
+  constexpr int U = KMAX >= 8 ? 1 : (KMAX >= 4 ? 2 : 4);  // U*KMAX rows' chunks in flight
+  for (int64_t c0 = (int64_t)lane * 8; c0 < H; c0 += 256 * U) {
+    Vec16<__nv_bfloat16> v[U][KMAX];
 #pragma unroll
-    for (int s = 0; s < KMAX; ++s)
-      if (src[s]) v[s].raw = ld_v4(src[s] + c);
-    float acc[8];
+    for (int u = 0; u < U; ++u)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      for (int s = 0; s < KMAX; ++s)
+        if (src[s] && c0 + u * 256 < H) v[u][s].raw = ld_v4(src[s] + c0 + u * 256);
 #pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-      if (!src[s]) continue;
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + u * 256;
+      if (c >= H) break;
+      float acc[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = fmaf(w[s], __bfloat162float(v[s].v[i]), acc[i]);
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (!src[s]) continue;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(w[s], __bfloat162float(v[u][s].v[i]), acc[i]);
+      }
+      if (dz) {
+        for (int e = 0; e < E; ++e) {
+          const float4* wp = reinterpret_cast<const float4*>(wgT + (int64_t)e * H + c);
+          const float4 wa = __ldg(wp), wb = __ldg(wp + 1);
+          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+          const float d = __ldg(dz + t * E + e);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = fmaf(d, wv[i], acc[i]);
+        }
+      }
+      Tout* o = out + t * H + c;
+      if (accumulate) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += to_f32(o[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = from_f32<Tout>(acc[i]);
     }
-    Tout* o = out + t * H + c;
-    if (accumulate) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += to_f32(o[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = from_f32<Tout>(acc[i]);
   }
 }
 
@@ -293,11 +330,11 @@ int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_
 }
 
 int ep_combine(int64_t Tn, int64_t H, int k, const int32_t* pair_dst, const int32_t* pair_rrow,
-               const uint64_t* peer_base, int64_t src_off, const float* gates, void* out, int out_dtype,
-               int accumulate, cudaStream_t st) {
+               const uint64_t* peer_base, int64_t src_off, const float* gates, const float* dz,
+               const float* wgT, int E, void* out, int out_dtype, int accumulate, cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div(Tn, 8);
-#define CBF(KM) ep_combine_kernel<__nv_bfloat16, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, static_cast<__nv_bfloat16*>(out), accumulate)
-#define CF(KM) ep_combine_kernel<float, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, static_cast<float*>(out), accumulate)
+#define CBF(KM) ep_combine_kernel<__nv_bfloat16, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, dz, wgT, E, static_cast<__nv_bfloat16*>(out), accumulate)
+#define CF(KM) ep_combine_kernel<float, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, dz, wgT, E, static_cast<float*>(out), accumulate)
   if (Tn > 0) {
     if (out_dtype == B200MOE_BF16) { KSW(k, CBF) }
     else { KSW(k, CF) }

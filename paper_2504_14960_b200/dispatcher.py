@@ -638,9 +638,12 @@ class RankLayer:
                               p.renormalize_topk)
             dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
             px = sv["peer"]
+            fuse = E <= 8  # router term in the combine (w_g^T chunks reused per warp)
             dx = K.ep_combine(st["pair_dst"], st["pair_rrow"], H, px.peer_base, px.off["dxr"],
-                              out=dx_sh, accumulate=dx_sh is not None)
-            K.router_term(dz, self.wg, dx)
+                              dz=dz if fuse else None, w_gT=self.wgT if fuse else None, out=dx_sh,
+                              accumulate=dx_sh is not None)
+            if not fuse:
+                K.router_term(dz, self.wg, dx)
             return dx, K.router_wgrad(x, dz), dw1p, dw2p
         elif sv.get("overlap"):
             rows, dgates, dw1p, dw2p = self._backward_overlap(ctx, u, sv, dec, plan)

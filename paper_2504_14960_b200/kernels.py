@@ -272,13 +272,17 @@ def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int,
     return pd, pr
 
 
-def ep_combine(pair_dst, pair_rrow, H: int, peer_base, src_off: int, gates=None, out=None,
-               out_dtype=torch.bfloat16, accumulate: bool = False):
+def ep_combine(pair_dst, pair_rrow, H: int, peer_base, src_off: int, gates=None, dz=None, w_gT=None,
+               out=None, out_dtype=torch.bfloat16, accumulate: bool = False):
+    """Pull-combine from the peers' buffers; with dz (E <= 8) also adds the
+    router term dz @ w_g^T of the input gradient."""
     T, k = pair_dst.shape
     if out is None:
         out = torch.empty((T, H), dtype=out_dtype, device=pair_dst.device)
+    E = 0 if dz is None else dz.shape[1]
     L.call("b200moe_ep_combine", T, H, k, L.ptr(pair_dst), L.ptr(pair_rrow), L.ptr(peer_base),
-           src_off, L.ptr(gates), L.ptr(out), L.dtype_code(out.dtype), int(accumulate), _sp())
+           src_off, L.ptr(gates), L.ptr(dz), L.ptr(w_gT), E, L.ptr(out), L.dtype_code(out.dtype),
+           int(accumulate), _sp())
     return out
 
 
