@@ -209,8 +209,8 @@ typedef struct {
 B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);
 
 /* ------------------------------------- EP all-to-all over NVLink peer memory
- * Device-side replacement of all_to_all_v + exchange_meta
- * (dispatcher.py:310-361, 430-466).  peer_base[ep] (device array) holds the
+ * Device-side replacement of all_to_all_v + exchange_meta + the grp_order
+ * regroup (dispatcher.py:309-362, 425-468).  peer_base[ep] (device array) holds the
  * base address of the same symmetric buffer on every rank of the EP group;
  * regions are addressed by byte offsets.  No call synchronises the host. */
 

@@ -1,15 +1,16 @@
 // EP all-to-all over NVLink peer memory (symmetric buffers), fused with the
 // permute / combine work -- the device-side replacement of the reference's
-// all_to_all_v + exchange_meta pair (dispatcher.py:310-361, 430-466).
+// all_to_all_v + exchange_meta + regroup of dispatcher.py:309-362, 425-468.
 //
 // Every rank of an EP group maps the same symmetric buffer layout; peer
 // addresses are  peer_base[d] + region offset.  Per forward step:
 //   counts_push   each rank writes its per-expert kept counts into row `me` of
 //                 every peer's count matrix                      (+ barrier)
 //   layout        every rank derives, from the full count matrix, the
-//                 receive layout of each destination: segments (sender s,
-//                 local expert le), s-major, each padded to `align` rows; it
-//                 keeps its own push offsets and its own GEMM group offsets
+//                 receive layout of each destination: expert-major, senders
+//                 contiguous in rank order inside an expert (the reference's
+//                 stable `grp_order` regroup), each expert padded to `align`
+//                 rows; it keeps its own push offsets and its GEMM groups
 //   dispatch      one warp per token reads x[t] once and stores it straight
 //                 into the destination ranks' receive buffers    (+ barrier)
 //   ... grouped GEMM on the local receive buffer ...             (+ barrier)
