@@ -352,20 +352,22 @@ def main():
         a2a = {"busbw_gbs": busbw, "nominal_gbs": 900.0, "frac_nominal": busbw / 900.0,
                "ms_per_step": t_a2a * 1e3, "calls_per_step": len(a2a_events),
                "bytes_per_step": sent, "impl": "NCCL all_to_all_single (grouped P2P)"}
-    peer_events = [(n, m) for n, m in all_launches if n in ("ep_dispatch", "ep_combine")]
+    peer_events = [(n, m) for n, m in all_launches if n == "ep_dispatch"]
     if peer_events and world > 1:
-        # device-side exchange: per step the kept pairs' rows cross the fabric
-        # 5 times (fwd push, fwd pull, bwd push + y pull, bwd pull); the
-        # (ep-1)/ep remote share of those bytes over the dispatch+combine time
-        # is the per-GPU, per-direction NVLink rate
+        # device-side exchange: the dispatch kernels push the kept pairs' rows
+        # twice per step (x forward, g*u backward); the (ep-1)/ep remote share
+        # of those bytes over the dispatch time is the per-GPU, per-direction
+        # NVLink rate.  The return direction (y, dx) is stored by the GEMM
+        # epilogues while they compute and has no separate time.
         pairs = float(sv_last["plan"].counts.sum())
-        moved = 5 * pairs * H * 2
+        moved = 2 * pairs * H * 2
         t_x = sum(m for _, m in peer_events) / 1e3
         remote = moved * (ep - 1) / ep
         a2a = {"busbw_gbs": remote / t_x / 1e9, "nominal_gbs": 900.0,
                "frac_nominal": remote / t_x / 1e9 / 900.0, "ms_per_step": t_x * 1e3,
                "bytes_per_step": moved, "remote_bytes_per_step": remote,
-               "impl": "NVLink peer memory: ep_dispatch push / ep_combine pull kernels (peer.py)"}
+               "return_bytes_in_gemm_epilogues": moved,
+               "impl": "NVLink peer memory: ep_dispatch push kernels + GEMM scatter epilogues (peer.py)"}
     # kept (token, expert) pairs of the last step, summed over ranks; each
     # pair costs 18*H*F flop fwd+bwd with SwiGLU (6PHF + 12PHF),
     # shared expert 18*T*H*Fs; per-GPU share of the whole job

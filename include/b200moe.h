@@ -188,7 +188,8 @@ B200MOE_API int b200moe_gemm_simt(const b200moe_gemm_args* args, void* stream);
  * grouped_dim 1 (K): group g reduces over rows [group_off[g], group_off[g+1])
  *   (multiples of 64), C_g = C + g*c_sg.
  * epilogue: 0 store (bf16/fp32, accumulate), 1 SwiGLU fwd (C=pre, H=h),
- *   2 SwiGLU bwd (acc=dh [.,N=F], PRE=pre, C=dpre), 3 act fwd, 4 act bwd.
+ *   2 SwiGLU bwd (acc=dh [.,N=F], PRE=pre, C=dpre), 3 act fwd, 4 act bwd,
+ *   5 scatter to peers (see row_origin).
  * num_ctas: persistent grid size (<= 0: one CTA per SM). */
 typedef struct {
   int G;
@@ -204,6 +205,12 @@ typedef struct {
   const void* PRE; int64_t ldpre;
   int num_ctas;
   const int32_t* group_end; /* nullable: group g = [group_off[g], group_end[g]) (gaps allowed) */
+  /* epilogue 5 (scatter, bf16, grouped M): C is not written; row r goes to
+   * peer_base[row_origin[2r]] + scatter_off + row_origin[2r+1] * ldc * 2 (a
+   * peer's buffer over NVLink, or this rank's); rows with row_origin[2r] < 0
+   * are skipped.  Replaces the return all_to_all_v of dispatcher.py:355-361
+   * (and :462-466 backward), overlapped with the GEMM. */
+  const int32_t* row_origin; const uint64_t* peer_base; int64_t scatter_off;
 } b200moe_tc_gemm_args;
 
 B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);
@@ -229,26 +236,22 @@ B200MOE_API int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, 
 B200MOE_API int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align,
                                   int64_t cap_rows, int32_t* seg_off, int32_t* goff, int32_t* gcount,
                                   void* stream);
-/* zero the pad rows of this rank's receive buffer (bf16 [rows, H]) */
+/* zero the pad rows of this rank's receive buffer (bf16 [rows, H]); with
+ * origin (int32 [rows, 2]) also mark them "no origin" for the scatter epilogue */
 B200MOE_API int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount,
-                                     int G, int align, void* stream);
-/* fused permute + push: x[t] (bwd: gates*u[t]) -> row seg_off[d,le] +
- * (gemm_row - poff[e]) of rank d's buffer at dst_off; bwd also pulls the
- * expert output row at y_off for dgates; fwd records pair_dst/pair_rrow. */
+                                     int G, int align, int32_t* origin, void* stream);
+/* fused permute + push: x[t] (bwd: gates*u[t]) -> row rr = seg_off[d,le] +
+ * (gemm_row - poff[e]) of rank d's buffer at dst_off.  Forward also writes
+ * (me, gemm_row) into rank d's int32 [rows, 2] origin table at origin_off, so
+ * d's GEMM epilogue (b200moe_gemm_tc epilogue 5) returns the expert output
+ * straight to this rank's padded layout.  Backward reads those returned rows
+ * (y_rows, local, padded layout) for dgates = <u[t], y>. */
 B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L,
                                     const int32_t* topk_idx, const int32_t* gemm_row,
                                     const int32_t* poff, const int32_t* seg_off,
-                                    const uint64_t* peer_base, int64_t dst_off, int64_t y_off,
-                                    const float* gates, float* dgates, int32_t* pair_dst,
-                                    int32_t* pair_rrow, int bwd, void* stream);
-/* pull-combine: out[t] (+)= sum_s w_s * row(pair_dst, pair_rrow) read from
- * the peers' buffer at src_off (w = gates or 1) [+ dz[t] . w_gT, E <= 8:
- * the router term of the input gradient, as in b200moe_combine]. */
-B200MOE_API int b200moe_ep_combine(int64_t T, int64_t H, int k, const int32_t* pair_dst,
-                                   const int32_t* pair_rrow, const uint64_t* peer_base,
-                                   int64_t src_off, const float* gates, const float* dz,
-                                   const float* w_gT, int E, void* out, int out_dtype,
-                                   int accumulate, void* stream);
+                                    const uint64_t* peer_base, int me, int64_t dst_off,
+                                    int64_t origin_off, const void* y_rows, const float* gates,
+                                    float* dgates, int bwd, void* stream);
 
 /* Elementwise expert activations in the padded row layout, rows < group_off[G].
  * SwiGLU layout: pre has 2F columns, 64-column blocks of [32 gate | 32 up]. */

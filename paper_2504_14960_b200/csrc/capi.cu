@@ -41,12 +41,10 @@ int gemm_tc(const b200moe_tc_gemm_args*, cudaStream_t);
 int ep_barrier(const uint64_t*, int64_t, int, int, uint32_t, cudaStream_t);
 int ep_counts_push(const int32_t*, int, int, int, const uint64_t*, int64_t, cudaStream_t);
 int ep_layout(const int32_t*, int, int, int, int, int64_t, int32_t*, int32_t*, int32_t*, cudaStream_t);
-int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, cudaStream_t);
+int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
-                const int32_t*, const int32_t*, const uint64_t*, int64_t, int64_t, const float*,
-                float*, int32_t*, int32_t*, int, cudaStream_t);
-int ep_combine(int64_t, int64_t, int, const int32_t*, const int32_t*, const uint64_t*, int64_t,
-               const float*, const float*, const float*, int, void*, int, int, cudaStream_t);
+                const int32_t*, const int32_t*, const uint64_t*, int, int64_t, int64_t, const void*,
+                const float*, float*, int, cudaStream_t);
 int act_fwd(const void*, int, int, const int32_t*, int, int64_t, int64_t, void*, cudaStream_t);
 int act_bwd(const void*, const void*, int, int, const int32_t*, int, int64_t, int64_t, void*,
             cudaStream_t);
@@ -219,8 +217,9 @@ int b200moe_gemm_tc(const b200moe_tc_gemm_args* a, void* stream) {
   REQUIRE(a->N >= 1 && a->a_rows >= 0 && a->b_batch >= 1, "gemm_tc: bad shape");
   REQUIRE(a->grouped_dim == 1 || a->K >= 1, "gemm_tc: bad K");
   REQUIRE(a->grouped_dim == 0 || a->M >= 1, "gemm_tc: bad M");
-  REQUIRE(a->A && a->B && a->C && a->group_off, "gemm_tc: null pointer");
-  REQUIRE(a->epilogue >= 0 && a->epilogue <= 4, "gemm_tc: bad epilogue %d", a->epilogue);
+  REQUIRE(a->A && a->B && (a->C || a->epilogue == 5) && a->group_off, "gemm_tc: null pointer");
+  REQUIRE(a->epilogue >= 0 && a->epilogue <= 5, "gemm_tc: bad epilogue %d", a->epilogue);
+  REQUIRE(a->epilogue != 5 || (a->row_origin && a->peer_base), "gemm_tc: scatter needs row_origin, peer_base");
   REQUIRE(a->epilogue == 0 || a->grouped_dim == 0, "gemm_tc: fused epilogues need grouped M");
   REQUIRE(a->epilogue == 0 || a->out_dtype == B200MOE_BF16, "gemm_tc: fused epilogues write bf16");
   REQUIRE(!a->accumulate || a->out_dtype == B200MOE_F32, "gemm_tc: accumulate needs fp32 out");
@@ -254,32 +253,21 @@ int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align
 }
 
 int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G,
-                         int align, void* stream) {
+                         int align, int32_t* origin, void* stream) {
   REQUIRE(buf && goff && gcount && H >= 1, "ep_zero_pads: bad args");
-  return ep_zero_pads(buf, H, goff, gcount, G, align, S(stream));
+  return ep_zero_pads(buf, H, goff, gcount, G, align, origin, S(stream));
 }
 
 int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const int32_t* topk_idx,
                         const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
-                        const uint64_t* peer_base, int64_t dst_off, int64_t y_off, const float* gates,
-                        float* dgates, int32_t* pair_dst, int32_t* pair_rrow, int bwd, void* stream) {
-  REQUIRE(H % 8 == 0 && k >= 1 && L >= 1, "ep_dispatch: H %% 8 and k >= 1 required");
+                        const uint64_t* peer_base, int me, int64_t dst_off, int64_t origin_off,
+                        const void* y_rows, const float* gates, float* dgates, int bwd, void* stream) {
+  REQUIRE(H % 8 == 0 && k >= 1 && L >= 1 && me >= 0, "ep_dispatch: H %% 8, k >= 1, me >= 0 required");
   if (T == 0) return B200MOE_OK;
   REQUIRE(x && topk_idx && gemm_row && poff && seg_off && peer_base, "ep_dispatch: null pointer");
-  REQUIRE(bwd ? (gates && dgates) : (pair_dst && pair_rrow), "ep_dispatch: null pointer");
-  return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, dst_off, y_off, gates,
-                     dgates, pair_dst, pair_rrow, bwd, S(stream));
-}
-
-int b200moe_ep_combine(int64_t T, int64_t H, int k, const int32_t* pair_dst, const int32_t* pair_rrow,
-                       const uint64_t* peer_base, int64_t src_off, const float* gates, const float* dz,
-                       const float* w_gT, int E, void* out, int out_dtype, int accumulate, void* stream) {
-  REQUIRE(H % 8 == 0 && dt_ok(out_dtype), "ep_combine: bad args");
-  REQUIRE(!dz || (w_gT && E >= 1 && E <= 8), "ep_combine: the fused router term needs w_gT and E <= 8");
-  if (T == 0) return B200MOE_OK;
-  REQUIRE(pair_dst && pair_rrow && peer_base && out, "ep_combine: null pointer");
-  return ep_combine(T, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, dz, w_gT, E, out, out_dtype,
-                    accumulate, S(stream));
+  REQUIRE(!bwd || (gates && dgates && y_rows), "ep_dispatch: backward needs gates, dgates, y_rows");
+  return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, dst_off, origin_off,
+                     y_rows, gates, dgates, bwd, S(stream));
 }
 
 int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,

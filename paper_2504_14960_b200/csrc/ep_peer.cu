@@ -102,29 +102,33 @@ __global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int me, int ep
   if (d == me) goff[L] = (int32_t)run;
 }
 
-// zero the alignment pad rows of this rank's receive buffer
+// zero the alignment pad rows of this rank's receive buffer (and, forward,
+// mark them "no origin" so the scatter epilogue skips them)
 __global__ void ep_zero_pads_kernel(__nv_bfloat16* __restrict__ buf, int64_t H,
-                                    const int32_t* __restrict__ goff, const int32_t* __restrict__ gcount) {
+                                    const int32_t* __restrict__ goff, const int32_t* __restrict__ gcount,
+                                    int32_t* __restrict__ origin) {
   const int g = blockIdx.y;
   const int64_t row = (int64_t)goff[g] + gcount[g] + blockIdx.x;
   if (row >= goff[g + 1]) return;
   __nv_bfloat16* p = buf + row * H;
   for (int64_t c = threadIdx.x; c < H; c += blockDim.x) p[c] = __float2bfloat16_rn(0.f);
+  if (origin && threadIdx.x == 0) origin[2 * row] = -1;
 }
 
 // ------------------------------------------------------------------ dispatch
-// Forward: rows x[t] -> dest receive buffers.  Backward (scale != NULL):
-// rows g*u[t] -> dest, and dgate = <u[t], y_row> with y pulled from the
-// dest's output buffer at the same row.  Also records, per pair, the
-// (dest, remote row) that the combines use.
+// Forward: x[t] -> row rr of the owner's receive buffer, and origin[rr] =
+// (this rank, the pair's row in this rank's padded layout) so the owner's
+// GEMM epilogue can return the expert output straight to that row.
+// Backward (BWD): g*u[t] -> the same rows of the owner's dyr, and
+// dgate = <u[t], y> with y read locally from the returned expert outputs.
 template <int KMAX, bool BWD>
 __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     const __nv_bfloat16* __restrict__ x, int64_t Tn, int64_t H, int k, int L,
     const int32_t* __restrict__ topk, const int32_t* __restrict__ gemm_row,
     const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
-    const uint64_t* __restrict__ peer_base, int64_t dst_off, int64_t y_off,
-    const float* __restrict__ gates, float* __restrict__ dgates, int32_t* __restrict__ pair_dst,
-    int32_t* __restrict__ pair_rrow) {
+    const uint64_t* __restrict__ peer_base, int me, int64_t dst_off, int64_t origin_off,
+    const __nv_bfloat16* __restrict__ y_rows, const float* __restrict__ gates,
+    float* __restrict__ dgates) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -139,27 +143,20 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     dot[s] = 0.f;
     if (s >= k) continue;
     const int32_t gr = gemm_row[t * k + s];
-    if (gr < 0) {
-      if (!BWD && lane == 0) {
-        pair_dst[t * k + s] = -1;
-        pair_rrow[t * k + s] = -1;
-      }
-      continue;
-    }
+    if (gr < 0) continue;
     const int e = topk[t * k + s];
     const int d = e / L, le = e % L;
     const int32_t rr = seg_off[d * L + le] + (gr - poff[e]);
     dst[s] = reinterpret_cast<__nv_bfloat16*>(peer_base[d] + dst_off) + (int64_t)rr * H;
     if (BWD) {
-      ysrc[s] = reinterpret_cast<const __nv_bfloat16*>(peer_base[d] + y_off) + (int64_t)rr * H;
+      ysrc[s] = y_rows + (int64_t)gr * H;
       g[s] = gates[t * k + s];
     } else if (lane == 0) {
-      pair_dst[t * k + s] = d;
-      pair_rrow[t * k + s] = rr;
+      int2* o = reinterpret_cast<int2*>(peer_base[d] + origin_off) + rr;
+      *o = make_int2(me, gr);
     }
   }
-  // U column chunks per iteration keep several 16 B loads (local x, remote
-  // y) in flight per lane
+  // U column chunks per iteration keep several 16 B loads in flight per lane
   constexpr int U = KMAX >= 4 ? 2 : 4;
   const __nv_bfloat16* src = x + t * H;
   for (int64_t c0 = (int64_t)lane * 8; c0 < H; c0 += 256 * U) {
@@ -172,7 +169,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       if (BWD) {
 #pragma unroll
         for (int s = 0; s < KMAX; ++s)
-          if (dst[s] && c < H) y[u][s].raw = ld_v4(ysrc[s] + c);  // NVLink pull (peer L2)
+          if (dst[s] && c < H) y[u][s].raw = ld_nc_v4(ysrc[s] + c);
       }
     }
 #pragma unroll
@@ -190,7 +187,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
             dot[s] = fmaf(uv, __bfloat162float(y[BWD ? u : 0][BWD ? s : 0].v[i]), dot[s]);
             o.v[i] = __float2bfloat16_rn(uv * g[s]);
           }
-          st_v4(dst[s] + c, o.raw);
+          st_v4(dst[s] + c, o.raw);  // NVLink push
         } else {
           st_v4(dst[s] + c, v[u].raw);  // NVLink push
         }
@@ -203,73 +200,6 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       if (s >= k) break;
       const float d = warp_sum(dot[s]);
       if (lane == 0) dgates[t * k + s] = dst[s] ? d : 0.f;
-    }
-  }
-}
-
-// ------------------------------------------------------------------ combine
-// out[t] = sum_s w_s * row(pair_dst[s], pair_rrow[s]) pulled from the peers'
-// buffer at src_off (w = gates, or 1) [+ dz[t] . w_g^T, the router term of the
-// input gradient, for E <= 8]; accumulate adds to out.
-template <typename Tout, int KMAX>
-__global__ void __launch_bounds__(256) ep_combine_kernel(
-    int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_dst,
-    const int32_t* __restrict__ pair_rrow, const uint64_t* __restrict__ peer_base, int64_t src_off,
-    const float* __restrict__ gates, const float* __restrict__ dz, const float* __restrict__ wgT, int E,
-    Tout* __restrict__ out, int accumulate) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= Tn) return;
-  const __nv_bfloat16* src[KMAX];
-  float w[KMAX];
-#pragma unroll
-  for (int s = 0; s < KMAX; ++s) {
-    src[s] = nullptr;
-    w[s] = 1.f;
-    if (s >= k) continue;
-    const int32_t d = pair_dst[t * k + s];
-    if (d < 0) continue;
-    src[s] = reinterpret_cast<const __nv_bfloat16*>(peer_base[d] + src_off) + (int64_t)pair_rrow[t * k + s] * H;
-    if (gates) w[s] = gates[t * k + s];
-  }
-  constexpr int U = KMAX >= 8 ? 1 : (KMAX >= 4 ? 2 : 4);  // U*KMAX rows' chunks in flight
-  for (int64_t c0 = (int64_t)lane * 8; c0 < H; c0 += 256 * U) {
-    Vec16<__nv_bfloat16> v[U][KMAX];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int s = 0; s < KMAX; ++s)
-        if (src[s] && c0 + u * 256 < H) v[u][s].raw = ld_v4(src[s] + c0 + u * 256);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t c = c0 + u * 256;
-      if (c >= H) break;
-      float acc[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-#pragma unroll
-      for (int s = 0; s < KMAX; ++s) {
-        if (!src[s]) continue;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fmaf(w[s], __bfloat162float(v[u][s].v[i]), acc[i]);
-      }
-      if (dz) {
-        for (int e = 0; e < E; ++e) {
-          const float4* wp = reinterpret_cast<const float4*>(wgT + (int64_t)e * H + c);
-          const float4 wa = __ldg(wp), wb = __ldg(wp + 1);
-          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
-          const float d = __ldg(dz + t * E + e);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] = fmaf(d, wv[i], acc[i]);
-        }
-      }
-      Tout* o = out + t * H + c;
-      if (accumulate) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += to_f32(o[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = from_f32<Tout>(acc[i]);
     }
   }
 }
@@ -304,22 +234,23 @@ int ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align, int64_
 }
 
 int ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G, int align,
-                 cudaStream_t st) {
+                 int32_t* origin, cudaStream_t st) {
   if (align <= 1 || G <= 0) return B200MOE_OK;
   dim3 grid((unsigned)(align - 1), (unsigned)G);
-  ep_zero_pads_kernel<<<grid, 128, 0, st>>>(static_cast<__nv_bfloat16*>(buf), H, goff, gcount);
+  ep_zero_pads_kernel<<<grid, 128, 0, st>>>(static_cast<__nv_bfloat16*>(buf), H, goff, gcount, origin);
   B200MOE_CHECK_LAUNCH("ep_zero_pads");
   return B200MOE_OK;
 }
 
 int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_t* topk,
                 const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
-                const uint64_t* peer_base, int64_t dst_off, int64_t y_off, const float* gates,
-                float* dgates, int32_t* pair_dst, int32_t* pair_rrow, int bwd, cudaStream_t st) {
+                const uint64_t* peer_base, int me, int64_t dst_off, int64_t origin_off,
+                const void* y_rows, const float* gates, float* dgates, int bwd, cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div(Tn, 8);
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
-#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, dst_off, y_off, gates, dgates, pair_dst, pair_rrow)
-#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, dst_off, y_off, gates, dgates, pair_dst, pair_rrow)
+  const __nv_bfloat16* yb = static_cast<const __nv_bfloat16*>(y_rows);
+#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, dst_off, origin_off, yb, gates, dgates)
+#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, dst_off, origin_off, yb, gates, dgates)
   if (Tn > 0) {
     if (bwd) { KSW(k, DB) }
     else { KSW(k, DF) }
@@ -327,22 +258,6 @@ int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_
 #undef DF
 #undef DB
   B200MOE_CHECK_LAUNCH("ep_dispatch");
-  return B200MOE_OK;
-}
-
-int ep_combine(int64_t Tn, int64_t H, int k, const int32_t* pair_dst, const int32_t* pair_rrow,
-               const uint64_t* peer_base, int64_t src_off, const float* gates, const float* dz,
-               const float* wgT, int E, void* out, int out_dtype, int accumulate, cudaStream_t st) {
-  const unsigned grid = (unsigned)ceil_div(Tn, 8);
-#define CBF(KM) ep_combine_kernel<__nv_bfloat16, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, dz, wgT, E, static_cast<__nv_bfloat16*>(out), accumulate)
-#define CF(KM) ep_combine_kernel<float, KM><<<grid, 256, 0, st>>>(Tn, H, k, pair_dst, pair_rrow, peer_base, src_off, gates, dz, wgT, E, static_cast<float*>(out), accumulate)
-  if (Tn > 0) {
-    if (out_dtype == B200MOE_BF16) { KSW(k, CBF) }
-    else { KSW(k, CF) }
-  }
-#undef CBF
-#undef CF
-  B200MOE_CHECK_LAUNCH("ep_combine");
   return B200MOE_OK;
 }
 

@@ -35,6 +35,7 @@ enum Epi : int {
   EPI_SWIGLU_BWD = 2,  // acc = dh [.. F]; reads pre -> dpre (interleaved)
   EPI_ACT_FWD = 3,     // acc = pre -> pre (bf16), h = act(pre)
   EPI_ACT_BWD = 4,     // acc = dh; reads pre -> dpre = dh * act'(pre)
+  EPI_SCATTER = 5,     // bf16 rows straight to the ranks they came from (peer memory)
 };
 
 struct Params {
@@ -61,6 +62,10 @@ struct Params {
   int tile_m;      // rows per tile: 128 (1 CTA) or 256 (CTA pair)
   int debug_nostore;  // perf experiments only: 1 = no epilogue global traffic, 2 = no bulk stores
   int use_tma;        // output tensor maps are valid (TMA-store epilogue)
+  // EPI_SCATTER: row r -> peer_base[origin[2r]] + scatter_off + origin[2r+1] * ldc * 2
+  const int32_t* origin;
+  const uint64_t* peer_base;
+  int64_t scatter_off;
 };
 
 // Per-CTA-group configuration.  CG = 2: a CTA pair (cluster of 2 on one TPC)
@@ -183,6 +188,10 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void st_global_v4(uint64_t addr, uint4 v) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
@@ -666,6 +675,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int r = 32 * q + lane;
       if (!cta_live) {
         // this CTA half holds no rows of the group
+      } else if (p.epi == EPI_SCATTER) {
+        // Fused return exchange: each bf16 row goes straight to the rank that
+        // sent it, at that rank's own row, so the transfer overlaps the MMAs
+        // of the next tile.  A warp stages its 32 rows (swizzled) in its own
+        // 4 KB of the staging tile and writes them back 4 rows x 128 B per
+        // instruction (full-line NVLink writes); only __syncwarp is needed.
+        uint64_t dst = 0;
+        if (live) {
+          const int32_t d = p.origin[2 * row];
+          if (d >= 0)
+            dst = p.peer_base[d] + (uint64_t)p.scatter_off + (uint64_t)p.origin[2 * row + 1] * p.ldc * 2;
+        }
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          const int64_t n = tl.n0 + c * 64;
+          if (n >= p.N) break;
+          uint32_t v0[32], v1[32];
+          tmem_ld32(t_row + c * 64, v0);
+          tmem_ld32(t_row + c * 64 + 32, v1);
+          float f0[32], f1[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            f0[i] = __uint_as_float(v0[i]);
+            f1[i] = __uint_as_float(v1[i]);
+          }
+          uint4 o[8];
+          pack32_bf16(f0, o);
+          pack32_bf16(f1, o + 4);
+          st_row_chunk(stg, r, o);
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int src = 4 * it + (lane >> 3), j = lane & 7;
+            const uint64_t d = __shfl_sync(0xffffffffu, dst, src);
+            const int rr = 32 * q + src;
+            const uint4 v = ld_shared_v4(stg + rr * 128 + ((j ^ (rr & 7)) << 4));
+            const int64_t col = n + 8 * j;
+            if (d && col < p.N) st_global_v4(d + col * 2, v);
+          }
+          __syncwarp();
+        }
       } else if (tma_path) {
         const int crow = (int)row0;
         if (p.epi == EPI_STORE && p.out_f32) {
@@ -991,6 +1041,13 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
     set_error("gemm_tc: leading dimensions must be multiples of 8 elements (16 B)");
     return B200MOE_EUNSUPPORTED;
   }
+  if (a->epilogue == EPI_SCATTER &&
+      (a->grouped_dim != 0 || a->out_dtype != B200MOE_BF16 || !a->row_origin || !a->peer_base ||
+       (a->ldc % 8) || (a->N % 8))) {
+    set_error("gemm_tc: the scatter epilogue needs grouped M, bf16 output, row_origin, peer_base "
+              "and N, ldc multiples of 8");
+    return B200MOE_EUNSUPPORTED;
+  }
   // CTA pairs (cta_group::2, 256 x 256 tiles) by default; B200MOE_CTA_GROUP=1
   // selects single-CTA 128 x 256 tiles.  num_ctas must be even for pairs.
   const char* cg_str = getenv("B200MOE_CTA_GROUP");
@@ -1063,6 +1120,9 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.ldh = a->ldh;
   p.PRE = a->PRE;
   p.ldpre = a->ldpre;
+  p.origin = a->row_origin;
+  p.peer_base = a->peer_base;
+  p.scatter_off = a->scatter_off;
   p.tile_m = BM * cg;
   const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
   p.debug_nostore = (ns && (ns[0] == '1' || ns[0] == '2')) ? ns[0] - '0' : 0;

@@ -319,8 +319,12 @@ class RankLayer:
         want = exchange or os.environ.get("B200MOE_EP_EXCHANGE", "peer")
         if want not in ("peer", "nccl"):
             raise ValidationError(f"unknown EP exchange {want!r}", constraint="exchange")
+        from . import gemm_tc
+
+        # (the return exchange is the tensor-core GEMM's scatter epilogue)
         self.use_peer = (want == "peer" and not self.single and len(groups.etp) == 1
-                         and dtype == torch.bfloat16 and self.k <= 8 and self.pk.hidden % 8 == 0)
+                         and dtype == torch.bfloat16 and self.k <= 8 and gemm_tc.available()
+                         and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
 
     # ------------------------------------------------------- shared expert
     # Builder-defined (no reference): a dense FFN over every token whose
@@ -533,8 +537,9 @@ class RankLayer:
     # ---- device-side EP exchange over NVLink peer memory (peer.py).  Tokens
     # are pushed straight from the token block into the owners' receive
     # buffers (no send buffer, no host sync), the GEMMs run on the receive
-    # buffer with one group per local expert, and the combines pull the rows
-    # back from the peers.
+    # buffer with one group per local expert, and the second GEMM's epilogue
+    # stores every output row straight back into the padded layout of the
+    # rank it came from, so the combines read local memory.
     def _peer(self, ctx, T: int):
         from . import peer as PX
 
@@ -548,7 +553,12 @@ class RankLayer:
             T_max = max(int(self.peer_tokens or 0), T)
             T_max = max(int(v) for v in ctx.exchange_meta(self.g.ep, T_max).values())
             cap = PX.capacity_rows(len(self.g.ep), T_max, self.k, self.L, ALIGN)
-            px = PX.PeerExchange(ctx, self.g.ep, self.E, self.L, H, cap, self.device)
+            ret = T_max * self.k + self.E * (ALIGN - 1)  # this rank's padded pair layout
+            if self.pad_to_capacity and not self.params.dropless:
+                seg = (capacity_limit(self.params.capacity_factor, T_max, self.E) + ALIGN - 1) // ALIGN
+                ret = max(ret, self.E * seg * ALIGN)
+            ret = (ret + ALIGN - 1) // ALIGN * ALIGN
+            px = PX.PeerExchange(ctx, self.g.ep, self.E, self.L, H, cap, ret, self.device)
             px.tokens = T_max
             cache[key] = px
         elif T > px.tokens:
@@ -558,32 +568,27 @@ class RankLayer:
         return px
 
     def _forward_peer(self, ctx, x, dec, plan, saved):
-        H = x.shape[1]
-        px = self._peer(ctx, x.shape[0])
+        T = x.shape[0]
+        px = self._peer(ctx, T)
         st = px.forward_dispatch(x, dec.experts, plan, ALIGN)
         pre, h, _ = X.ffn_forward(px.region("xr"), st["goff"], self.L, None, self.pk, px.cap,
-                                  y_out=px.region("yr"))
+                                  y_scatter=px.scatter("yret"))
         y_sh = self._shared_forward(x, saved)
-        px.barrier()  # every expert output row is in place
-        out = K.ep_combine(st["pair_dst"], st["pair_rrow"], H, px.peer_base, px.off["yr"],
-                           gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
+        px.barrier()  # every expert output row is back in yret
+        out = K.combine(px.region("yret"), plan.gemm_row, T, gates=dec.gates, out=y_sh,
+                        accumulate=y_sh is not None)
         saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row)
         return out, saved
 
     def _backward_peer(self, ctx, u, sv, dec, plan):
         px, st = sv["peer"], sv["pst"]
         px.check_generation(st)
-        H = u.shape[1]
-        dyr = px.region("dyr")
-        K.ep_zero_pads(dyr, st["goff"], st["gcount"], self.L, ALIGN)
-        dgates = K.ep_dispatch(u, dec.experts, plan.gemm_row, plan.poffsets, st["seg_off"], self.L,
-                               px.peer_base, px.off["dyr"], bwd=True, y_off=px.off["yr"],
-                               gates=dec.gates)
-        px.barrier()  # every upstream row is in place
-        _, dw1p, dw2p = X.ffn_backward(dyr, px.region("xr"), sv["pre"], sv["h"], st["goff"], self.L,
-                                       None, self.pk, px.cap, dx_out=px.region("dxr"))
-        px.barrier()  # every input-gradient row is in place
-        return st, dgates, dw1p, dw2p
+        dgates = px.backward_dispatch(u, dec.experts, plan, dec.gates, st, ALIGN)
+        _, dw1p, dw2p = X.ffn_backward(px.region("dyr"), px.region("xr"), sv["pre"], sv["h"],
+                                       st["goff"], self.L, None, self.pk, px.cap,
+                                       dx_scatter=px.scatter("dxret"))
+        px.barrier()  # every input-gradient row is back in dxret
+        return px.region("dxret"), dgates, dw1p, dw2p
 
     def _forward_exchange(self, ctx, x, dec, plan, saved):
         T, H = x.shape
@@ -633,18 +638,7 @@ class RankLayer:
             dw1p, dw2p = dw1g, dw2g
             rows = dxp
         elif sv.get("peer") is not None:
-            st, dgates, dw1p, dw2p = self._backward_peer(ctx, u, sv, dec, plan)
-            dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
-                              p.renormalize_topk)
-            dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
-            px = sv["peer"]
-            fuse = E <= 8  # router term in the combine (w_g^T chunks reused per warp)
-            dx = K.ep_combine(st["pair_dst"], st["pair_rrow"], H, px.peer_base, px.off["dxr"],
-                              dz=dz if fuse else None, w_gT=self.wgT if fuse else None, out=dx_sh,
-                              accumulate=dx_sh is not None)
-            if not fuse:
-                K.router_term(dz, self.wg, dx)
-            return dx, K.router_wgrad(x, dz), dw1p, dw2p
+            rows, dgates, dw1p, dw2p = self._backward_peer(ctx, u, sv, dec, plan)
         elif sv.get("overlap"):
             rows, dgates, dw1p, dw2p = self._backward_overlap(ctx, u, sv, dec, plan)
         else:

@@ -235,11 +235,13 @@ def _gemm(A, B, C, **kw):
 
 def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor],
                 pk: PackedExperts, max_rows: int, gend: Optional[torch.Tensor] = None,
-                y_out: Optional[torch.Tensor] = None):
+                y_scatter=None):
     """pre = xp W1_g ; h = act(pre) ; y = h W2_g  for every group g
     (experts.py:130-143 batched over groups).  Returns (pre, h, y).
     ``gend`` (optional) gives explicit group ends so groups may skip rows;
-    then goff[G] must bound the last end."""
+    then goff[G] must bound the last end.  ``y_scatter`` = (row_origin,
+    peer_base, byte offset): y rows are stored straight into the ranks they
+    came from by the GEMM epilogue (bf16 tensor-core path; y is then None)."""
     from . import gemm_tc
 
     R = xp.shape[0]
@@ -255,7 +257,12 @@ def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[tor
               b_sg=N1 * H, b_sk=1, b_sn=H, c_sg=0, ldc=N1, group_off=goff, group_expert=gexp,
               max_rows=max_rows, group_end=gend)
         K.act_fwd(pre, act, goff, G, F, out=h)
-    y = torch.empty((R, H), dtype=dt, device=xp.device) if y_out is None else y_out
+    if y_scatter is not None:
+        gemm_tc.gemm(h, pk.w2p, None, grouped_dim=0, G=G, M=0, N=H, K=F, a_sm=F, a_sk=1, b_sg=H * F,
+                     b_sk=1, b_sn=F, c_sg=0, ldc=H, group_off=goff, group_expert=gexp,
+                     max_rows=max_rows, group_end=gend, scatter=y_scatter)
+        return pre, h, None
+    y = torch.empty((R, H), dtype=dt, device=xp.device)
     _gemm(h, pk.w2p, y, grouped_dim=0, G=G, M=0, N=H, K=F, a_sm=F, a_sk=1, b_sg=H * F, b_sk=1,
           b_sn=F, c_sg=0, ldc=H, group_off=goff, group_expert=gexp, max_rows=max_rows,
           group_end=gend)
@@ -265,9 +272,10 @@ def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[tor
 def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torch.Tensor,
                  goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor], pk: PackedExperts,
                  max_rows: int, want_dx: bool = True, gend: Optional[torch.Tensor] = None,
-                 dx_out: Optional[torch.Tensor] = None):
+                 dx_scatter=None):
     """experts.py:146-172 batched over groups: returns (dxp, dw1p, dw2p) with
-    dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert)."""
+    dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert).
+    ``dx_scatter``: as ffn_forward's y_scatter, for the input gradient."""
     from . import gemm_tc
 
     R = dyp.shape[0]
@@ -285,8 +293,12 @@ def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torc
               group_end=gend)
         K.act_bwd(dh, pre, act, goff, G, F, out=dpre)
     dxp = None
-    if want_dx:
-        dxp = torch.empty((R, H), dtype=dt, device=dev) if dx_out is None else dx_out
+    if dx_scatter is not None:
+        gemm_tc.gemm(dpre, pk.w1p, None, grouped_dim=0, G=G, M=0, N=H, K=N1, a_sm=N1, a_sk=1,
+                     b_sg=N1 * H, b_sk=H, b_sn=1, c_sg=0, ldc=H, group_off=goff, group_expert=gexp,
+                     max_rows=max_rows, group_end=gend, scatter=dx_scatter)
+    elif want_dx:
+        dxp = torch.empty((R, H), dtype=dt, device=dev)
         _gemm(dpre, pk.w1p, dxp, grouped_dim=0, G=G, M=0, N=H, K=N1, a_sm=N1, a_sk=1,
               b_sg=N1 * H, b_sk=H, b_sn=1, c_sg=0, ldc=H, group_off=goff, group_expert=gexp,
               max_rows=max_rows, group_end=gend)

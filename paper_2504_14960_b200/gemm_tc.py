@@ -15,7 +15,7 @@ import torch
 
 from . import _lib as L
 
-EPI_STORE, EPI_SWIGLU_FWD, EPI_SWIGLU_BWD, EPI_ACT_FWD, EPI_ACT_BWD = range(5)
+EPI_STORE, EPI_SWIGLU_FWD, EPI_SWIGLU_BWD, EPI_ACT_FWD, EPI_ACT_BWD, EPI_SCATTER = range(6)
 P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
 
 
@@ -30,6 +30,7 @@ class TcGemmArgs(ctypes.Structure):
         ("group_off", P), ("group_expert", P),
         ("epilogue", I32), ("act", I32), ("H", P), ("ldh", I64), ("PRE", P), ("ldpre", I64),
         ("num_ctas", I32), ("group_end", P),
+        ("row_origin", P), ("peer_base", P), ("scatter_off", I64),
     ]
 
 
@@ -70,7 +71,7 @@ def supports(**kw) -> bool:
 
 
 _EPI_NAMES = {EPI_STORE: "store", EPI_SWIGLU_FWD: "swiglu_fwd", EPI_SWIGLU_BWD: "swiglu_bwd",
-              EPI_ACT_FWD: "act_fwd", EPI_ACT_BWD: "act_bwd"}
+              EPI_ACT_FWD: "act_fwd", EPI_ACT_BWD: "act_bwd", EPI_SCATTER: "scatter"}
 
 
 def _run(args: TcGemmArgs) -> None:
@@ -85,8 +86,10 @@ def _run(args: TcGemmArgs) -> None:
 
 
 def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg, ldc, group_off,
-         group_expert=None, max_rows=0, accumulate=False, group_end=None):
-    """Same argument convention as kernels.gemm_simt."""
+         group_expert=None, max_rows=0, accumulate=False, group_end=None, scatter=None):
+    """Same argument convention as kernels.gemm_simt.  ``scatter`` =
+    (row_origin, peer_base, byte_offset): bf16 rows go to the ranks they came
+    from instead of C (C may be None; ldc is the destination row length)."""
     a = TcGemmArgs()
     a.G, a.grouped_dim, a.M, a.N, a.K = G, grouped_dim, M, N, K
     a.A, a.a_rows = L.ptr(A), A.shape[0]
@@ -103,11 +106,14 @@ def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg
         a.b_major, a.ldb, a.b_batch, a.b_batch_stride = L.MAJOR_MN, b_sk, 1, 0
     a.B = L.ptr(B)
     a.C, a.ldc, a.c_sg = L.ptr(C), ldc, c_sg
-    a.out_dtype = L.dtype_code(C.dtype)
+    a.out_dtype = L.dtype_code(C.dtype) if C is not None else L.BF16
     a.accumulate = int(accumulate)
     a.group_off, a.group_expert = L.ptr(group_off), L.ptr(group_expert)
     a.group_end = L.ptr(group_end)
     a.epilogue = EPI_STORE
+    if scatter is not None:
+        a.epilogue = EPI_SCATTER
+        a.row_origin, a.peer_base, a.scatter_off = L.ptr(scatter[0]), L.ptr(scatter[1]), scatter[2]
     _run(a)
     return C
 

@@ -244,46 +244,25 @@ def ep_layout(cnt: torch.Tensor, me: int, ep: int, L_: int, align: int, cap_rows
     return seg_off, goff, gcount
 
 
-def ep_zero_pads(buf: torch.Tensor, goff, gcount, G: int, align: int):
+def ep_zero_pads(buf: torch.Tensor, goff, gcount, G: int, align: int, origin=None):
     _cuda(buf, "receive buffer", torch.bfloat16)
     L.call("b200moe_ep_zero_pads", L.ptr(buf), buf.shape[1], L.ptr(goff), L.ptr(gcount), G, align,
-           _sp())
+           L.ptr(origin), _sp())
 
 
-def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int, peer_base,
-                dst_off: int, bwd: bool = False, y_off: int = 0, gates=None):
-    """Forward: push x rows to the owners' receive buffers -> (pair_dst, pair_rrow).
-    Backward: push gates*u rows, pull y rows -> dgates [T, k] fp32."""
+def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int, peer_base, me: int,
+                dst_off: int, origin_off: int = 0, bwd: bool = False, y_rows=None, gates=None):
+    """Forward: push x rows to the owners' receive buffers and record their
+    origin.  Backward: push gates*u rows; returns dgates [T, k] fp32 = <u, y>
+    with y the returned expert outputs (``y_rows``, local padded layout)."""
     T, H = x.shape
     k = topk_idx.shape[1]
     _cuda(x, "x", torch.bfloat16)
-    dev = x.device
-    if bwd:
-        dg = torch.empty((T, k), dtype=torch.float32, device=dev)
-        L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
-               L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), dst_off, y_off, L.ptr(gates),
-               L.ptr(dg), None, None, 1, _sp())
-        return dg
-    pd = torch.empty((T, k), dtype=torch.int32, device=dev)
-    pr = torch.empty((T, k), dtype=torch.int32, device=dev)
+    dg = torch.empty((T, k), dtype=torch.float32, device=x.device) if bwd else None
     L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
-           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), dst_off, 0, None, None, L.ptr(pd),
-           L.ptr(pr), 0, _sp())
-    return pd, pr
-
-
-def ep_combine(pair_dst, pair_rrow, H: int, peer_base, src_off: int, gates=None, dz=None, w_gT=None,
-               out=None, out_dtype=torch.bfloat16, accumulate: bool = False):
-    """Pull-combine from the peers' buffers; with dz (E <= 8) also adds the
-    router term dz @ w_g^T of the input gradient."""
-    T, k = pair_dst.shape
-    if out is None:
-        out = torch.empty((T, H), dtype=out_dtype, device=pair_dst.device)
-    E = 0 if dz is None else dz.shape[1]
-    L.call("b200moe_ep_combine", T, H, k, L.ptr(pair_dst), L.ptr(pair_rrow), L.ptr(peer_base),
-           src_off, L.ptr(gates), L.ptr(dz), L.ptr(w_gT), E, L.ptr(out), L.dtype_code(out.dtype),
-           int(accumulate), _sp())
-    return out
+           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, dst_off, origin_off,
+           L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), _sp())
+    return dg
 
 
 def act_bwd(dh, pre, act: int, group_off, G: int, F: int, out=None):

@@ -1,22 +1,28 @@
-"""EP all-to-all over NVLink peer memory (replaces dispatcher.py:310-361 and
-430-466 of the reference for ETP = 1).
+"""EP all-to-all over NVLink peer memory (replaces dispatcher.py:309-362 and
+425-468 of the reference for ETP = 1).
 
 Every member of an EP group maps one symmetric buffer:
 
-    [flags | count matrix | xr | yr | dyr | dxr]
+    [flags | count matrix | xr | dyr | origin | yret | dxret]
 
-``xr`` receives the token rows routed to this rank's experts (pushed by the
-senders' dispatch kernels straight from their token blocks), ``yr`` holds the
-expert outputs the senders pull back in their combine kernels; ``dyr`` /
-``dxr`` are the backward twins.  Split sizes never reach the host: every
-sender writes its per-expert counts into row ``me`` of every peer's count
-matrix and each rank derives all receive layouts on the device.
+Receive side (rows routed to this rank's experts, expert-major, senders
+contiguous -- the reference's ``grp_order`` layout): ``xr`` gets the token
+rows, pushed by the senders' dispatch kernels straight from their token
+blocks; ``origin`` records for every row (sender, row in the sender's padded
+layout); ``dyr`` gets the backward's g*u rows.  Return side (this rank's own
+pairs, in its padded expert-major layout): ``yret`` / ``dxret`` receive the
+expert outputs / input gradients that the owners' GEMM epilogues store
+directly over NVLink (gemm_tc epilogue 5), so the return all-to-all overlaps
+the GEMM tile by tile and the combines read local memory.
 
-On an NcclWorld the buffer comes from torch symmetric memory (one mapping per
-peer over NVLink) and ranks synchronise with a flag barrier kernel.  On a
-LocalWorld (ranks as threads on one GPU) each rank owns an ordinary device
-buffer, the addresses are exchanged with exchange_meta and the barrier is a
-host rendezvous after a stream synchronize -- the same kernels run on both.
+Split sizes never reach the host: every sender writes its per-expert counts
+into row ``me`` of every peer's count matrix and each rank derives all
+receive layouts on the device.  On an NcclWorld the buffer comes from torch
+symmetric memory (one mapping per peer over NVLink) and ranks synchronise
+with a flag barrier kernel.  On a LocalWorld (ranks as threads on one GPU)
+each rank owns an ordinary device buffer, the addresses are exchanged with
+exchange_meta and the barrier is a host rendezvous after a stream
+synchronize -- the same kernels run on both.
 """
 from __future__ import annotations
 
@@ -30,7 +36,6 @@ from .errors import ProtocolError
 
 _FLAG_BYTES = 4096
 _REGION_ALIGN = 1 << 16
-REGIONS = ("xr", "yr", "dyr", "dxr")
 
 
 def _up(n: int, a: int) -> int:
@@ -44,22 +49,28 @@ def capacity_rows(ep: int, T_max: int, k: int, L_: int, align: int) -> int:
 
 
 class PeerExchange:
-    """Symmetric buffers + device exchange of one EP group, as seen by one rank."""
+    """Symmetric buffers + device exchange of one EP group, as seen by one rank.
 
-    def __init__(self, ctx, group: Tuple[int, ...], E: int, L_: int, H: int, cap_rows: int, device):
+    cap_rows: receive rows (xr/dyr/origin); ret_rows: rows of this rank's own
+    padded pair layout (yret/dxret)."""
+
+    def __init__(self, ctx, group: Tuple[int, ...], E: int, L_: int, H: int, cap_rows: int,
+                 ret_rows: int, device):
         self.group = tuple(group)
         self.ep = len(group)
         self.me = self.group.index(ctx.rank)
-        self.E, self.L, self.H, self.cap = E, L_, H, int(cap_rows)
+        self.E, self.L, self.H = E, L_, H
+        self.cap, self.ret_rows = int(cap_rows), int(ret_rows)
         self.ctx = ctx
         self.device = device
         self.cnt_off = _FLAG_BYTES
         off = _up(self.cnt_off + self.ep * E * 4, _REGION_ALIGN)
         self.off: Dict[str, int] = {}
-        region = _up(self.cap * H * 2, _REGION_ALIGN)
-        for r in REGIONS:
-            self.off[r] = off
-            off += region
+        for name, nbytes in (("xr", self.cap * H * 2), ("dyr", self.cap * H * 2),
+                             ("origin", self.cap * 8), ("yret", self.ret_rows * H * 2),
+                             ("dxret", self.ret_rows * H * 2)):
+            self.off[name] = off
+            off += _up(nbytes, _REGION_ALIGN)
         self.nbytes = off
         self.epoch = 0
         self.generation = 0  # forwards run on these buffers (checked by backward)
@@ -95,14 +106,22 @@ class PeerExchange:
         self.device_barrier = False
 
     def region(self, name: str) -> torch.Tensor:
-        """This rank's [cap, H] bf16 view of a region."""
+        """This rank's bf16 [rows, H] view of a row region."""
         o = self.off[name]
-        n = self.cap * self.H * 2
-        return self.buf[o:o + n].view(torch.bfloat16).view(self.cap, self.H)
+        rows = self.ret_rows if name in ("yret", "dxret") else self.cap
+        return self.buf[o:o + rows * self.H * 2].view(torch.bfloat16).view(rows, self.H)
+
+    def origin(self) -> torch.Tensor:
+        o = self.off["origin"]
+        return self.buf[o:o + self.cap * 8].view(torch.int32).view(self.cap, 2)
 
     def counts(self) -> torch.Tensor:
         """This rank's copy of the [ep, E] count matrix."""
         return self.buf[self.cnt_off:self.cnt_off + self.ep * self.E * 4].view(torch.int32)
+
+    def scatter(self, region: str):
+        """Scatter-epilogue target: (row origin table, peer bases, byte offset)."""
+        return (self.origin(), self.peer_base, self.off[region])
 
     # ------------------------------------------------------------ sync
     def barrier(self):
@@ -116,18 +135,26 @@ class PeerExchange:
 
     # ------------------------------------------------------------ steps
     def forward_dispatch(self, x, topk_idx, plan, align: int):
-        """counts push -> barrier -> layout -> pad zero -> dispatch -> barrier.
-        Returns the saved routing state (seg_off, goff, gcount, pair_dst, pair_rrow)."""
+        """counts push -> barrier -> layout -> pads -> dispatch -> barrier.
+        Returns the routing state the rest of the step needs."""
         K.ep_counts_push(plan.counts, self.me, self.ep, self.peer_base, self.cnt_off)
         self.barrier()
         seg_off, goff, gcount = K.ep_layout(self.counts(), self.me, self.ep, self.L, align, self.cap)
-        K.ep_zero_pads(self.region("xr"), goff, gcount, self.L, align)
-        pd, pr = K.ep_dispatch(x, topk_idx, plan.gemm_row, plan.poffsets, seg_off, self.L,
-                               self.peer_base, self.off["xr"])
+        K.ep_zero_pads(self.region("xr"), goff, gcount, self.L, align, origin=self.origin())
+        K.ep_dispatch(x, topk_idx, plan.gemm_row, plan.poffsets, seg_off, self.L, self.peer_base,
+                      self.me, self.off["xr"], self.off["origin"])
         self.barrier()
         self.generation += 1
-        return dict(seg_off=seg_off, goff=goff, gcount=gcount, pair_dst=pd, pair_rrow=pr,
-                    generation=self.generation)
+        return dict(seg_off=seg_off, goff=goff, gcount=gcount, generation=self.generation)
+
+    def backward_dispatch(self, u, topk_idx, plan, gates, st, align: int):
+        """pads -> push g*u rows (dgates from the returned y) -> barrier."""
+        K.ep_zero_pads(self.region("dyr"), st["goff"], st["gcount"], self.L, align)
+        dg = K.ep_dispatch(u, topk_idx, plan.gemm_row, plan.poffsets, st["seg_off"], self.L,
+                           self.peer_base, self.me, self.off["dyr"], bwd=True,
+                           y_rows=self.region("yret"), gates=gates)
+        self.barrier()
+        return dg
 
     def check_generation(self, st):
         if st["generation"] != self.generation:

@@ -49,6 +49,7 @@ CASES = [
     (4, 4, 4, 2, 128, 192, (64, 128, 0, 200), None, "gelu"),  # k > L, an empty rank
     (4, 2, 8, 4, 64, 128, (160, 96, 128, 64), 1.25, "swiglu"),  # ep < world (EDP = 2)
     (4, 4, 16, 8, 64, 64, (256, 256, 256, 256), None, "swiglu"),  # k = 8
+    (8, 8, 8, 2, 128, 128, (128,) * 8, None, "swiglu"),  # the 8-GPU layout: one expert per rank
 ]
 
 

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--variants", default="",
                     help="comma list of ENV=VAL[;ENV=VAL] settings timed interleaved, e.g. "
                          "'B200MOE_STORE_HINT=0,B200MOE_STORE_HINT=1'")
+    ap.add_argument("--routed", action="store_true", help="uneven groups from a real routing")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     R, E, H, F = a.rows, a.experts, a.hidden, a.ffn
@@ -39,9 +40,22 @@ def main():
     w2 = [(torch.rand((F, H), generator=g, device=dev) * 2 - 1) * bnd for _ in range(E)]
     pk = B.ExpertWeights(tuple(range(E)), w1, w2, "swiglu", 0, 1).packed(torch.bfloat16, dev)
     del w1, w2
+    if a.routed:
+        # group sizes of a real top-2 routing of R/2 tokens (128-row padded layout)
+        from paper_2504_14960_b200 import kernels as K
+
+        T = R // 2
+        xt = torch.randn((T, H), generator=g, device=dev).to(torch.bfloat16)
+        wg = ((torch.rand((H, E), generator=g, device=dev) * 2 - 1) * bnd).float()
+        _, idx, gates, _ = K.router_topk(K.router_logits(xt, wg), 2, 0, False)
+        plan = K.dispatch_plan(idx, gates, E)
+        goff = plan.poffsets
+        R = int(goff[-1])
+        print("routed groups:", [int(v) for v in plan.counts], "rows", R)
+    else:
+        goff = torch.arange(0, R + 1, R // E, dtype=torch.int32, device=dev)
     x = torch.randn((R, H), generator=g, device=dev).to(torch.bfloat16)
     dy = torch.randn((R, H), generator=g, device=dev).to(torch.bfloat16)
-    goff = torch.arange(0, R + 1, R // E, dtype=torch.int32, device=dev)
     pre = torch.empty((R, 2 * F), dtype=torch.bfloat16, device=dev)
     h = torch.empty((R, F), dtype=torch.bfloat16, device=dev)
     y = torch.empty((R, H), dtype=torch.bfloat16, device=dev)
