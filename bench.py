@@ -388,6 +388,8 @@ def main():
             "other_kernels_ms": {n: round(m, 4) for n, m in sorted(other.items(), key=lambda x: -x[1])},
             "instrumented_span_ms": span_ms,
             "launch_gaps_ms": span_ms - sum(m for _, m in all_launches),
+            # the cross-GPU barriers in step order (time = wait for the slowest peer)
+            "ep_barrier_ms": [round(m, 4) for n, m in all_launches if n == "ep_barrier"],
             "layer_frac_of_peak": value / world * flops_step / T / 1e12 / sustained}
 
     # ---- e2e through the public API with host (pinned) buffers

@@ -118,6 +118,20 @@ B200MOE_API size_t b200moe_router_wgrad_ws(int64_t T, int64_t H, int E);
 B200MOE_API int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz, int64_t T, int64_t H, int E,
                          float* dw_g, void* workspace, size_t workspace_bytes, void* stream);
 
+/* fp32 router GEMMs on the bf16 tensor cores (router.py:145, dispatcher.py:
+ * 489-490 for bf16 tokens): an fp32 matrix is split into three bf16 parts
+ * hi + mid + lo that sum to it exactly; with Ep = E rounded up to 8,
+ * out3 [rows, 3 Ep] = (hi | mid | lo) and out6 [rows, 6 Ep] =
+ * (hi | hi | hi | mid | mid | lo) (either may be NULL).  x . W_g then runs
+ * as one b200moe_gemm_tc launch against the W_g parts, dz . W_g^T as one
+ * launch over K = 6 Ep, x^T dz as one split-K launch. */
+B200MOE_API int b200moe_split_bf16x3(const float* src, int64_t rows, int E, void* out3, void* out6,
+                                     void* stream);
+/* out[r, e] = sum over g ascending of ((p[g,r,e] + p[g,r,Ep+e]) + p[g,r,2Ep+e]),
+ * parts [G, rows, 3 Ep] fp32: folds the three part products (and split-K groups). */
+B200MOE_API int b200moe_sum_parts(const float* parts, int64_t G, int64_t rows, int E, float* out,
+                                  void* stream);
+
 /* ------------------------------------------------------- permute/combine */
 
 /* out[row_of(t,s)] = x[t] (* scale[t,s] when scale != NULL) for every kept

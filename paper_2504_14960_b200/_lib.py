@@ -61,6 +61,8 @@ _SIGS = {
     "b200moe_gemm_tc": [P, P],  # argtypes refined in gemm_tc.py
     "b200moe_act_fwd": [P, I32, I32, P, I32, I64, I64, P, P],
     "b200moe_act_bwd": [P, P, I32, I32, P, I32, I64, I64, P, P],
+    "b200moe_split_bf16x3": [P, I64, I32, P, P, P],
+    "b200moe_sum_parts": [P, I64, I64, I32, P, P],
     "b200moe_ep_counts_push": [P, I32, I32, I32, P, I64, P],
     "b200moe_ep_barrier": [P, I64, I32, I32, ctypes.c_uint32, P],
     "b200moe_ep_layout": [P, I32, I32, I32, I32, I64, P, P, P, P],

@@ -45,6 +45,8 @@ int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, int32
 int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
                 const int32_t*, const int32_t*, const uint64_t*, int, int64_t, int64_t, const void*,
                 const float*, float*, int, cudaStream_t);
+int split_bf16x3(const float*, int64_t, int, void*, void*, cudaStream_t);
+int sum_parts(const float*, int64_t, int64_t, int, float*, cudaStream_t);
 int act_fwd(const void*, int, int, const int32_t*, int, int64_t, int64_t, void*, cudaStream_t);
 int act_bwd(const void*, const void*, int, int, const int32_t*, int, int64_t, int64_t, void*,
             cudaStream_t);
@@ -222,7 +224,7 @@ int b200moe_gemm_tc(const b200moe_tc_gemm_args* a, void* stream) {
   REQUIRE(a->epilogue != 5 || (a->row_origin && a->peer_base), "gemm_tc: scatter needs row_origin, peer_base");
   REQUIRE(a->epilogue == 0 || a->grouped_dim == 0, "gemm_tc: fused epilogues need grouped M");
   REQUIRE(a->epilogue == 0 || a->out_dtype == B200MOE_BF16, "gemm_tc: fused epilogues write bf16");
-  REQUIRE(!a->accumulate || a->out_dtype == B200MOE_F32, "gemm_tc: accumulate needs fp32 out");
+  REQUIRE(!a->accumulate || a->epilogue == 0, "gemm_tc: accumulate only with the plain store epilogue");
   REQUIRE((a->epilogue != 1 && a->epilogue != 3) || a->H, "gemm_tc: epilogue needs H");
   REQUIRE((a->epilogue != 2 && a->epilogue != 4) || a->PRE, "gemm_tc: epilogue needs PRE");
   REQUIRE(a->epilogue != 1 || a->N % 64 == 0, "gemm_tc: SwiGLU fwd needs N %% 64 == 0");
@@ -268,6 +270,20 @@ int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const
   REQUIRE(!bwd || (gates && dgates && y_rows), "ep_dispatch: backward needs gates, dgates, y_rows");
   return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, dst_off, origin_off,
                      y_rows, gates, dgates, bwd, S(stream));
+}
+
+int b200moe_split_bf16x3(const float* src, int64_t rows, int E, void* out3, void* out6, void* stream) {
+  REQUIRE(rows >= 0 && E >= 1 && (out3 || out6), "split_bf16x3: bad args");
+  if (rows == 0) return B200MOE_OK;
+  REQUIRE(src, "split_bf16x3: null pointer");
+  return split_bf16x3(src, rows, E, out3, out6, S(stream));
+}
+
+int b200moe_sum_parts(const float* parts, int64_t G, int64_t rows, int E, float* out, void* stream) {
+  REQUIRE(G >= 1 && rows >= 0 && E >= 1, "sum_parts: bad args");
+  if (rows == 0) return B200MOE_OK;
+  REQUIRE(parts && out, "sum_parts: null pointer");
+  return sum_parts(parts, G, rows, E, out, S(stream));
 }
 
 int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,

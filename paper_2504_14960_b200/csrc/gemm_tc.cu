@@ -467,20 +467,24 @@ __device__ __forceinline__ void store_row32(void* base, bool f32, int64_t row_of
     }
   } else {
     __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + row_off + n;
+    // bf16 accumulate: C = bf16(C + bf16(acc)), matching the TMA bf16 reduce-add
+    auto term = [&](int i) {
+      return accumulate ? __bfloat162float(p[i]) + __bfloat162float(__float2bfloat16_rn(f[i])) : f[i];
+    };
     if (n + 32 <= N && (((uintptr_t)p) & 15) == 0) {
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
         uint4 v;
-        v.x = pack_bf16(f[i], f[i + 1]);
-        v.y = pack_bf16(f[i + 2], f[i + 3]);
-        v.z = pack_bf16(f[i + 4], f[i + 5]);
-        v.w = pack_bf16(f[i + 6], f[i + 7]);
+        v.x = pack_bf16(term(i), term(i + 1));
+        v.y = pack_bf16(term(i + 2), term(i + 3));
+        v.z = pack_bf16(term(i + 4), term(i + 5));
+        v.w = pack_bf16(term(i + 6), term(i + 7));
         *reinterpret_cast<uint4*>(p + i) = v;
       }
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (n + i < N) p[i] = __float2bfloat16_rn(f[i]);
+        if (n + i < N) p[i] = __float2bfloat16_rn(term(i));
     }
   }
 }
@@ -751,7 +755,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             pack32_bf16(f0, o);
             pack32_bf16(f1, o + 4);
             st_row_chunk(stgr.acquire(), r, o);
-            stgr.issue(&map_c, (int)n, crow, p.grouped_k ? tl.g : 0, false);
+            stgr.issue(&map_c, (int)n, crow, p.grouped_k ? tl.g : 0, p.accumulate);  // bf16 reduce-add
           }
         } else if (p.epi == EPI_SWIGLU_FWD) {
           uint4 hb[8];

@@ -613,8 +613,81 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int64
 }
 
 // ---------------------------------------------------------------------------
+// fp32 router GEMMs on the bf16 tensor cores: an fp32 value v is split into
+// three bf16 parts hi + mid + lo == v exactly (8 + 8 + 8 significand bits),
+// so x(bf16) . W_g = x.hi + x.mid + x.lo with exact products and fp32
+// accumulation.  Parts are laid out as column blocks of stride Ep (E rounded
+// up to 8, zero padded).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void split3(float v, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+
+// src [rows, E] fp32 -> out3 [rows, 3 Ep] = (hi | mid | lo) and/or
+// out6 [rows, 6 Ep] = (hi | hi | hi | mid | mid | lo) (the dz side of the
+// six-term product dz . W^T)
+__global__ void split_bf16x3_kernel(const float* __restrict__ src, int64_t rows, int E, int Ep,
+                                    __nv_bfloat16* __restrict__ out3, __nv_bfloat16* __restrict__ out6) {
+  const int64_t n = rows * Ep;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / Ep;
+    const int e = (int)(i % Ep);
+    __nv_bfloat16 hi, mid, lo;
+    split3(e < E ? src[r * E + e] : 0.f, hi, mid, lo);
+    if (out3) {
+      __nv_bfloat16* o = out3 + r * 3 * Ep + e;
+      o[0] = hi; o[Ep] = mid; o[2 * Ep] = lo;
+    }
+    if (out6) {
+      __nv_bfloat16* o = out6 + r * 6 * Ep + e;
+      o[0] = hi; o[Ep] = hi; o[2 * Ep] = hi; o[3 * Ep] = mid; o[4 * Ep] = mid; o[5 * Ep] = lo;
+    }
+  }
+}
+
+// out[r, e] = sum_g ((p[g, r, e] + p[g, r, Ep + e]) + p[g, r, 2 Ep + e]), g ascending
+__global__ void sum_parts_kernel(const float* __restrict__ parts, int64_t G, int64_t rows, int E, int Ep,
+                                 float* __restrict__ out) {
+  const int64_t n = rows * E;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / E;
+    const int e = (int)(i % E);
+    float s = 0.f;
+    for (int64_t g = 0; g < G; ++g) {
+      const float* p = parts + (g * rows + r) * 3 * Ep + e;
+      s += (p[0] + p[Ep]) + p[2 * Ep];
+    }
+    out[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+int split_bf16x3(const float* src, int64_t rows, int E, void* out3, void* out6, cudaStream_t st) {
+  const int Ep = (E + 7) / 8 * 8;
+  const int64_t n = rows * Ep;
+  if (n == 0) return B200MOE_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 16);
+  split_bf16x3_kernel<<<grid, 256, 0, st>>>(src, rows, E, Ep, static_cast<__nv_bfloat16*>(out3),
+                                            static_cast<__nv_bfloat16*>(out6));
+  B200MOE_CHECK_LAUNCH("split_bf16x3");
+  return B200MOE_OK;
+}
+
+int sum_parts(const float* parts, int64_t G, int64_t rows, int E, float* out, cudaStream_t st) {
+  const int Ep = (E + 7) / 8 * 8;
+  const int64_t n = rows * E;
+  if (n == 0) return B200MOE_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 16);
+  sum_parts_kernel<<<grid, 256, 0, st>>>(parts, G, rows, E, Ep, out);
+  B200MOE_CHECK_LAUNCH("sum_parts");
+  return B200MOE_OK;
+}
+
 int router_logits(const void* x, int dt, const float* wg, int64_t Tn, int64_t H, int E,
                   float* out, cudaStream_t st) {
   if (dt == B200MOE_BF16)

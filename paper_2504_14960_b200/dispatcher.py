@@ -311,6 +311,11 @@ class RankLayer:
         self.pk = weights.packed(dtype, device)
         self.wg = params.device_w_g(device)
         self.wgT = params.device_w_gT(device)
+        # bf16 tokens: the three router GEMMs on the tensor cores against the
+        # exact bf16 parts of W_g (B200MOE_ROUTER_TC=0: CUDA-core kernels)
+        self.wg_parts = None
+        if dtype == torch.bfloat16 and os.environ.get("B200MOE_ROUTER_TC", "1") != "0":
+            self.wg_parts = params.device_w_g_parts(device)
         self.single = len(groups.ep) == 1 and len(groups.etp) == 1
         # EP exchange: device-side over NVLink peer memory (bf16, ETP = 1), or
         # NCCL all_to_all_single (B200MOE_EP_EXCHANGE=nccl, fp32, ETP > 1)
@@ -355,7 +360,7 @@ class RankLayer:
         x = x.to(self.device, self.dtype).contiguous()
         if self.check:
             check_finite(x, "token block")
-        logits = K.router_logits(x, self.wg)
+        logits = K.router_logits(x, self.wg, parts=self.wg_parts)
         dec = routing_from_logits(logits, p, positions)
         return self.forward_routed(ctx, x, dec, logits)
 
@@ -659,13 +664,14 @@ class RankLayer:
         dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
                           p.renormalize_topk)
         dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
-        if E <= 8:  # router term fused into the combine (w_g^T chunks reused per warp)
+        if self.wg_parts is None and E <= 8:
+            # router term fused into the combine (w_g^T chunks reused per warp)
             dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT, out=dx_sh,
                            accumulate=dx_sh is not None)
         else:
             dx = K.combine(rows, sv["pair_row"], T, gates=None, out=dx_sh, accumulate=dx_sh is not None)
-            K.router_term(dz, self.wg, dx)
-        dwg = K.router_wgrad(x, dz)
+            K.router_term(dz, self.wg, dx, parts=self.wg_parts)
+        dwg = K.router_wgrad(x, dz, tc=self.wg_parts is not None)
         return dx, dwg, dw1p, dw2p
 
 

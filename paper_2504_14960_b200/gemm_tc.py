@@ -74,7 +74,7 @@ _EPI_NAMES = {EPI_STORE: "store", EPI_SWIGLU_FWD: "swiglu_fwd", EPI_SWIGLU_BWD: 
               EPI_ACT_FWD: "act_fwd", EPI_ACT_BWD: "act_bwd", EPI_SCATTER: "scatter"}
 
 
-def _run(args: TcGemmArgs) -> None:
+def _run(args: TcGemmArgs, tag: str = "gemm_tc") -> None:
     lib = _lib()
     prof = L.PROFILE
     e0 = prof.begin() if prof.on else None
@@ -82,11 +82,12 @@ def _run(args: TcGemmArgs) -> None:
     L.note_launches(1)
     if e0 is not None:
         kind = "wgrad" if args.grouped_dim == 1 else _EPI_NAMES[args.epilogue]
-        prof.end(f"gemm_tc[{kind} N={args.N} K={args.K} M={args.M}]", e0)
+        prof.end(f"{tag}[{kind} N={args.N} K={args.K} M={args.M}]", e0)
 
 
 def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg, ldc, group_off,
-         group_expert=None, max_rows=0, accumulate=False, group_end=None, scatter=None):
+         group_expert=None, max_rows=0, accumulate=False, group_end=None, scatter=None,
+         tag="gemm_tc"):
     """Same argument convention as kernels.gemm_simt.  ``scatter`` =
     (row_origin, peer_base, byte_offset): bf16 rows go to the ranks they came
     from instead of C (C may be None; ldc is the destination row length)."""
@@ -114,7 +115,7 @@ def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg
     if scatter is not None:
         a.epilogue = EPI_SCATTER
         a.row_origin, a.peer_base, a.scatter_off = L.ptr(scatter[0]), L.ptr(scatter[1]), scatter[2]
-    _run(a)
+    _run(a, tag)
     return C
 
 

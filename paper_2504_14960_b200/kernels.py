@@ -52,11 +52,52 @@ def dense_gemm(A, B, C, *, M: int, N: int, K: int, a_sm, a_sk, b_sk, b_sn, ldc, 
                      max_rows=M, accumulate=accumulate)
 
 
-def router_logits(x: torch.Tensor, w_g: torch.Tensor) -> torch.Tensor:
+def _ep(E: int) -> int:
+    return (E + 7) // 8 * 8
+
+
+def _tc_router(x: torch.Tensor, parts) -> bool:
+    """Tensor-core router GEMMs: bf16 tokens, W_g parts given, tcgen05 on."""
+    from . import gemm_tc
+
+    return parts is not None and x.dtype == torch.bfloat16 and gemm_tc.available() and x.shape[1] % 8 == 0
+
+
+def split_bf16x3(src: torch.Tensor, want3: bool = True, want6: bool = False):
+    """fp32 [rows, E] -> bf16 (hi | mid | lo) [rows, 3Ep] and/or
+    (hi | hi | hi | mid | mid | lo) [rows, 6Ep]."""
+    rows, E = src.shape
+    _cuda(src, "src", torch.float32)
+    o3 = torch.empty((rows, 3 * _ep(E)), dtype=torch.bfloat16, device=src.device) if want3 else None
+    o6 = torch.empty((rows, 6 * _ep(E)), dtype=torch.bfloat16, device=src.device) if want6 else None
+    L.call("b200moe_split_bf16x3", L.ptr(src), rows, E, L.ptr(o3), L.ptr(o6), _sp())
+    return o3, o6
+
+
+def sum_parts(parts: torch.Tensor, G: int, rows: int, E: int) -> torch.Tensor:
+    out = torch.empty((rows, E), dtype=torch.float32, device=parts.device)
+    L.call("b200moe_sum_parts", L.ptr(parts), G, rows, E, L.ptr(out), _sp())
+    return out
+
+
+def router_logits(x: torch.Tensor, w_g: torch.Tensor, parts=None) -> torch.Tensor:
+    """logits = x @ W_g (router.py:145) in fp32.  bf16 tokens with ``parts``
+    (GatingParams.device_w_g_parts): one tensor-core GEMM against the three
+    exact bf16 parts of W_g, then the parts are folded in fixed order."""
     T, H = x.shape
     E = w_g.shape[1]
     _cuda(x, "x")
     _cuda(w_g, "w_g", torch.float32)
+    if T > 0 and _tc_router(x, parts):
+        from . import gemm_tc
+
+        w3t = parts[0]
+        n3 = w3t.shape[0]
+        l3 = torch.empty((T, n3), dtype=torch.float32, device=x.device)
+        gemm_tc.gemm(x, w3t, l3, grouped_dim=0, G=1, M=0, N=n3, K=H, a_sm=H, a_sk=1, b_sg=0, b_sk=1,
+                     b_sn=H, c_sg=0, ldc=n3, group_off=_single_group(T, x.device), max_rows=T,
+                     tag="router_tc")
+        return sum_parts(l3, 1, T, E)
     out = torch.empty((T, E), dtype=torch.float32, device=x.device)
     if E > 8 and T > 0:
         # tiled fp32 GEMM (64x64 tiles) instead of the per-token warp kernel
@@ -66,14 +107,39 @@ def router_logits(x: torch.Tensor, w_g: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def router_term(dz: torch.Tensor, w_g: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
-    """out += dz @ w_g^T  (dispatcher.py:490) as a tiled GEMM."""
+def router_term(dz: torch.Tensor, w_g: torch.Tensor, out: torch.Tensor, parts=None) -> torch.Tensor:
+    """out += dz @ w_g^T  (dispatcher.py:490).  bf16 ``out`` with ``parts``:
+    one tensor-core GEMM over K = 6Ep (the six significant part products of
+    dz and W_g), reduce-added into out; otherwise a tiled fp32 GEMM."""
     T, E = dz.shape
     H = w_g.shape[0]
     if T == 0:
         return out
+    if _tc_router(out, parts):
+        from . import gemm_tc
+
+        _, dz6 = split_bf16x3(dz, want3=False, want6=True)
+        w6 = parts[1]
+        k6 = w6.shape[1]
+        return gemm_tc.gemm(dz6, w6, out, grouped_dim=0, G=1, M=0, N=H, K=k6, a_sm=k6, a_sk=1, b_sg=0,
+                            b_sk=1, b_sn=k6, c_sg=0, ldc=H, group_off=_single_group(T, dz.device),
+                            max_rows=T, accumulate=True, tag="router_tc")
     return dense_gemm(dz, w_g, out, M=T, N=H, K=E, a_sm=E, a_sk=1, b_sk=1, b_sn=E, ldc=H,
                       accumulate=True)
+
+
+_SPLITK_CACHE = {}
+
+
+def _splitk_groups(T: int, device, parts: int = 8) -> Tuple[torch.Tensor, int]:
+    """Token-chunk offsets (multiples of 64, last = T) for a split-K GEMM."""
+    key = (T, str(device), parts)
+    if key not in _SPLITK_CACHE:
+        c = max(64, ((T + parts - 1) // parts + 63) // 64 * 64)
+        offs = list(range(0, T, c)) + [T]
+        t = torch.tensor(offs, dtype=torch.int32).pin_memory().to(device, non_blocking=True)
+        _SPLITK_CACHE[key] = (t, len(offs) - 1)
+    return _SPLITK_CACHE[key]
 
 
 def router_topk(logits: torch.Tensor, k: int, gate_fn: int, renorm: bool, want_f64: bool = False):
@@ -186,9 +252,23 @@ def router_bwd(dgates, scores, topk_idx, gates, gate_fn: int, renorm: bool) -> t
     return dz
 
 
-def router_wgrad(x: torch.Tensor, dz: torch.Tensor) -> torch.Tensor:
+def router_wgrad(x: torch.Tensor, dz: torch.Tensor, tc: bool = False) -> torch.Tensor:
+    """dW_g = x^T dz (dispatcher.py:489).  ``tc`` (bf16 x): one split-K
+    tensor-core GEMM against dz's three exact bf16 parts, folded in fixed
+    order; otherwise the deterministic split-K CUDA-core kernels."""
     T, H = x.shape
     E = dz.shape[1]
+    if tc and T > 0 and _tc_router(x, ()):
+        from . import gemm_tc
+
+        dz3, _ = split_bf16x3(dz)
+        n3 = dz3.shape[1]
+        goff, G = _splitk_groups(T, x.device)
+        part = torch.empty((G, H, n3), dtype=torch.float32, device=x.device)
+        gemm_tc.gemm(x, dz3, part, grouped_dim=1, G=G, M=H, N=n3, K=0, a_sm=1, a_sk=H, b_sg=0,
+                     b_sk=n3, b_sn=1, c_sg=H * n3, ldc=n3, group_off=goff, max_rows=T,
+                     tag="router_tc")
+        return sum_parts(part, G, H, E)
     dwg = torch.empty((H, E), dtype=torch.float32, device=x.device)
     ws_bytes = int(L.load().b200moe_router_wgrad_ws(T, H, E))
     ws = torch.empty((max(ws_bytes // 4, 1),), dtype=torch.float32, device=x.device)

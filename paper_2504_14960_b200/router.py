@@ -97,6 +97,29 @@ class GatingParams:
             self._dev_cache[key] = self.device_w_g(device).T.contiguous()
         return self._dev_cache[key]
 
+    def device_w_g_parts(self, device=None):
+        """W_g as three bf16 parts hi + mid + lo (== W_g exactly) for the
+        tensor-core router GEMMs (kernels.router_logits/router_term), cached:
+        (w3t [3Ep, H]: rows (part, e), the B operand of x . W_g;
+         w6 [H, 6Ep]: column blocks (hi, mid, lo, hi, mid, hi), the B operand
+         of dz . W_g^T against dz's (hi, hi, hi, mid, mid, lo))."""
+        device = torch.device(device or _device_default())
+        key = ("wg_parts", str(device))
+        if key not in self._dev_cache:
+            w = self.device_w_g(device)
+            H, E = w.shape
+            Ep = (E + 7) // 8 * 8
+            hi = w.to(torch.bfloat16)
+            r = w - hi.float()
+            mid = r.to(torch.bfloat16)
+            lo = (r - mid.float()).to(torch.bfloat16)
+            pad = lambda t: torch.nn.functional.pad(t, (0, Ep - E))  # noqa: E731
+            hi, mid, lo = pad(hi), pad(mid), pad(lo)
+            w3t = torch.cat([hi, mid, lo], dim=1).T.contiguous()
+            w6 = torch.cat([hi, mid, lo, hi, mid, hi], dim=1).contiguous()
+            self._dev_cache[key] = (w3t, w6)
+        return self._dev_cache[key]
+
 
 @dataclass
 class RoutingDecision:
