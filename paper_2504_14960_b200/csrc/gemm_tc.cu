@@ -60,7 +60,8 @@ struct Params {
   int64_t ldpre;
   int panel_m;     // raster panel height in m-tiles
   int tile_m;      // rows per tile: 128 (1 CTA) or 256 (CTA pair)
-  int debug_nostore;  // perf experiments only: 1 = no epilogue global traffic, 2 = no bulk stores
+  int debug_nostore;  // perf experiments only: 1 = no epilogue global traffic, 2 = no bulk
+                      // stores, 3 = SwiGLU backward without its pre loads
   int use_tma;        // output tensor maps are valid (TMA-store epilogue)
   // EPI_SCATTER: row r -> peer_base[origin[2r]] + scatter_off + origin[2r+1] * ldc * 2
   const int32_t* origin;
@@ -411,7 +412,9 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
 }
 
 // ------------------------------------------------------------- epilogues
-__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+// fast divide (MUFU.RCP): exact limits at +-inf, ~2 ulp, far below bf16 rounding
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.f + __expf(-g)); }
+__device__ __forceinline__ float sigmoid_f(float g) { return __fdividef(1.f, 1.f + __expf(-g)); }
 __device__ __forceinline__ float gelu_tc(float x) {
   const float c = 0.7978845608028654f;
   return 0.5f * x * (1.f + tanhf(c * (x + 0.044715f * x * x * x)));
@@ -522,6 +525,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tfull_bar = bars + 16 * S, tempty_bar = tfull_bar + 16;
   const uint32_t ld_bar = tfull_bar + 32;  // epilogue TMA loads into the staging ring
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + bars_off + 16 * S + 32 + 8 * C::NSTG + 8);
+  const uint32_t ld_empty = ld_bar + 8 * C::NSTG + 16;  // staging slot handed back by the epilogue
   int32_t* prefix = reinterpret_cast<int32_t*>(gbase + bars_off + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -548,7 +552,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(tfull_bar + 8 * i, 1);
       mbar_init(tempty_bar + 8 * i, 4 * CG);  // epilogue warps of both CTAs
     }
-    for (int i = 0; i < C::NSTG; ++i) mbar_init(ld_bar + 8 * i, 1);
+    for (int i = 0; i < C::NSTG; ++i) {
+      mbar_init(ld_bar + 8 * i, 1);
+      mbar_init(ld_empty + 8 * i, 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -653,12 +660,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ epilogue input
+    // SwiGLU backward reads the saved pre-activations: this lane streams the
+    // 64-column pre chunks of each tile into the staging ring ahead of the
+    // epilogue (same tile/chunk sequence), so their DRAM latency overlaps the
+    // mainloop instead of stalling the epilogue.
+    if (lane == 0 && p.epi == EPI_SWIGLU_BWD && p.use_tma && p.debug_nostore != 1 && p.debug_nostore != 3) {
+      prefetch_map(&map_h);
+      uint32_t ctr = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const Tile tl = decode(p, prefix, t);
+        const int64_t row0 = tl.m0 + BM * (int64_t)crank;
+        if (!(row0 + BM <= tl.m_end)) continue;  // not the epilogue's TMA path
+        for (int c = 0; c < BN / 32 && tl.n0 + c * 32 < p.N; ++c, ++ctr) {
+          const uint32_t sl = ctr % C::NSTG, ph = (ctr / C::NSTG) & 1u;
+          mbar_wait(ld_empty + 8 * sl, ph ^ 1u);
+          mbar_expect_tx(ld_bar + 8 * sl, STG_BYTES);
+          tma_load_3d(&map_h, stg + sl * STG_BYTES, ld_bar + 8 * sl, (int)(((tl.n0 + c * 32) / 32) * 64),
+                      (int)row0, 0);
+        }
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
     const int row_in_tile = BM * (int)crank + 32 * q + lane;
     Stager<C::NSTG> stgr{stg, 0, threadIdx.x == 128, p.debug_nostore == 2};
-    uint32_t ld_par = 0;  // phase bits of the staging-ring load barriers
+    uint32_t bwd_ctr = 0;  // SwiGLU-backward staging chunks consumed (matches warp 3)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < total; t += ncl) {
@@ -803,31 +832,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         } else {  // EPI_SWIGLU_BWD: acc = dh over F columns; pre/dpre [.., 2F] interleaved
           // The matching 64-column pre chunk (32 gate | 32 up, 128 B per row)
-          // is TMA-loaded into the staging tile, transformed in place into
-          // d[gate|up] and TMA-stored: pre and dpre share the layout.  The
-          // load of chunk c+1 is issued before chunk c is processed.
+          // arrives in the staging ring from warp 3, is transformed in place
+          // into d[gate|up] and TMA-stored: pre and dpre share the layout.
+          // The slot goes back to warp 3 once its store has read it (checked
+          // one chunk later, so the epilogue never waits on its own store).
           int nch = 0;
           while (nch < BN / 32 && tl.n0 + nch * 32 < p.N) ++nch;
-          auto load_pre = [&](int c, uint32_t ctr, bool prologue) {
-            if (threadIdx.x == 128) {
-              if (prologue) bulk_wait_read<C::NSTG - 1>();
-              else bulk_wait_read<C::NSTG - 2>();
-              const uint32_t sl = ctr % C::NSTG;
-              mbar_expect_tx(ld_bar + 8 * sl, STG_BYTES);
-              tma_load_3d(&map_h, stg + sl * STG_BYTES, ld_bar + 8 * sl,
-                          (int)(((tl.n0 + c * 32) / 32) * 64), crow, 0);
-            }
-          };
-          if (nch > 0) load_pre(0, (uint32_t)stgr.buf, true);
 #pragma unroll 1
           for (int c = 0; c < nch; ++c) {
-            const uint32_t ctr = (uint32_t)stgr.buf;
-            if (c + 1 < nch) load_pre(c + 1, ctr + 1, false);
+            const uint32_t ctr = bwd_ctr++;
+            const uint32_t sl = ctr % C::NSTG;
             uint32_t v[32];
             tmem_ld32(t_row + c * 32, v);
-            const uint32_t sl = ctr % C::NSTG;
-            mbar_wait(ld_bar + 8 * sl, (ld_par >> sl) & 1u);
-            ld_par ^= 1u << sl;
+            if (p.debug_nostore != 3) mbar_wait(ld_bar + 8 * sl, (ctr / C::NSTG) & 1u);
             const uint32_t rowp = stg + sl * STG_BYTES + (uint32_t)r * 128;
             uint4 o[8];
 #pragma unroll
@@ -847,14 +864,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float d = __uint_as_float(v[i]);
-              const float s = 1.f / (1.f + __expf(-g[i]));
+              const float s = sigmoid_f(g[i]);
               dg[i] = d * u[i] * s * (1.f + g[i] * (1.f - s));
               du[i] = d * g[i] * s;
             }
             pack32_bf16(dg, o);
             pack32_bf16(du, o + 4);
             st_row_chunk(stg + sl * STG_BYTES, r, o);
-            stgr.issue(&map_c, (int)(((tl.n0 + c * 32) / 32) * 64), crow, 0, false);
+            fence_async_smem();
+            epi_bar();
+            if (threadIdx.x == 128) {
+              if (p.debug_nostore != 2) {
+                tma_store_3d(&map_c, stg + sl * STG_BYTES, (int)(((tl.n0 + c * 32) / 32) * 64), crow, 0);
+                bulk_commit();
+              }
+              bulk_wait_read<1>();  // the previous chunk's store has read its slot
+              if (ctr > 0) mbar_arrive(ld_empty + 8 * ((ctr - 1) % C::NSTG));
+            }
           }
         }
       } else if (p.epi == EPI_STORE) {
@@ -905,7 +931,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float d = __uint_as_float(v[i]);
-            const float s = 1.f / (1.f + __expf(-g[i]));
+            const float s = sigmoid_f(g[i]);
             dg[i] = d * u[i] * s * (1.f + g[i] * (1.f - s));
             du[i] = d * g[i] * s;
           }
@@ -1129,7 +1155,7 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.scatter_off = a->scatter_off;
   p.tile_m = BM * cg;
   const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
-  p.debug_nostore = (ns && (ns[0] == '1' || ns[0] == '2')) ? ns[0] - '0' : 0;
+  p.debug_nostore = (ns && ns[0] >= '1' && ns[0] <= '3') ? ns[0] - '0' : 0;
   p.panel_m = choose_panel(a, p.tile_m);
 
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
