@@ -225,6 +225,11 @@ typedef struct {
    * are skipped.  Replaces the return all_to_all_v of dispatcher.py:355-361
    * (and :462-466 backward), overlapped with the GEMM. */
   const int32_t* row_origin; const uint64_t* peer_base; int64_t scatter_off;
+  /* glu_f > 0 (grouped K, fp32 store, M = 2 glu_f): the M rows are packed
+   * SwiGLU rows ([32 gate | 32 up] per 64) and are stored de-interleaved as
+   * [gate rows | up rows], i.e. C_g^T is the reference's [H, 2F] = [gate | up]
+   * dW1 layout (experts.py:168) without a copy. */
+  int64_t glu_f;
 } b200moe_tc_gemm_args;
 
 B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);

@@ -67,7 +67,16 @@ struct Params {
   const int32_t* origin;
   const uint64_t* peer_base;
   int64_t scatter_off;
+  // grouped-K weight gradient of the SwiGLU W1: output rows are packed rows
+  // ([32 gate | 32 up] per 64) and are stored de-interleaved ([gate | up])
+  int64_t glu_f;
 };
+
+// packed SwiGLU row -> [gate | up] row (rows come in 32-row halves)
+__device__ __forceinline__ int64_t glu_row(int64_t m, int64_t F) {
+  const int64_t b = m >> 6, w = m & 63;
+  return w < 32 ? b * 32 + w : F + b * 32 + (w - 32);
+}
 
 // Per-CTA-group configuration.  CG = 2: a CTA pair (cluster of 2 on one TPC)
 // computes a 256 x 256 tile with tcgen05.mma.cta_group::2; each CTA stages
@@ -231,6 +240,24 @@ struct Stager {
       const uint32_t src = base + buf * STG_BYTES;
       if (reduce) tma_reduce_add_3d(map, src, c0, c1, c2);
       else tma_store_3d(map, src, c0, c1, c2);
+      bulk_commit();
+    }
+    buf = (buf + 1) % NSTG;
+  }
+  // the staged 128 rows as four 32-row sub-tiles to rows glu_row(row0 + 32 i)
+  // (map box: 32 rows)
+  __device__ __forceinline__ void issue_glu(const CUtensorMap* map, int c0, int64_t row0, int c2, bool reduce,
+                                            int64_t F) {
+    fence_async_smem();
+    epi_bar();
+    if (leader && !skip) {
+      const uint32_t src = base + buf * STG_BYTES;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int dr = (int)glu_row(row0 + 32 * i, F);
+        if (reduce) tma_reduce_add_3d(map, src + i * 4096, c0, dr, c2);
+        else tma_store_3d(map, src + i * 4096, c0, dr, c2);
+      }
       bulk_commit();
     }
     buf = (buf + 1) % NSTG;
@@ -764,7 +791,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint4 o[8];
             pack32_f32(f, o);
             st_row_chunk(stgr.acquire(), r, o);
-            stgr.issue(&map_c, (int)n, crow, p.grouped_k ? tl.g : 0, p.accumulate);
+            if (p.glu_f)
+              stgr.issue_glu(&map_h, (int)n, row0, tl.g, p.accumulate, p.glu_f);
+            else
+              stgr.issue(&map_c, (int)n, crow, p.grouped_k ? tl.g : 0, p.accumulate);
           }
         } else if (p.epi == EPI_STORE) {
 #pragma unroll 1
@@ -892,7 +922,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = zero ? 0.f : __uint_as_float(v[i]);
           const int64_t n = tl.n0 + c * 32;
-          if (live && n < p.N) store_row32(p.C, p.out_f32, c_off + row * p.ldc, n, p.N, f, p.accumulate);
+          const int64_t drow = p.glu_f ? glu_row(row, p.glu_f) : row;
+          if (live && n < p.N) store_row32(p.C, p.out_f32, c_off + drow * p.ldc, n, p.N, f, p.accumulate);
         }
       } else if (p.epi == EPI_SWIGLU_FWD) {
         // columns: 4 blocks of [32 gate | 32 up]; h column = (n0 + 64 b)/2 + i
@@ -1071,6 +1102,11 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
     set_error("gemm_tc: leading dimensions must be multiples of 8 elements (16 B)");
     return B200MOE_EUNSUPPORTED;
   }
+  if (a->glu_f && (a->grouped_dim != 1 || a->epilogue != EPI_STORE || a->out_dtype != B200MOE_F32 ||
+                   a->M != 2 * a->glu_f || (a->glu_f % 32))) {
+    set_error("gemm_tc: glu_f needs a grouped-K fp32 store with M == 2 * glu_f, glu_f %% 32 == 0");
+    return B200MOE_EUNSUPPORTED;
+  }
   if (a->epilogue == EPI_SCATTER &&
       (a->grouped_dim != 0 || a->out_dtype != B200MOE_BF16 || !a->row_origin || !a->peer_base ||
        (a->ldc % 8) || (a->N % 8))) {
@@ -1119,6 +1155,8 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
       rc = make_map(&mh, a->H, (uint64_t)a->N / 2, R, 1, (uint64_t)a->ldh, (uint64_t)a->ldh * R, BM);
     else if (rc == B200MOE_OK && a->epilogue == 2)  // pre [R, 2F], read by the epilogue
       rc = make_map(&mh, a->PRE, 2 * (uint64_t)a->N, R, 1, (uint64_t)a->ldpre, (uint64_t)a->ldpre * R, BM);
+    else if (rc == B200MOE_OK && a->glu_f)  // C again, 32-row boxes for the de-interleaving store
+      rc = make_map(&mh, a->C, ccols, crows, cg_n, (uint64_t)a->ldc, csg, 32, of32);
     else
       mh = mc;
     use_tma = rc == B200MOE_OK && (a->ldc % 8 == 0) && (a->epilogue != 1 || a->ldh % 8 == 0) &&
@@ -1153,6 +1191,7 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   p.origin = a->row_origin;
   p.peer_base = a->peer_base;
   p.scatter_off = a->scatter_off;
+  p.glu_f = a->glu_f;
   p.tile_m = BM * cg;
   const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
   p.debug_nostore = (ns && ns[0] >= '1' && ns[0] <= '3') ? ns[0] - '0' : 0;

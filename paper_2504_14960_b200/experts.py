@@ -48,16 +48,6 @@ def swiglu_interleave_cols(w1: torch.Tensor) -> torch.Tensor:
     return torch.stack([g, u], dim=1).reshape(F2, H)
 
 
-def swiglu_deinterleave_rows(p: torch.Tensor) -> torch.Tensor:
-    """Inverse of swiglu_interleave_cols: [2F, H] -> [H, 2F] = [gate | up]."""
-    F2, H = p.shape
-    F = F2 // 2
-    b = p.reshape(F // 32, 2, 32, H)
-    g = b[:, 0].reshape(F, H)
-    u = b[:, 1].reshape(F, H)
-    return torch.cat([g, u], dim=0).T
-
-
 def swiglu_deinterleave_cols_rows(pre: torch.Tensor) -> torch.Tensor:
     """Padded-layout activations [R, 2F] interleaved -> [R, 2F] = [gate | up]."""
     R, F2 = pre.shape
@@ -105,9 +95,8 @@ def pack_experts(w1: Sequence, w2: Sequence, act: str, dtype, device) -> PackedE
 
 
 def unpack_w1_grad(dw1p: torch.Tensor, act: str) -> List[torch.Tensor]:
-    """[L, N1, H] device grads -> list of reference-layout [H, N1']."""
-    if act == ACT_SWIGLU:
-        return [swiglu_deinterleave_rows(g) for g in dw1p]
+    """[L, N1, H] device grads (SwiGLU rows already [gate | up], see
+    ffn_backward) -> list of reference-layout [H, N1] views (no copy)."""
     return [g.T for g in dw1p]
 
 
@@ -274,7 +263,9 @@ def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torc
                  max_rows: int, want_dx: bool = True, gend: Optional[torch.Tensor] = None,
                  dx_scatter=None):
     """experts.py:146-172 batched over groups: returns (dxp, dw1p, dw2p) with
-    dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert).
+    dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert);
+    dw1p[g] is [N1, H] with SwiGLU rows in [gate | up] order, so dw1p[g].T is
+    the reference layout.
     ``dx_scatter``: as ffn_forward's y_scatter, for the input gradient."""
     from . import gemm_tc
 
@@ -306,8 +297,17 @@ def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torc
     _gemm(dyp, h, dw2p, grouped_dim=1, G=G, M=H, N=F, K=0, a_sm=1, a_sk=H, b_sg=0, b_sk=F,
           b_sn=1, c_sg=H * F, ldc=F, group_off=goff, max_rows=max_rows, group_end=gend)
     dw1p = torch.empty((G, N1, H), dtype=torch.float32, device=dev)
-    _gemm(dpre, xp, dw1p, grouped_dim=1, G=G, M=N1, N=H, K=0, a_sm=1, a_sk=N1, b_sg=0, b_sk=H,
-          b_sn=1, c_sg=N1 * H, ldc=H, group_off=goff, max_rows=max_rows, group_end=gend)
+    kw = dict(grouped_dim=1, G=G, M=N1, N=H, K=0, a_sm=1, a_sk=N1, b_sg=0, b_sk=H, b_sn=1,
+              c_sg=N1 * H, ldc=H, group_off=goff, max_rows=max_rows, group_end=gend)
+    glu = pk.act == "swiglu"
+    if glu and dt == torch.bfloat16 and gemm_tc.available() and gemm_tc.supports(**kw):
+        # the epilogue stores the packed SwiGLU rows de-interleaved ([gate | up])
+        gemm_tc.gemm(dpre, xp, dw1p, glu_f=F, **kw)
+    else:
+        _gemm(dpre, xp, dw1p, **kw)
+        if glu:
+            b = dw1p.view(G, F // 32, 2, 32, H)
+            dw1p = torch.cat([b[:, :, 0].reshape(G, F, H), b[:, :, 1].reshape(G, F, H)], dim=1)
     return dxp, dw1p, dw2p
 
 

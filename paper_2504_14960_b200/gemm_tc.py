@@ -30,7 +30,7 @@ class TcGemmArgs(ctypes.Structure):
         ("group_off", P), ("group_expert", P),
         ("epilogue", I32), ("act", I32), ("H", P), ("ldh", I64), ("PRE", P), ("ldpre", I64),
         ("num_ctas", I32), ("group_end", P),
-        ("row_origin", P), ("peer_base", P), ("scatter_off", I64),
+        ("row_origin", P), ("peer_base", P), ("scatter_off", I64), ("glu_f", I64),
     ]
 
 
@@ -87,7 +87,7 @@ def _run(args: TcGemmArgs, tag: str = "gemm_tc") -> None:
 
 def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg, ldc, group_off,
          group_expert=None, max_rows=0, accumulate=False, group_end=None, scatter=None,
-         tag="gemm_tc"):
+         tag="gemm_tc", glu_f=0):
     """Same argument convention as kernels.gemm_simt.  ``scatter`` =
     (row_origin, peer_base, byte_offset): bf16 rows go to the ranks they came
     from instead of C (C may be None; ldc is the destination row length)."""
@@ -112,6 +112,7 @@ def gemm(A, B, C, *, grouped_dim, G, M, N, K, a_sm, a_sk, b_sg, b_sk, b_sn, c_sg
     a.group_off, a.group_expert = L.ptr(group_off), L.ptr(group_expert)
     a.group_end = L.ptr(group_end)
     a.epilogue = EPI_STORE
+    a.glu_f = glu_f
     if scatter is not None:
         a.epilogue = EPI_SCATTER
         a.row_origin, a.peer_base, a.scatter_off = L.ptr(scatter[0]), L.ptr(scatter[1]), scatter[2]
