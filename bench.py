@@ -18,7 +18,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -61,57 +60,69 @@ def parse():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock, power and throttle reasons polled through NVML every 10 ms
+    from a thread while the timed region runs (nvidia-smi as a fallback)."""
+
+    # NVML clocks-event reason bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.rows = []  # (t, sm_mhz, max_mhz, power_w, reason_bits)
         self.window = None  # (t0, t1) wall-clock of the timed region
+        self.stop_ev = threading.Event()
+        self.err = None
 
     def mark(self, t0, t1):
         self.window = (t0, t1)
 
-    def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+    def _handle(self, nv):
+        import torch
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append([time.time()] + parts)
+        try:
+            prop = torch.cuda.get_device_properties(self.index)
+            bus = f"{prop.pci_domain_id:08x}:{prop.pci_bus_id:02x}:{prop.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:  # noqa: BLE001
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = self._handle(nv)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self.stop_ev.is_set():
+                self.rows.append((time.time(), nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
+                                  nv.nvmlDeviceGetPowerUsage(h) / 1000.0, int(get_reasons(h))))
+                time.sleep(0.01)
+        except Exception as exc:  # noqa: BLE001
+            self.err = f"nvml unavailable: {exc}"
+
+    def start(self):
+        self.thread = threading.Thread(target=self._poll, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:  # noqa: BLE001
-            self.proc.kill()
+        self.stop_ev.set()
+        self.thread.join(timeout=5)
         rows = self.rows
         if self.window is not None:
-            inside = [r for r in rows if self.window[0] - 0.25 <= r[0] <= self.window[1] + 0.25]
-            rows = inside or rows
-        rows = [r[1:] for r in rows]
-        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
-        mx = max((float(r[1]) for r in rows if r[1].replace(".", "").isdigit()), default=None)
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
-        med = sm[len(sm) // 2] if sm else None
-        pw = sorted(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm),
-                "power_w_median": pw[len(pw) // 2] if pw else None}
+            rows = [r for r in rows if self.window[0] <= r[0] <= self.window[1]] or rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"]}
+        sm = sorted(r[1] for r in rows)
+        pw = sorted(r[3] for r in rows)
+        bits = 0
+        for r in rows:
+            bits |= r[4]
+        reasons = sorted(name for bit, name in self.REASONS.items() if bits & bit)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][2], "reasons": reasons,
+                "samples": len(rows), "sm_mhz_min": sm[0], "power_w_median": pw[len(pw) // 2]}
 
 
 def peaks():
@@ -298,7 +309,7 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(1.0)  # let nvidia-smi start sampling before the timed region
+    time.sleep(0.2)  # let the NVML poller start before the timed region
     _lib.reset_launch_count()
     total_ms = 0.0
     # every launch of the timed steps is bracketed by CUDA events on the
