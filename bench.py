@@ -125,6 +125,19 @@ class ClockSampler:
                 "samples": len(rows), "sm_mhz_min": sm[0], "power_w_median": pw[len(pw) // 2]}
 
 
+def traffic(config: str):
+    """DRAM bytes per step of the expert GEMMs from the committed ncu --set
+    full capture (profiles/traffic.json), or None for configs not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f).get(config)
+        return None if d is None else {"dram_bytes_per_step": d["gemm_tc_dram_bytes_per_step"],
+                                       "algorithmic_bytes_per_step": d["gemm_tc_algorithmic_bytes_per_step"],
+                                       "source": d["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -383,15 +396,28 @@ def main():
     # pair costs 18*H*F flop fwd+bwd with SwiGLU (6PHF + 12PHF),
     # shared expert 18*T*H*Fs; per-GPU share of the whole job
     kept = torch.tensor([float(sv_last["plan"].counts.sum())], device=dev)
+    # rows this rank's expert GEMMs processed (pairs routed to its experts)
+    if sv_last.get("pst") is not None:
+        local_pairs = float(sv_last["pst"]["gcount"].sum())
+    elif sv_last.get("xpl") is not None:
+        local_pairs = float(sv_last["xpl"].recv_counts.sum())
+    else:
+        local_pairs = float(kept)
+    gemm_ms = sum(ms_ for _, ms_ in per_launch)
+    per_rank = None
     if world > 1:
         dist.all_reduce(kept)
-    P = float(kept) / world
+        g = torch.tensor([local_pairs, gemm_ms], dtype=torch.float64, device=dev)
+        allg = [torch.empty_like(g) for _ in range(world)]
+        dist.all_gather(allg, g)
+        per_rank = {"expert_rows": [int(v[0]) for v in allg],
+                    "gemm_ms": [round(float(v[1]), 3) for v in allg]}
+    P = local_pairs
     flops_step = 18.0 * P * H * F + 18.0 * T * H * c["shared"]
-    gemm_ms = sum(ms_ for _, ms_ in per_launch)
     achieved = flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     roof = {"bound": "tensor", "kernel": "gemm_tc (grouped SwiGLU FFN, 6 launches/step)",
             "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
-            "frac": achieved / sustained if achieved else None, "traffic": None,
+            "frac": achieved / sustained if achieved else None, "traffic": traffic(a.config),
             "peak_kind": f"{src} sustained bf16 (burst {burst})",
             "algorithmic_flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
             "gemm_share_of_step": gemm_ms / ms if ms else None,
@@ -401,7 +427,10 @@ def main():
             "launch_gaps_ms": span_ms - sum(m for _, m in all_launches),
             # the cross-GPU barriers in step order (time = wait for the slowest peer)
             "ep_barrier_ms": [round(m, 4) for n, m in all_launches if n == "ep_barrier"],
-            "layer_frac_of_peak": value / world * flops_step / T / 1e12 / sustained}
+            "per_rank": per_rank,
+            # whole layer: job tokens/s x average flop per token vs the per-GPU peak
+            "layer_frac_of_peak": value / world * (18.0 * float(kept) / world * H * F / T
+                                                   + 18.0 * H * c["shared"]) / 1e12 / sustained}
 
     # ---- e2e through the public API with host (pinned) buffers
     e2e = None
