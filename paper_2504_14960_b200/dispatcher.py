@@ -371,7 +371,8 @@ class RankLayer:
         # ---- capacity (router.py:171-269) ----
         if not p.dropless:
             if p.drop_mode == DROP_FULLSEQUENCE:
-                _, dec = gather_full_sequence_decision(ctx, self.g.seq, dec, self.seq_len, E, p)
+                _, dec = gather_full_sequence_decision(ctx, self.g.seq, dec, self.seq_len, E, p,
+                                                      check=self.check)
             else:
                 dec.kept = kept_mask(dec, T, E, p).bool()
         kept_in = None if p.dropless else dec.kept.to(torch.uint8).contiguous()

@@ -201,18 +201,22 @@ def _monotone(positions: torch.Tensor) -> bool:
 
 
 def kept_mask(decision: RoutingDecision, l_scope: int, num_experts: int,
-              params: GatingParams) -> torch.Tensor:
-    """Capacity drop flags as a uint8 [n,k] device tensor (router.py:171-206)."""
+              params: GatingParams, cap: Optional[int] = None,
+              sorted_positions: bool = False) -> torch.Tensor:
+    """Capacity drop flags as a uint8 [n,k] device tensor (router.py:171-206).
+    ``cap`` overrides capacity_limit(l_scope, num_experts) (virtual experts);
+    ``sorted_positions`` skips the host monotonicity check."""
     dev = decision.experts.device
     n, k = decision.experts.shape
     kept_in = decision.kept.to(torch.uint8).contiguous()
     if params.dropless:
         return kept_in
-    cap = capacity_limit(params.capacity_factor, l_scope, num_experts)
+    if cap is None:
+        cap = capacity_limit(params.capacity_factor, l_scope, num_experts)
     idx = decision.experts.contiguous()
     if params.drop_priority == PRIORITY_POSITION:
         order = None
-        if not _monotone(decision.positions):
+        if not sorted_positions and not _monotone(decision.positions):
             order = torch.argsort(decision.positions.cpu(), stable=True).to(torch.int32).to(dev)
         plan = K.dispatch_plan(idx, decision.gates, num_experts, cap=cap, kept_in=kept_in,
                                order=order, want_perm_gates=False)
@@ -238,16 +242,21 @@ def apply_capacity(decision: RoutingDecision, l_scope: int, num_experts: int,
 
 
 def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: int,
-                                  num_experts: int, params: GatingParams
+                                  num_experts: int, params: GatingParams, check: bool = True
                                   ) -> Tuple[RoutingDecision, RoutingDecision]:
     """Capacity per full sequence across the ranks sharding it (router.py:209-269).
 
     The (position, slot, expert, gate) pairs of the group are all-gathered on
-    the device, capacity is applied per sequence with the K1 kernels, and the
-    flags of this rank's pairs are mapped back."""
+    the device (the size exchange is the one host synchronisation), sorted by
+    position, and every sequence's experts become a block of E virtual
+    experts, so ONE capacity pass of the plan kernels applies the
+    per-sequence capacity to all sequences at once; the flags of this rank's
+    pairs are mapped back through the gather permutation.  ``check``
+    validates unique positions (one more sync)."""
     from .collectives import VarBuffer
 
     n, k = local.experts.shape
+    E = num_experts
     dev = local.experts.device
     pos = local.positions.to(dev, torch.int64)
     rows = torch.stack([
@@ -256,33 +265,44 @@ def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: i
         local.experts.reshape(-1).double(),
         (local.gates_f64 if local.gates_f64 is not None else local.gates.double()).reshape(-1),
     ], dim=1)
-    buf, _ = ctx.all_gather_v(tuple(group), VarBuffer.from_rows(rows))
+    buf, counts = ctx.all_gather_v(tuple(group), VarBuffer.from_rows(rows))
     g = buf.rows()
     if g.shape[0] % k:
         raise ProtocolError(f"full-sequence gather: {g.shape[0]} pairs is not a multiple of k={k}; "
                             "shard lengths are inconsistent")
-    gpos = g[::k, 0].to(torch.int64)
-    order = torch.argsort(gpos, stable=True)
-    gpos = gpos[order]
-    if torch.unique(gpos).numel() != gpos.numel():
+    N = g.shape[0] // k
+    gk = g.reshape(N, k, 4)
+    order = torch.argsort(gk[:, 0, 0].to(torch.int64), stable=True)
+    gk = gk[order]
+    gpos = gk[:, 0, 0].to(torch.int64)
+    if check and N > 1 and bool((gpos[1:] == gpos[:-1]).any()):
         raise ProtocolError("full-sequence gather: duplicate token positions across shards")
-    gk = g.reshape(-1, k, 4)[order]
     experts = gk[:, :, 2].to(torch.int32).contiguous()
     g64 = gk[:, :, 3].contiguous()
     global_dec = RoutingDecision(experts, g64.float(), torch.ones_like(experts, dtype=torch.bool),
                                  gpos, None, g64)
-    kept = torch.ones_like(experts, dtype=torch.bool)
-    seq_ids = gpos // seq_len
-    for sid in torch.unique(seq_ids).tolist():
-        m = (seq_ids == sid).nonzero().reshape(-1)
-        sub = RoutingDecision(experts[m].contiguous(), global_dec.gates[m].contiguous(),
-                              kept[m].contiguous(), gpos[m], None, g64[m].contiguous())
-        kept[m] = kept_mask(sub, seq_len, num_experts, params).bool()
+    # compact sequence index of every token (positions are sorted)
+    sid = gpos // seq_len
+    new_seq = torch.ones_like(sid)
+    if N > 1:
+        new_seq[1:] = (sid[1:] != sid[:-1]).to(sid.dtype)
+    cid = torch.cumsum(new_seq, 0) - 1
+    n_seq = int(cid[-1]) + 1 if N else 0
+    if n_seq * E > 4096:
+        raise ValidationError(f"full-sequence capacity: {n_seq} sequences x {E} experts in one "
+                              "group exceeds 4096", constraint="full-seq-virtual-experts")
+    vdec = RoutingDecision((cid[:, None].to(torch.int32) * E + experts).contiguous(), global_dec.gates,
+                           global_dec.kept, gpos, None, g64)
+    cap = capacity_limit(params.capacity_factor, seq_len, E)
+    kept = kept_mask(vdec, seq_len, max(n_seq, 1) * E, params, cap=cap, sorted_positions=True).bool()
     global_dec.kept = kept
-    # map back: local position -> row in the gathered (sorted) table
-    where = torch.searchsorted(gpos, pos)
+    # map back: this rank's pairs sit at rows [off, off + n) of the gathered table
+    me = tuple(group).index(ctx.rank)
+    off = int(np.asarray(counts[:me]).sum()) // k
+    inv = torch.empty_like(order)
+    inv[order] = torch.arange(N, device=dev)
     out = local.copy()
-    out.kept = kept[where]
+    out.kept = kept[inv[off:off + n]]
     return global_dec, out
 
 

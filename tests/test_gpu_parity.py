@@ -316,3 +316,35 @@ def test_pad_to_capacity_equals_unpadded(world, ep, etp, tp):
     for key in r0.expert_grads:
         for a, b in zip(r0.expert_grads[key][0], r1.expert_grads[key][0]):
             assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("priority", ["position", "probability"])
+def test_full_sequence_capacity_many_sequences_vs_oracle(priority):
+    """Device full-sequence dropping (one virtual-expert capacity pass over all
+    sequences of a group) vs the oracle: 3 ranks share a group holding 5
+    sequences, positions shuffled and ragged across the shards."""
+    from paper_2504_14960_b200.router import gather_full_sequence_decision
+
+    E, k, seq_len, n_seq, world = 8, 2, 96, 5, 3
+    rng = np.random.default_rng(11)
+    allpos = rng.permutation(n_seq * seq_len) + 7 * seq_len  # sequences 7..11
+    cuts = np.sort(rng.choice(np.arange(1, allpos.size), world - 1, replace=False))
+    shards = np.split(allpos, cuts)
+    params = B.GatingParams(w_g=np.eye(E), k=k, capacity_factor=1.0, drop_mode="fullsequence",
+                            drop_priority=priority)
+    logits = [rng.standard_normal((s.size, E)).astype(np.float32) for s in shards]
+    world_ = B.LocalWorld(world)
+
+    def program(ctx):
+        r = ctx.rank
+        dec = B.router.routing_from_logits(t(logits[r]), params, shards[r])
+        _, out = gather_full_sequence_decision(ctx, tuple(range(world)), dec, seq_len, E, params)
+        return dec, out
+
+    res = world_.run(program)
+    exps = [r[0].experts.cpu().numpy() for r in res]
+    g64 = [r[0].gates_f64.cpu().numpy() if r[0].gates_f64 is not None else r[0].gates.double().cpu().numpy()
+           for r in res]
+    want = O.full_sequence_kept(exps, g64, shards, seq_len, 1.0, E, priority)
+    for r in range(world):
+        np.testing.assert_array_equal(res[r][1].kept.cpu().numpy(), want[r])
