@@ -283,7 +283,8 @@ def main():
     groups = B.generate_parallel_groups(topo)
     if world > 1:
         nw = B.NcclWorld()
-        nw.setup_groups([groups.moe["EP"], groups.moe["ETP"], groups.moe["EDP"], [tuple(range(world))]])
+        nw.setup_groups([groups.moe["EP"], groups.moe["ETP"], groups.moe["EDP"], [tuple(range(world))],
+                         D.exchange_groups(topo)])
         ctx = B.collectives.NcclRankContext(nw)
     else:
         nw = B.LocalWorld(1, dev)

@@ -236,23 +236,27 @@ B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);
 
 /* ------------------------------------- EP all-to-all over NVLink peer memory
  * Device-side replacement of all_to_all_v + exchange_meta + the grp_order
- * regroup (dispatcher.py:309-362, 425-468).  peer_base[ep] (device array) holds the
- * base address of the same symmetric buffer on every rank of the EP group;
- * regions are addressed by byte offsets.  No call synchronises the host. */
+ * regroup, and of the ETP all-gather-v / reduce-scatter-v
+ * (dispatcher.py:309-362, 425-468).  The exchange group is the EP x ETP block
+ * of ranks, member m = ep_idx * etp + etp_idx; peer_base[ep*etp] (device
+ * array) holds the base address of the same symmetric buffer on every
+ * member; regions are addressed by byte offsets.  No call synchronises the
+ * host. */
 
-/* row `me` of every peer's [ep, E] int32 count matrix := counts[E] */
-B200MOE_API int b200moe_ep_counts_push(const int32_t* counts, int me, int ep, int E,
+/* row `me` of every member's [members, E] int32 count matrix := counts[E] */
+B200MOE_API int b200moe_ep_counts_push(const int32_t* counts, int me, int members, int E,
                                        const uint64_t* peer_base, int64_t cnt_off, void* stream);
-/* cross-GPU barrier: flag exchange at flag_off with system-scope
- * release/acquire; epoch must increase by one per call (bounded spin, traps
- * if a peer never arrives). */
-B200MOE_API int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep,
+/* cross-GPU barrier over the members: flag exchange at flag_off with
+ * system-scope release/acquire; epoch must increase by one per call (bounded
+ * spin, traps if a peer never arrives). */
+B200MOE_API int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int members,
                                    uint32_t epoch, void* stream);
 /* from this rank's copy of the count matrix: seg_off[ep*L] (first row of
- * (me, le) in rank d's receive buffer), goff[L+1] / gcount[L] (this rank's
- * GEMM groups: one per local expert, senders contiguous in rank order, the
- * group padded to align rows).  Traps if a layout exceeds cap_rows. */
-B200MOE_API int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align,
+ * (me, le) in EP index d's receive buffers -- the same on its etp members),
+ * goff[L+1] / gcount[L] (this rank's GEMM groups: one per local expert,
+ * senders contiguous in member order, the group padded to align rows).
+ * Traps if a layout exceeds cap_rows. */
+B200MOE_API int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align,
                                   int64_t cap_rows, int32_t* seg_off, int32_t* goff, int32_t* gcount,
                                   void* stream);
 /* zero the pad rows of this rank's receive buffer (bf16 [rows, H]); with
@@ -260,17 +264,23 @@ B200MOE_API int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int 
 B200MOE_API int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount,
                                      int G, int align, int32_t* origin, void* stream);
 /* fused permute + push: x[t] (bwd: gates*u[t]) -> row rr = seg_off[d,le] +
- * (gemm_row - poff[e]) of rank d's buffer at dst_off.  Forward also writes
- * (me, gemm_row) into rank d's int32 [rows, 2] origin table at origin_off, so
- * d's GEMM epilogue (b200moe_gemm_tc epilogue 5) returns the expert output
- * straight to this rank's padded layout.  Backward reads those returned rows
+ * (gemm_row - poff[e]) of the buffers at dst_off of all etp members of EP
+ * index d = e / L.  Forward also writes (me, gemm_row) into their int32
+ * [rows, 2] origin tables at origin_off, so their GEMM epilogues
+ * (b200moe_gemm_tc epilogue 5) return the expert outputs straight to this
+ * rank's padded layout.  Backward reads the returned (ETP-reduced) rows
  * (y_rows, local, padded layout) for dgates = <u[t], y>. */
 B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L,
                                     const int32_t* topk_idx, const int32_t* gemm_row,
                                     const int32_t* poff, const int32_t* seg_off,
-                                    const uint64_t* peer_base, int me, int64_t dst_off,
+                                    const uint64_t* peer_base, int me, int etp, int64_t dst_off,
                                     int64_t origin_off, const void* y_rows, const float* gates,
                                     float* dgates, int bwd, void* stream);
+/* out[i] = bf16(sum over p ascending of parts[p * part_stride + i]), fp32
+ * accumulation: the ETP reduce of the members' partial expert outputs that
+ * their scatter epilogues returned (collectives.py:386-388 fold order). */
+B200MOE_API int b200moe_ep_reduce_parts(const void* parts, int nparts, int64_t part_stride, int64_t n,
+                                        void* out, void* stream);
 
 /* Elementwise expert activations in the padded row layout, rows < group_off[G].
  * SwiGLU layout: pre has 2F columns, 64-column blocks of [32 gate | 32 up]. */

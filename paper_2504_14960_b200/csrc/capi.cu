@@ -40,10 +40,11 @@ int gemm_simt(const b200moe_gemm_args*, cudaStream_t);
 int gemm_tc(const b200moe_tc_gemm_args*, cudaStream_t);
 int ep_barrier(const uint64_t*, int64_t, int, int, uint32_t, cudaStream_t);
 int ep_counts_push(const int32_t*, int, int, int, const uint64_t*, int64_t, cudaStream_t);
-int ep_layout(const int32_t*, int, int, int, int, int64_t, int32_t*, int32_t*, int32_t*, cudaStream_t);
+int ep_layout(const int32_t*, int, int, int, int, int, int64_t, int32_t*, int32_t*, int32_t*, cudaStream_t);
+int ep_reduce_parts(const void*, int, int64_t, int64_t, void*, cudaStream_t);
 int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
-                const int32_t*, const int32_t*, const uint64_t*, int, int64_t, int64_t, const void*,
+                const int32_t*, const int32_t*, const uint64_t*, int, int, int64_t, int64_t, const void*,
                 const float*, float*, int, cudaStream_t);
 int split_bf16x3(const float*, int64_t, int, void*, void*, cudaStream_t);
 int sum_parts(const float*, int64_t, int64_t, int, float*, cudaStream_t);
@@ -246,12 +247,12 @@ int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int 
   return ep_barrier(peer_base, flag_off, me, ep, epoch, S(stream));
 }
 
-int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align, int64_t cap_rows,
+int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align, int64_t cap_rows,
                       int32_t* seg_off, int32_t* goff, int32_t* gcount, void* stream) {
-  REQUIRE(cnt_local && seg_off && goff && gcount && ep >= 1 && ep <= 32 && L >= 1 && align >= 1 &&
-              cap_rows >= 0 && cap_rows < (1ll << 31),
+  REQUIRE(cnt_local && seg_off && goff && gcount && ep >= 1 && etp >= 1 && ep * etp <= 32 && L >= 1 &&
+              align >= 1 && me >= 0 && me < ep * etp && cap_rows >= 0 && cap_rows < (1ll << 31),
           "ep_layout: bad args");
-  return ep_layout(cnt_local, me, ep, L, align, cap_rows, seg_off, goff, gcount, S(stream));
+  return ep_layout(cnt_local, me, ep, etp, L, align, cap_rows, seg_off, goff, gcount, S(stream));
 }
 
 int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G,
@@ -262,14 +263,24 @@ int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_
 
 int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const int32_t* topk_idx,
                         const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
-                        const uint64_t* peer_base, int me, int64_t dst_off, int64_t origin_off,
+                        const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
                         const void* y_rows, const float* gates, float* dgates, int bwd, void* stream) {
-  REQUIRE(H % 8 == 0 && k >= 1 && L >= 1 && me >= 0, "ep_dispatch: H %% 8, k >= 1, me >= 0 required");
+  REQUIRE(H % 8 == 0 && k >= 1 && L >= 1 && me >= 0 && etp >= 1 && etp <= 32,
+          "ep_dispatch: H %% 8, k >= 1, me >= 0, 1 <= etp <= 32 required");
   if (T == 0) return B200MOE_OK;
   REQUIRE(x && topk_idx && gemm_row && poff && seg_off && peer_base, "ep_dispatch: null pointer");
   REQUIRE(!bwd || (gates && dgates && y_rows), "ep_dispatch: backward needs gates, dgates, y_rows");
-  return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, dst_off, origin_off,
-                     y_rows, gates, dgates, bwd, S(stream));
+  return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, etp, dst_off,
+                     origin_off, y_rows, gates, dgates, bwd, S(stream));
+}
+
+int b200moe_ep_reduce_parts(const void* parts, int nparts, int64_t part_stride, int64_t n, void* out,
+                            void* stream) {
+  REQUIRE(nparts >= 1 && n >= 0 && n % 8 == 0 && part_stride % 8 == 0 && part_stride >= n,
+          "ep_reduce_parts: bad args");
+  if (n == 0) return B200MOE_OK;
+  REQUIRE(parts && out, "ep_reduce_parts: null pointer");
+  return ep_reduce_parts(parts, nparts, part_stride, n, out, S(stream));
 }
 
 int b200moe_split_bf16x3(const float* src, int64_t rows, int E, void* out3, void* out6, void* stream) {

@@ -68,38 +68,43 @@ __global__ void ep_counts_push_kernel(const int32_t* __restrict__ counts, int me
 }
 
 // ------------------------------------------------------------------ layout
-// cnt: this rank's copy of the [ep, E] matrix (row s = sender s's counts).
-// Receive buffers are expert-major: local expert le's rows from all senders
-// are contiguous (sender order), and only the expert's group is padded to
-// `align` rows -- so one GEMM group per local expert, no per-sender padding.
-// seg_off[d*L + le] = first row of (me, le) in rank d's receive buffer;
+// The exchange group is the EP x ETP block of ranks (member m = ep_idx * etp +
+// etp_idx).  cnt: this rank's copy of the [ep*etp, E] matrix (row s = member
+// s's kept counts).  The ETP members of one EP index receive the same rows
+// in the same layout (the reference's ETP all-gather, dispatcher.py:325-334,
+// folded into the dispatch).  Receive buffers are expert-major: local expert
+// le's rows from all senders are contiguous (member order), and only the
+// expert's group is padded to `align` rows -- one GEMM group per local
+// expert, no per-sender padding.
+// seg_off[d*L + le] = first row of (me, le) in EP index d's receive buffers;
 // goff[le] / gcount[le] = group start / real rows in this rank's buffer,
 // goff[L] = end.  A layout beyond cap_rows (the buffer size) traps.
-__global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int me, int ep, int L, int align,
-                                 int64_t cap_rows, int32_t* __restrict__ seg_off,
+__global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int me, int ep, int etp, int L,
+                                 int align, int64_t cap_rows, int32_t* __restrict__ seg_off,
                                  int32_t* __restrict__ goff, int32_t* __restrict__ gcount) {
-  const int E = ep * L;
-  const int d = threadIdx.x;  // one thread per destination layout
+  const int E = ep * L, nmem = ep * etp;
+  const int d = threadIdx.x;  // one thread per destination EP index
   if (d >= ep) return;
+  const bool mine = d == me / etp;
   int64_t run = 0;
   for (int le = 0; le < L; ++le) {
     int64_t tot = 0;
-    for (int s = 0; s < ep; ++s) {
+    for (int s = 0; s < nmem; ++s) {
       if (s == me) seg_off[d * L + le] = (int32_t)(run + tot);
       tot += cnt[s * E + d * L + le];
     }
-    if (d == me) {
+    if (mine) {
       goff[le] = (int32_t)run;
       gcount[le] = (int32_t)tot;
     }
     run += (tot + align - 1) / align * align;
   }
   if (run > cap_rows) {
-    printf("b200moe ep_layout: rank %d receive layout needs %lld rows > capacity %lld\n", d,
+    printf("b200moe ep_layout: EP index %d receive layout needs %lld rows > capacity %lld\n", d,
            (long long)run, (long long)cap_rows);
     __trap();
   }
-  if (d == me) goff[L] = (int32_t)run;
+  if (mine) goff[L] = (int32_t)run;
 }
 
 // zero the alignment pad rows of this rank's receive buffer (and, forward,
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     const __nv_bfloat16* __restrict__ x, int64_t Tn, int64_t H, int k, int L,
     const int32_t* __restrict__ topk, const int32_t* __restrict__ gemm_row,
     const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
-    const uint64_t* __restrict__ peer_base, int me, int64_t dst_off, int64_t origin_off,
+    const uint64_t* __restrict__ peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
     const __nv_bfloat16* __restrict__ y_rows, const float* __restrict__ gates,
     float* __restrict__ dgates) {
   const int lane = threadIdx.x & 31;
@@ -134,10 +139,14 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
   if (t >= Tn) return;
   __nv_bfloat16* dst[KMAX];
   const __nv_bfloat16* ysrc[KMAX];
+  int mem[KMAX];
+  int64_t roff[KMAX];
   float g[KMAX], dot[KMAX];
 #pragma unroll
   for (int s = 0; s < KMAX; ++s) {
     dst[s] = nullptr;
+    mem[s] = 0;
+    roff[s] = 0;
     ysrc[s] = nullptr;
     g[s] = 1.f;
     dot[s] = 0.f;
@@ -147,12 +156,14 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     const int e = topk[t * k + s];
     const int d = e / L, le = e % L;
     const int32_t rr = seg_off[d * L + le] + (gr - poff[e]);
-    dst[s] = reinterpret_cast<__nv_bfloat16*>(peer_base[d] + dst_off) + (int64_t)rr * H;
+    mem[s] = d * etp;  // the ETP members of EP index d all get the row
+    roff[s] = dst_off + (int64_t)rr * H * 2;
+    dst[s] = reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s]] + roff[s]);
     if (BWD) {
       ysrc[s] = y_rows + (int64_t)gr * H;
       g[s] = gates[t * k + s];
-    } else if (lane == 0) {
-      int2* o = reinterpret_cast<int2*>(peer_base[d] + origin_off) + rr;
+    } else if (lane < etp) {
+      int2* o = reinterpret_cast<int2*>(peer_base[mem[s] + lane] + origin_off) + rr;
       *o = make_int2(me, gr);
     }
   }
@@ -188,8 +199,12 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
             o.v[i] = __float2bfloat16_rn(uv * g[s]);
           }
           st_v4(dst[s] + c, o.raw);  // NVLink push
+          for (int m = 1; m < etp; ++m)
+            st_v4(reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s] + m] + roff[s]) + c, o.raw);
         } else {
           st_v4(dst[s] + c, v[u].raw);  // NVLink push
+          for (int m = 1; m < etp; ++m)
+            st_v4(reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s] + m] + roff[s]) + c, v[u].raw);
         }
       }
     }
@@ -204,7 +219,39 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
   }
 }
 
+// ------------------------------------------------------------------ ETP reduce
+// out = sum over the ETP members' partial rows, fp32, ascending member order
+// (the reduce-scatter fold of collectives.py:386-388), rounded to bf16 once.
+__global__ void ep_reduce_parts_kernel(const __nv_bfloat16* __restrict__ parts, int nparts,
+                                       int64_t stride, int64_t n8, __nv_bfloat16* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int p = 0; p < nparts; ++p) {
+      Vec16<__nv_bfloat16> v;
+      v.raw = ld_nc_v4(parts + p * stride + i * 8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(v.v[j]);
+    }
+    Vec16<__nv_bfloat16> o;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o.v[j] = __float2bfloat16_rn(acc[j]);
+    st_v4(out + i * 8, o.raw);
+  }
+}
+
 // ------------------------------------------------------------------ host
+int ep_reduce_parts(const void* parts, int nparts, int64_t stride, int64_t n, void* out, cudaStream_t st) {
+  const int64_t n8 = n / 8;
+  if (n8 == 0) return B200MOE_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n8, 256), 148 * 16);
+  ep_reduce_parts_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(parts), nparts, stride, n8,
+                                               static_cast<__nv_bfloat16*>(out));
+  B200MOE_CHECK_LAUNCH("ep_reduce_parts");
+  return B200MOE_OK;
+}
+
 #define KSW(k, M)                       \
   if (k <= 1) { M(1); }                 \
   else if (k <= 2) { M(2); }            \
@@ -226,9 +273,9 @@ int ep_counts_push(const int32_t* counts, int me, int ep, int E, const uint64_t*
   return B200MOE_OK;
 }
 
-int ep_layout(const int32_t* cnt_local, int me, int ep, int L, int align, int64_t cap_rows,
+int ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align, int64_t cap_rows,
               int32_t* seg_off, int32_t* goff, int32_t* gcount, cudaStream_t st) {
-  ep_layout_kernel<<<1, 32, 0, st>>>(cnt_local, me, ep, L, align, cap_rows, seg_off, goff, gcount);
+  ep_layout_kernel<<<1, 32, 0, st>>>(cnt_local, me, ep, etp, L, align, cap_rows, seg_off, goff, gcount);
   B200MOE_CHECK_LAUNCH("ep_layout");
   return B200MOE_OK;
 }
@@ -244,13 +291,13 @@ int ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcoun
 
 int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_t* topk,
                 const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
-                const uint64_t* peer_base, int me, int64_t dst_off, int64_t origin_off,
+                const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
                 const void* y_rows, const float* gates, float* dgates, int bwd, cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div(Tn, 8);
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* yb = static_cast<const __nv_bfloat16*>(y_rows);
-#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, dst_off, origin_off, yb, gates, dgates)
-#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, dst_off, origin_off, yb, gates, dgates)
+#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, yb, gates, dgates)
+#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, yb, gates, dgates)
   if (Tn > 0) {
     if (bwd) { KSW(k, DB) }
     else { KSW(k, DF) }

@@ -228,6 +228,7 @@ class LayerGroups:
     edp: Tuple[int, ...]
     world: Tuple[int, ...]
     seq: Tuple[int, ...]
+    xch: Tuple[int, ...] = ()  # EP x ETP block (member = ep_idx * etp + etp_idx)
 
 
 @dataclass
@@ -327,7 +328,7 @@ class RankLayer:
         from . import gemm_tc
 
         # (the return exchange is the tensor-core GEMM's scatter epilogue)
-        self.use_peer = (want == "peer" and not self.single and len(groups.etp) == 1
+        self.use_peer = (want == "peer" and not self.single and len(groups.xch) > 1
                          and dtype == torch.bfloat16 and self.k <= 8 and gemm_tc.available()
                          and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
 
@@ -551,20 +552,21 @@ class RankLayer:
 
         H = self.pk.hidden
         cache = ctx.world.__dict__.setdefault("_peer_exchanges", {})
-        key = (ctx.rank, self.g.ep, self.E, self.k, H, self.peer_tag)
+        xch = self.g.xch
+        key = (ctx.rank, xch, self.E, self.k, H, self.peer_tag)
         px = cache.get(key)
         if px is None:
             # buffer layout must be identical on every member: agree on the
             # largest token block once, when the buffers are created
             T_max = max(int(self.peer_tokens or 0), T)
-            T_max = max(int(v) for v in ctx.exchange_meta(self.g.ep, T_max).values())
-            cap = PX.capacity_rows(len(self.g.ep), T_max, self.k, self.L, ALIGN)
+            T_max = max(int(v) for v in ctx.exchange_meta(xch, T_max).values())
+            cap = PX.capacity_rows(len(xch), T_max, self.k, self.L, ALIGN)
             ret = T_max * self.k + self.E * (ALIGN - 1)  # this rank's padded pair layout
             if self.pad_to_capacity and not self.params.dropless:
                 seg = (capacity_limit(self.params.capacity_factor, T_max, self.E) + ALIGN - 1) // ALIGN
                 ret = max(ret, self.E * seg * ALIGN)
             ret = (ret + ALIGN - 1) // ALIGN * ALIGN
-            px = PX.PeerExchange(ctx, self.g.ep, self.E, self.L, H, cap, ret, self.device)
+            px = PX.PeerExchange(ctx, xch, self.E, self.L, H, cap, ret, self.device, etp=len(self.g.etp))
             px.tokens = T_max
             cache[key] = px
         elif T > px.tokens:
@@ -580,21 +582,21 @@ class RankLayer:
         pre, h, _ = X.ffn_forward(px.region("xr"), st["goff"], self.L, None, self.pk, px.cap,
                                   y_scatter=px.scatter("yret"))
         y_sh = self._shared_forward(x, saved)
-        px.barrier()  # every expert output row is back in yret
-        out = K.combine(px.region("yret"), plan.gemm_row, T, gates=dec.gates, out=y_sh,
-                        accumulate=y_sh is not None)
-        saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row)
+        px.barrier()  # every expert output row (ETP: every partial) is back in yret
+        y = px.returned("yret")
+        out = K.combine(y, plan.gemm_row, T, gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
+        saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row, y=y)
         return out, saved
 
     def _backward_peer(self, ctx, u, sv, dec, plan):
         px, st = sv["peer"], sv["pst"]
         px.check_generation(st)
-        dgates = px.backward_dispatch(u, dec.experts, plan, dec.gates, st, ALIGN)
+        dgates = px.backward_dispatch(u, dec.experts, plan, dec.gates, st, sv["y"], ALIGN)
         _, dw1p, dw2p = X.ffn_backward(px.region("dyr"), px.region("xr"), sv["pre"], sv["h"],
                                        st["goff"], self.L, None, self.pk, px.cap,
                                        dx_scatter=px.scatter("dxret"))
-        px.barrier()  # every input-gradient row is back in dxret
-        return px.region("dxret"), dgates, dw1p, dw2p
+        px.barrier()  # every input-gradient row (ETP: every partial) is back in dxret
+        return px.returned("dxret"), dgates, dw1p, dw2p
 
     def _forward_exchange(self, ctx, x, dec, plan, saved):
         T, H = x.shape
@@ -677,10 +679,22 @@ class RankLayer:
 
 
 # ============================================================ layer API
+def exchange_group(topology: ParallelTopology, rank: int) -> Tuple[int, ...]:
+    """The EP x ETP block of ``rank``: EP and ETP are the innermost MoE axes
+    in both layouts, so it is ep*etp consecutive ranks, ordered ep-major."""
+    te, e, _, _ = topology.moe_coords(rank)
+    base = rank - (e * topology.etp + te)
+    return tuple(base + i for i in range(topology.ep * topology.etp))
+
+
+def exchange_groups(topology: ParallelTopology) -> List[Tuple[int, ...]]:
+    return sorted({exchange_group(topology, r) for r in range(topology.world_size)})
+
+
 def _rank_groups(topology, groups: GroupSets, rank: int) -> LayerGroups:
     return LayerGroups(groups.group_of("moe", "EP", rank), groups.group_of("moe", "ETP", rank),
                        groups.group_of("moe", "EDP", rank), tuple(range(topology.world_size)),
-                       sequence_group(topology, rank))
+                       sequence_group(topology, rank), exchange_group(topology, rank))
 
 
 def _validate(blocks, topology, params, seq_len):
@@ -719,7 +733,8 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
     if hasattr(world, "setup_groups"):
         world.setup_groups([groups.moe["EP"], groups.moe["ETP"], groups.moe["EDP"],
                             [tuple(range(topology.world_size))],
-                            sorted({sequence_group(topology, r) for r in range(topology.world_size)})])
+                            sorted({sequence_group(topology, r) for r in range(topology.world_size)}),
+                            exchange_groups(topology)])
 
     def program(ctx):
         rank = ctx.rank

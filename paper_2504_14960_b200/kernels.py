@@ -313,14 +313,14 @@ def ep_barrier(peer_base, flag_off: int, me: int, ep: int, epoch: int):
     L.call("b200moe_ep_barrier", L.ptr(peer_base), flag_off, me, ep, epoch & 0xFFFFFFFF, _sp())
 
 
-def ep_layout(cnt: torch.Tensor, me: int, ep: int, L_: int, align: int, cap_rows: int):
+def ep_layout(cnt: torch.Tensor, me: int, ep: int, etp: int, L_: int, align: int, cap_rows: int):
     """-> (seg_off [ep*L], goff [L+1], gcount [L]) int32 on the device."""
     dev = cnt.device
     seg_off = torch.empty((ep * L_,), dtype=torch.int32, device=dev)
     goff = torch.empty((L_ + 1,), dtype=torch.int32, device=dev)
     gcount = torch.empty((L_,), dtype=torch.int32, device=dev)
-    L.call("b200moe_ep_layout", L.ptr(cnt), me, ep, L_, align, cap_rows, L.ptr(seg_off), L.ptr(goff),
-           L.ptr(gcount), _sp())
+    L.call("b200moe_ep_layout", L.ptr(cnt), me, ep, etp, L_, align, cap_rows, L.ptr(seg_off),
+           L.ptr(goff), L.ptr(gcount), _sp())
     return seg_off, goff, gcount
 
 
@@ -331,7 +331,8 @@ def ep_zero_pads(buf: torch.Tensor, goff, gcount, G: int, align: int, origin=Non
 
 
 def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int, peer_base, me: int,
-                dst_off: int, origin_off: int = 0, bwd: bool = False, y_rows=None, gates=None):
+                etp: int, dst_off: int, origin_off: int = 0, bwd: bool = False, y_rows=None,
+                gates=None):
     """Forward: push x rows to the owners' receive buffers and record their
     origin.  Backward: push gates*u rows; returns dgates [T, k] fp32 = <u, y>
     with y the returned expert outputs (``y_rows``, local padded layout)."""
@@ -340,9 +341,17 @@ def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int,
     _cuda(x, "x", torch.bfloat16)
     dg = torch.empty((T, k), dtype=torch.float32, device=x.device) if bwd else None
     L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
-           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, dst_off, origin_off,
+           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, etp, dst_off, origin_off,
            L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), _sp())
     return dg
+
+
+def ep_reduce_parts(parts: torch.Tensor) -> torch.Tensor:
+    """[P, rows, H] bf16 partial rows -> [rows, H] bf16, summed in fp32."""
+    P_, rows, H = parts.shape
+    out = torch.empty((rows, H), dtype=parts.dtype, device=parts.device)
+    L.call("b200moe_ep_reduce_parts", L.ptr(parts), P_, rows * H, rows * H, L.ptr(out), _sp())
+    return out
 
 
 def act_bwd(dh, pre, act: int, group_off, G: int, F: int, out=None):

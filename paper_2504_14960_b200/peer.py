@@ -1,7 +1,12 @@
-"""EP all-to-all over NVLink peer memory (replaces dispatcher.py:309-362 and
-425-468 of the reference for ETP = 1).
+"""EP all-to-all (and the ETP all-gather / reduce-scatter) over NVLink peer
+memory (replaces dispatcher.py:309-362 and 425-468 of the reference).
 
-Every member of an EP group maps one symmetric buffer:
+The exchange group is the EP x ETP block of ranks (member = ep_idx * etp +
+etp_idx).  A token row routed to EP index d is pushed to all etp members of
+d (the ETP all-gather folded into the dispatch); each member computes its
+F-shard's partial output and returns it into its own block of the sender's
+return region, where the sender sums the blocks (the reduce-scatter).
+Every member maps one symmetric buffer:
 
     [flags | count matrix | xr | dyr | origin | yret | dxret]
 
@@ -49,26 +54,31 @@ def capacity_rows(ep: int, T_max: int, k: int, L_: int, align: int) -> int:
 
 
 class PeerExchange:
-    """Symmetric buffers + device exchange of one EP group, as seen by one rank.
+    """Symmetric buffers + device exchange of one EP x ETP block, as seen by
+    one rank.  ``group`` lists the members in order ep_idx * etp + etp_idx.
 
     cap_rows: receive rows (xr/dyr/origin); ret_rows: rows of this rank's own
-    padded pair layout (yret/dxret)."""
+    padded pair layout (yret/dxret hold one such block per ETP member: the
+    members' partial outputs, reduced by the receiver)."""
 
     def __init__(self, ctx, group: Tuple[int, ...], E: int, L_: int, H: int, cap_rows: int,
-                 ret_rows: int, device):
+                 ret_rows: int, device, etp: int = 1):
         self.group = tuple(group)
-        self.ep = len(group)
+        self.members = len(group)
+        self.etp = etp
+        self.ep = self.members // etp
         self.me = self.group.index(ctx.rank)
+        self.te = self.me % etp
         self.E, self.L, self.H = E, L_, H
         self.cap, self.ret_rows = int(cap_rows), int(ret_rows)
         self.ctx = ctx
         self.device = device
         self.cnt_off = _FLAG_BYTES
-        off = _up(self.cnt_off + self.ep * E * 4, _REGION_ALIGN)
+        off = _up(self.cnt_off + self.members * E * 4, _REGION_ALIGN)
         self.off: Dict[str, int] = {}
         for name, nbytes in (("xr", self.cap * H * 2), ("dyr", self.cap * H * 2),
-                             ("origin", self.cap * 8), ("yret", self.ret_rows * H * 2),
-                             ("dxret", self.ret_rows * H * 2)):
+                             ("origin", self.cap * 8), ("yret", etp * self.ret_rows * H * 2),
+                             ("dxret", etp * self.ret_rows * H * 2)):
             self.off[name] = off
             off += _up(nbytes, _REGION_ALIGN)
         self.nbytes = off
@@ -106,29 +116,39 @@ class PeerExchange:
         self.device_barrier = False
 
     def region(self, name: str) -> torch.Tensor:
-        """This rank's bf16 [rows, H] view of a row region."""
+        """This rank's bf16 view of a row region: [cap, H] (receive side) or
+        [etp, ret_rows, H] (return side, one block per ETP member)."""
         o = self.off[name]
-        rows = self.ret_rows if name in ("yret", "dxret") else self.cap
-        return self.buf[o:o + rows * self.H * 2].view(torch.bfloat16).view(rows, self.H)
+        if name in ("yret", "dxret"):
+            n = self.etp * self.ret_rows * self.H * 2
+            return self.buf[o:o + n].view(torch.bfloat16).view(self.etp, self.ret_rows, self.H)
+        return self.buf[o:o + self.cap * self.H * 2].view(torch.bfloat16).view(self.cap, self.H)
+
+    def returned(self, name: str) -> torch.Tensor:
+        """The returned rows [ret_rows, H]: the single block, or the ETP
+        members' partial blocks summed (reduce-scatter fold order)."""
+        parts = self.region(name)
+        return parts[0] if self.etp == 1 else K.ep_reduce_parts(parts)
 
     def origin(self) -> torch.Tensor:
         o = self.off["origin"]
         return self.buf[o:o + self.cap * 8].view(torch.int32).view(self.cap, 2)
 
     def counts(self) -> torch.Tensor:
-        """This rank's copy of the [ep, E] count matrix."""
-        return self.buf[self.cnt_off:self.cnt_off + self.ep * self.E * 4].view(torch.int32)
+        """This rank's copy of the [members, E] count matrix."""
+        return self.buf[self.cnt_off:self.cnt_off + self.members * self.E * 4].view(torch.int32)
 
     def scatter(self, region: str):
-        """Scatter-epilogue target: (row origin table, peer bases, byte offset)."""
-        return (self.origin(), self.peer_base, self.off[region])
+        """Scatter-epilogue target: (row origin table, peer bases, byte offset
+        of this ETP member's block in the senders' return region)."""
+        return (self.origin(), self.peer_base, self.off[region] + self.te * self.ret_rows * self.H * 2)
 
     # ------------------------------------------------------------ sync
     def barrier(self):
         """All members' prior stream work (local and remote writes) is visible."""
         if self.device_barrier:
             self.epoch += 1
-            K.ep_barrier(self.peer_base, 0, self.me, self.ep, self.epoch)
+            K.ep_barrier(self.peer_base, 0, self.me, self.members, self.epoch)
         else:
             torch.cuda.current_stream().synchronize()
             self.ctx.exchange_meta(self.group, None)
@@ -137,22 +157,23 @@ class PeerExchange:
     def forward_dispatch(self, x, topk_idx, plan, align: int):
         """counts push -> barrier -> layout -> pads -> dispatch -> barrier.
         Returns the routing state the rest of the step needs."""
-        K.ep_counts_push(plan.counts, self.me, self.ep, self.peer_base, self.cnt_off)
+        K.ep_counts_push(plan.counts, self.me, self.members, self.peer_base, self.cnt_off)
         self.barrier()
-        seg_off, goff, gcount = K.ep_layout(self.counts(), self.me, self.ep, self.L, align, self.cap)
+        seg_off, goff, gcount = K.ep_layout(self.counts(), self.me, self.ep, self.etp, self.L, align,
+                                            self.cap)
         K.ep_zero_pads(self.region("xr"), goff, gcount, self.L, align, origin=self.origin())
         K.ep_dispatch(x, topk_idx, plan.gemm_row, plan.poffsets, seg_off, self.L, self.peer_base,
-                      self.me, self.off["xr"], self.off["origin"])
+                      self.me, self.etp, self.off["xr"], self.off["origin"])
         self.barrier()
         self.generation += 1
         return dict(seg_off=seg_off, goff=goff, gcount=gcount, generation=self.generation)
 
-    def backward_dispatch(self, u, topk_idx, plan, gates, st, align: int):
+    def backward_dispatch(self, u, topk_idx, plan, gates, st, y_rows, align: int):
         """pads -> push g*u rows (dgates from the returned y) -> barrier."""
         K.ep_zero_pads(self.region("dyr"), st["goff"], st["gcount"], self.L, align)
         dg = K.ep_dispatch(u, topk_idx, plan.gemm_row, plan.poffsets, st["seg_off"], self.L,
-                           self.peer_base, self.me, self.off["dyr"], bwd=True,
-                           y_rows=self.region("yret"), gates=gates)
+                           self.peer_base, self.me, self.etp, self.off["dyr"], bwd=True,
+                           y_rows=y_rows, gates=gates)
         self.barrier()
         return dg
 

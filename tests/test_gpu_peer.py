@@ -43,22 +43,25 @@ def _run(exchange, topo, params, weights, blocks, ups, shared=None):
 
 
 CASES = [
-    # world, ep, E, k, H, F, sizes, cf, act
-    (2, 2, 8, 2, 256, 512, (384, 384), None, "swiglu"),
-    (2, 2, 8, 2, 128, 256, (96, 300), 1.0, "swiglu"),  # ragged blocks, dropping
-    (4, 4, 4, 2, 128, 192, (64, 128, 0, 200), None, "gelu"),  # k > L, an empty rank
-    (4, 2, 8, 4, 64, 128, (160, 96, 128, 64), 1.25, "swiglu"),  # ep < world (EDP = 2)
-    (4, 4, 16, 8, 64, 64, (256, 256, 256, 256), None, "swiglu"),  # k = 8
-    (8, 8, 8, 2, 128, 128, (128,) * 8, None, "swiglu"),  # the 8-GPU layout: one expert per rank
+    # world, ep, etp, E, k, H, F, sizes, cf, act
+    (2, 2, 1, 8, 2, 256, 512, (384, 384), None, "swiglu"),
+    (2, 2, 1, 8, 2, 128, 256, (96, 300), 1.0, "swiglu"),  # ragged blocks, dropping
+    (4, 4, 1, 4, 2, 128, 192, (64, 128, 0, 200), None, "gelu"),  # k > L, an empty rank
+    (4, 2, 1, 8, 4, 64, 128, (160, 96, 128, 64), 1.25, "swiglu"),  # ep < world (EDP = 2)
+    (4, 4, 1, 16, 8, 64, 64, (256, 256, 256, 256), None, "swiglu"),  # k = 8
+    (8, 8, 1, 8, 2, 128, 128, (128,) * 8, None, "swiglu"),  # the 8-GPU layout: one expert per rank
+    (4, 2, 2, 8, 2, 128, 256, (192, 64, 128, 256), 1.0, "swiglu"),  # EP x ETP (C3 shape)
+    (2, 1, 2, 4, 2, 64, 128, (100, 200), None, "swiglu"),  # ETP only
+    (8, 2, 4, 8, 2, 64, 256, (64, 96, 32, 128, 64, 64, 80, 16), None, "gelu"),  # ETP 4
 ]
 
 
-@pytest.mark.parametrize("world,ep,E,k,H,F,sizes,cf,act", CASES)
-def test_peer_exchange_matches_nccl_exchange(world, ep, E, k, H, F, sizes, cf, act):
+@pytest.mark.parametrize("world,ep,etp,E,k,H,F,sizes,cf,act", CASES)
+def test_peer_exchange_matches_nccl_exchange(world, ep, etp, E, k, H, F, sizes, cf, act):
     seed = 11
-    topo = B.ParallelTopology(world_size=world, ep=ep)
+    topo = B.ParallelTopology(world_size=world, ep=ep, etp=etp, tp=etp)
     params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=cf)
-    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=ep, activation=act)
+    weights = B.init_expert_weights(E, H, F, etp, seed, ep_size=ep, activation=act)
     blocks, ups = _blocks(sizes, H, seed)
     o0, c0, r0 = _run("nccl", topo, params, weights, blocks, ups)
     o1, c1, r1 = _run("peer", topo, params, weights, blocks, ups)
