@@ -401,7 +401,8 @@ def main():
     if sv_last.get("pst") is not None:
         local_pairs = float(sv_last["pst"]["gcount"].sum())
     elif sv_last.get("xpl") is not None:
-        local_pairs = float(sv_last["xpl"].recv_counts.sum())
+        # rows this member received; the ETP gather gives every member about etp x that
+        local_pairs = float(sv_last["xpl"].recv_counts.sum()) * etp
     else:
         local_pairs = float(kept)
     gemm_ms = sum(ms_ for _, ms_ in per_launch)
@@ -414,7 +415,8 @@ def main():
         per_rank = {"expert_rows": [int(v[0]) for v in allg],
                     "gemm_ms": [round(float(v[1]), 3) for v in allg]}
     P = local_pairs
-    flops_step = 18.0 * P * H * F + 18.0 * T * H * c["shared"]
+    # each ETP member multiplies its rows by its F/etp shard
+    flops_step = 18.0 * P * H * (F // etp) + 18.0 * T * H * c["shared"]
     achieved = flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     roof = {"bound": "tensor", "kernel": "gemm_tc (grouped SwiGLU FFN, 6 launches/step)",
             "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
