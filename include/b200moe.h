@@ -118,6 +118,16 @@ B200MOE_API size_t b200moe_router_wgrad_ws(int64_t T, int64_t H, int E);
 B200MOE_API int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz, int64_t T, int64_t H, int E,
                          float* dw_g, void* workspace, size_t workspace_bytes, void* stream);
 
+/* load statistics (router.py:279-301): counts[e] = kept pairs routed to e,
+ * top1[e] = tokens whose best expert is e, score_sum[e] = sum over tokens of
+ * scores[t, e] / sum_e' scores[t, e'] (fp64; scores may be NULL).  kept may
+ * be NULL (all kept).  Deterministic: per-chunk partials folded in order. */
+B200MOE_API size_t b200moe_router_stats_ws(int64_t T, int E);
+B200MOE_API int b200moe_router_stats(const int32_t* topk_idx, const uint8_t* kept, const float* scores,
+                                     int64_t T, int k, int E, int64_t* counts, int64_t* top1,
+                                     double* score_sum, void* workspace, size_t workspace_bytes,
+                                     void* stream);
+
 /* fp32 router GEMMs on the bf16 tensor cores (router.py:145, dispatcher.py:
  * 489-490 for bf16 tokens): an fp32 matrix is split into three bf16 parts
  * hi + mid + lo that sum to it exactly; with Ep = E rounded up to 8,

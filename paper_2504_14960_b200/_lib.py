@@ -62,6 +62,8 @@ _SIGS = {
     "b200moe_act_fwd": [P, I32, I32, P, I32, I64, I64, P, P],
     "b200moe_act_bwd": [P, P, I32, I32, P, I32, I64, I64, P, P],
     "b200moe_split_bf16x3": [P, I64, I32, P, P, P],
+    "b200moe_router_stats_ws": [I64, I32],
+    "b200moe_router_stats": [P, P, P, I64, I32, I32, P, P, P, P, SZ, P],
     "b200moe_sum_parts": [P, I64, I64, I32, P, P],
     "b200moe_ep_counts_push": [P, I32, I32, I32, P, I64, P],
     "b200moe_ep_barrier": [P, I64, I32, I32, ctypes.c_uint32, P],
@@ -75,6 +77,7 @@ _RESTYPES = {
     "b200moe_last_error": ctypes.c_char_p,
     "b200moe_dispatch_plan_ws": SZ,
     "b200moe_router_wgrad_ws": SZ,
+    "b200moe_router_stats_ws": SZ,
 }
 
 _lib: Optional[ctypes.CDLL] = None
@@ -121,8 +124,9 @@ def check(rc: int, what: str) -> None:
 # kernels launched per entry point (bench.py reports the total as gpu_launches)
 _LAUNCHES = {"b200moe_dispatch_plan": 3}
 _LAUNCHES["b200moe_router_wgrad"] = 2
+_LAUNCHES["b200moe_router_stats"] = 2
 _NO_LAUNCH = {"b200moe_version", "b200moe_last_error", "b200moe_device_check",
-              "b200moe_dispatch_plan_ws", "b200moe_router_wgrad_ws"}
+              "b200moe_dispatch_plan_ws", "b200moe_router_wgrad_ws", "b200moe_router_stats_ws"}
 _launches = 0
 
 

@@ -47,6 +47,9 @@ int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const i
                 const int32_t*, const int32_t*, const uint64_t*, int, int, int64_t, int64_t, const void*,
                 const float*, float*, int, cudaStream_t);
 int split_bf16x3(const float*, int64_t, int, void*, void*, cudaStream_t);
+size_t router_stats_ws_bytes(int64_t, int);
+int router_stats(const int32_t*, const uint8_t*, const float*, int64_t, int, int, int64_t*, int64_t*,
+                 double*, void*, cudaStream_t);
 int sum_parts(const float*, int64_t, int64_t, int, float*, cudaStream_t);
 int act_fwd(const void*, int, int, const int32_t*, int, int64_t, int64_t, void*, cudaStream_t);
 int act_bwd(const void*, const void*, int, int, const int32_t*, int, int64_t, int64_t, void*,
@@ -281,6 +284,17 @@ int b200moe_ep_reduce_parts(const void* parts, int nparts, int64_t part_stride, 
   if (n == 0) return B200MOE_OK;
   REQUIRE(parts && out, "ep_reduce_parts: null pointer");
   return ep_reduce_parts(parts, nparts, part_stride, n, out, S(stream));
+}
+
+size_t b200moe_router_stats_ws(int64_t T, int E) { return router_stats_ws_bytes(T, E); }
+
+int b200moe_router_stats(const int32_t* topk_idx, const uint8_t* kept, const float* scores, int64_t T, int k,
+                         int E, int64_t* counts, int64_t* top1, double* score_sum, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  REQUIRE(T >= 0 && k >= 1 && E >= 1 && k <= E, "router_stats: bad shape");
+  REQUIRE(workspace_bytes >= router_stats_ws_bytes(T, E), "router_stats: workspace too small");
+  REQUIRE(counts && top1 && score_sum && workspace && (T == 0 || topk_idx), "router_stats: null pointer");
+  return router_stats(topk_idx, kept, scores, T, k, E, counts, top1, score_sum, workspace, S(stream));
 }
 
 int b200moe_split_bf16x3(const float* src, int64_t rows, int E, void* out3, void* out6, void* stream) {

@@ -613,6 +613,84 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int64
 }
 
 // ---------------------------------------------------------------------------
+// load statistics                                          (router.py:279-301)
+// ---------------------------------------------------------------------------
+// Per 256-token chunk: kept pairs per expert, top-1 counts, and the sum of
+// row-normalised scores per expert (fp64); a second pass folds the chunks in
+// order, so the result is deterministic.
+constexpr int ST_CHUNK = 256;
+
+__global__ void __launch_bounds__(ST_CHUNK) router_stats_partial_kernel(
+    const int32_t* __restrict__ topk, const uint8_t* __restrict__ kept, const float* __restrict__ scores,
+    int64_t Tn, int k, int E, int32_t* __restrict__ pc, int32_t* __restrict__ pt, double* __restrict__ pp) {
+  __shared__ double rinv[ST_CHUNK];
+  const int64_t t0 = (int64_t)blockIdx.x * ST_CHUNK;
+  const int nt = (int)(Tn - t0 < ST_CHUNK ? Tn - t0 : ST_CHUNK);
+  if (scores && threadIdx.x < nt) {
+    const float* row = scores + (t0 + threadIdx.x) * E;
+    double s = 0.0;
+    for (int e = 0; e < E; ++e) s += row[e];
+    rinv[threadIdx.x] = 1.0 / s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += ST_CHUNK) {
+    int32_t c = 0, c1 = 0;
+    double p = 0.0;
+    for (int i = 0; i < nt; ++i) {
+      const int64_t t = t0 + i;
+      for (int s = 0; s < k; ++s)
+        c += (topk[t * k + s] == e && (!kept || kept[t * k + s])) ? 1 : 0;
+      c1 += topk[t * k] == e ? 1 : 0;
+      if (scores) p += (double)scores[t * E + e] * rinv[i];
+    }
+    pc[(int64_t)blockIdx.x * E + e] = c;
+    pt[(int64_t)blockIdx.x * E + e] = c1;
+    pp[(int64_t)blockIdx.x * E + e] = p;
+  }
+}
+
+__global__ void router_stats_reduce_kernel(const int32_t* __restrict__ pc, const int32_t* __restrict__ pt,
+                                           const double* __restrict__ pp, int64_t nch, int E,
+                                           int64_t* __restrict__ counts, int64_t* __restrict__ top1,
+                                           double* __restrict__ psum) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int64_t c = 0, c1 = 0;
+  double p = 0.0;
+  for (int64_t i = 0; i < nch; ++i) {
+    c += pc[i * E + e];
+    c1 += pt[i * E + e];
+    p += pp[i * E + e];
+  }
+  counts[e] = c;
+  top1[e] = c1;
+  psum[e] = p;
+}
+
+size_t router_stats_ws_bytes(int64_t Tn, int E) {
+  return (size_t)ceil_div(Tn > 0 ? Tn : 1, ST_CHUNK) * E * (4 + 4 + 8);
+}
+
+int router_stats(const int32_t* topk, const uint8_t* kept, const float* scores, int64_t Tn, int k, int E,
+                 int64_t* counts, int64_t* top1, double* psum, void* ws, cudaStream_t st) {
+  const int64_t nch = ceil_div(Tn > 0 ? Tn : 1, ST_CHUNK);
+  double* pp = static_cast<double*>(ws);
+  int32_t* pc = reinterpret_cast<int32_t*>(pp + nch * E);
+  int32_t* pt = pc + nch * E;
+  if (Tn > 0)
+    router_stats_partial_kernel<<<(unsigned)nch, ST_CHUNK, 0, st>>>(topk, kept, scores, Tn, k, E, pc, pt, pp);
+  else {
+    cudaMemsetAsync(pc, 0, (size_t)E * 4, st);
+    cudaMemsetAsync(pt, 0, (size_t)E * 4, st);
+    cudaMemsetAsync(pp, 0, (size_t)E * 8, st);
+  }
+  router_stats_reduce_kernel<<<(unsigned)ceil_div(E, 128), 128, 0, st>>>(pc, pt, pp, Tn > 0 ? nch : 1, E, counts,
+                                                                          top1, psum);
+  B200MOE_CHECK_LAUNCH("router_stats");
+  return B200MOE_OK;
+}
+
+// ---------------------------------------------------------------------------
 // fp32 router GEMMs on the bf16 tensor cores: an fp32 value v is split into
 // three bf16 parts hi + mid + lo == v exactly (8 + 8 + 8 significand bits),
 // so x(bf16) . W_g = x.hi + x.mid + x.lo with exact products and fp32

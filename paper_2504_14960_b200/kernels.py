@@ -142,6 +142,20 @@ def _splitk_groups(T: int, device, parts: int = 8) -> Tuple[torch.Tensor, int]:
     return _SPLITK_CACHE[key]
 
 
+def router_stats(topk_idx: torch.Tensor, kept, scores, E: int):
+    """-> (counts [E] int64, top1 [E] int64, score_sum [E] fp64) on the device."""
+    T, k = topk_idx.shape
+    dev = topk_idx.device
+    ws = torch.empty((max(int(L.load().b200moe_router_stats_ws(T, E)), 8),), dtype=torch.uint8, device=dev)
+    counts = torch.empty((E,), dtype=torch.int64, device=dev)
+    top1 = torch.empty((E,), dtype=torch.int64, device=dev)
+    psum = torch.empty((E,), dtype=torch.float64, device=dev)
+    kept_u8 = None if kept is None else kept.to(torch.uint8).contiguous()
+    L.call("b200moe_router_stats", L.ptr(topk_idx), L.ptr(kept_u8), L.ptr(scores), T, k, E,
+           L.ptr(counts), L.ptr(top1), L.ptr(psum), L.ptr(ws), ctypes.c_size_t(ws.numel()), _sp())
+    return counts, top1, psum
+
+
 def router_topk(logits: torch.Tensor, k: int, gate_fn: int, renorm: bool, want_f64: bool = False):
     T, E = logits.shape
     _cuda(logits, "logits", torch.float32)

@@ -314,18 +314,20 @@ class LoadStats:
 
 
 def load_stats(decision: RoutingDecision, num_experts: int) -> LoadStats:
-    """Kept pairs per expert, imbalance, Switch aux loss (router.py:279-301)."""
-    e = decision.experts.reshape(-1).long()
-    kept = decision.kept.reshape(-1).bool()
-    counts = torch.bincount(e[kept], minlength=num_experts).cpu().numpy().astype(np.int64)
+    """Kept pairs per expert, imbalance, Switch aux loss (router.py:279-301):
+    one deterministic reduction kernel (router_stats), one host read."""
+    n = decision.n_tokens
+    scores = None if decision.scores is None else decision.scores.float().contiguous()
+    counts_d, top1_d, psum_d = K.router_stats(decision.experts.contiguous(), decision.kept, scores,
+                                              num_experts)
+    counts = counts_d.cpu().numpy().astype(np.int64)
     mean = counts.sum() / num_experts
     imbalance = float(counts.max() / mean) if mean > 0 else float("nan")
-    if decision.scores is None or decision.n_tokens == 0:
+    if scores is None or n == 0:
         aux = float("nan")
     else:
-        f = torch.bincount(decision.experts[:, 0].long(), minlength=num_experts).double() / decision.n_tokens
-        s = decision.scores.double()
-        p = (s / s.sum(dim=1, keepdim=True)).mean(dim=0)
+        f = top1_d.double() / n
+        p = psum_d / n
         aux = float(num_experts * torch.dot(f, p))
     return LoadStats(counts=counts, imbalance=imbalance, aux_loss=aux)
 

@@ -348,3 +348,20 @@ def test_full_sequence_capacity_many_sequences_vs_oracle(priority):
     want = O.full_sequence_kept(exps, g64, shards, seq_len, 1.0, E, priority)
     for r in range(world):
         np.testing.assert_array_equal(res[r][1].kept.cpu().numpy(), want[r])
+
+
+@pytest.mark.parametrize("E,k,n,gate", [(8, 2, 1000, "softmax"), (64, 8, 777, "sigmoid"), (4, 1, 0, "softmax")])
+def test_load_stats_kernel_vs_oracle(E, k, n, gate):
+    """router_stats kernel (load_stats, router.py:279-301) vs the oracle, with drops."""
+    rng = np.random.default_rng(E + n)
+    logits = rng.standard_normal((n, E)).astype(np.float32)
+    params = B.GatingParams(w_g=np.eye(E), k=k, gate_fn=gate, capacity_factor=1.0)
+    dec = B.router.routing_from_logits(t(logits).reshape(n, E), params)
+    dec = B.apply_capacity(dec, n, E, params) if n else dec
+    got = B.load_stats(dec, E)
+    want = O.load_stats(dec.experts.cpu().numpy(), dec.kept.cpu().numpy(),
+                        dec.scores.double().cpu().numpy(), E)
+    np.testing.assert_array_equal(got.counts, want[0])
+    if n:
+        assert abs(got.imbalance - want[1]) < 1e-12
+        assert abs(got.aux_loss - want[2]) < 1e-6 * max(1.0, abs(want[2]))
