@@ -33,6 +33,8 @@ from __future__ import annotations
 
 from typing import Dict, Tuple
 
+import numpy as np
+
 import torch
 
 from . import kernels as K
@@ -51,6 +53,28 @@ def capacity_rows(ep: int, T_max: int, k: int, L_: int, align: int) -> int:
     """Receive rows a rank can need: every sender routes each of its tokens
     to at most min(k, L) of this rank's experts, plus one pad per expert."""
     return ep * T_max * min(k, L_) + L_ * (align - 1)
+
+
+def wire_rows(send_counts, topology) -> int:
+    """Token rows the exchange moves between GPUs in one layer step (forward
+    + backward), from every rank's kept rows per EP destination
+    (``send_counts[r]`` [ep, L], DispatchPlan.send_counts).
+
+    A pair routed from rank r to EP index j is pushed to the etp members of
+    j -- all but r itself cross the wire -- and each member returns its
+    partial the same way; the backward repeats both.  This equals the
+    reference SimWorld ledger's all_to_all_v + all_gather_v +
+    reduce_scatter_v token rows (collectives.py:11-18; the a2a charges
+    off-rank rows, the ETP gather (etp-1) rows per received row and the
+    reduce-scatter the non-owned partials), which tests/test_cpu_host.py
+    checks against the golden ledger."""
+    etp = topology.etp
+    total = 0
+    for r, sc in enumerate(send_counts):
+        _, e_idx, _, _ = topology.moe_coords(r)
+        sc = [int(v) for v in np.asarray(sc).sum(axis=1)]
+        total += sum(c * (etp - (1 if j == e_idx else 0)) for j, c in enumerate(sc))
+    return 4 * total
 
 
 class PeerExchange:

@@ -192,6 +192,14 @@ def layer_cases():
             dw2[e] = np.concatenate([res.expert_grads[(ei, t)][1][le] for t in range(etp)], axis=0)
         out[pre + "dw1"] = dw1
         out[pre + "dw2"] = dw2
+        # SimWorld wire ledger (collectives.py:11-18): token rows (width H) per
+        # primitive; the full-sequence routing gather has width 4 and is skipped
+        rows = {"all_to_all_v": 0, "all_gather_v": 0, "reduce_scatter_v": 0}
+        for rec in world.ledger:
+            if rec.primitive in rows and rec.row_width == H:
+                rows[rec.primitive] += rec.total_elements // rec.row_width
+        out[pre + "ledger_rows"] = np.array([rows["all_to_all_v"], rows["all_gather_v"],
+                                             rows["reduce_scatter_v"]], dtype=np.int64)
     return out
 
 

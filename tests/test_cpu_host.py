@@ -115,3 +115,22 @@ def test_no_device_fails_loudly():
         pytest.skip("libb200moe.so not built")
     with pytest.raises(RuntimeError):
         _lib.load()
+
+
+def test_peer_exchange_wire_rows_match_reference_ledger(golden):
+    """The device exchange moves exactly the token rows the reference's
+    collectives charge on the wire (SimWorld ledger: all_to_all_v +
+    all_gather_v + reduce_scatter_v), for every golden multi-rank topology."""
+    from paper_2504_14960_b200.peer import wire_rows
+
+    d = golden("layer")
+    checked = 0
+    for c in sorted({k.split("_")[0] for k in d if k.startswith("l")}):
+        w, tp, cp, ep, etp = (int(v) for v in d[c + "_meta"][:5])
+        if w == 1:
+            continue
+        topo = ParallelTopology(world_size=w, tp=tp, cp=cp, ep=ep, etp=etp)
+        counts = [d[c + f"_counts{r}"] for r in range(w)]
+        assert wire_rows(counts, topo) == int(d[c + "_ledger_rows"].sum()), c
+        checked += 1
+    assert checked >= 4
