@@ -379,19 +379,26 @@ def main():
                "bytes_per_step": sent, "impl": "NCCL all_to_all_single (grouped P2P)"}
     peer_events = [(n, m) for n, m in all_launches if n == "ep_dispatch"]
     if peer_events and world > 1:
-        # device-side exchange: the dispatch kernels push the kept pairs' rows
-        # twice per step (x forward, g*u backward); the (ep-1)/ep remote share
-        # of those bytes over the dispatch time is the per-GPU, per-direction
-        # NVLink rate.  The return direction (y, dx) is stored by the GEMM
-        # epilogues while they compute and has no separate time.
-        pairs = float(sv_last["plan"].counts.sum())
-        moved = 2 * pairs * H * 2
+        # device-side exchange: the dispatch kernels push this rank's kept
+        # rows to the etp members of each owning EP index, forward (x) and
+        # backward (g*u); the rows that leave the GPU over the dispatch time is
+        # the per-GPU, per-direction NVLink rate.  The return direction (y,
+        # dx) is stored by the GEMM epilogues while they compute (no separate
+        # time).  Exact bytes from the plan counts (peer.wire_rows semantics).
+        from paper_2504_14960_b200.peer import wire_rows
+
+        cnt = sv_last["plan"].counts.to(torch.int64)
+        _, e_idx, _, _ = topo.moe_coords(rank)
+        per_ep = cnt.reshape(ep, -1).sum(1).cpu().tolist()
+        pushed_rows = sum(c * (etp - (1 if j == e_idx else 0)) for j, c in enumerate(per_ep))
+        remote = 2 * pushed_rows * H * 2
+        allc = [torch.empty_like(cnt) for _ in range(world)]
+        dist.all_gather(allc, cnt)
+        job_wire = wire_rows([c.reshape(ep, -1).cpu().numpy() for c in allc], topo) * H * 2
         t_x = sum(m for _, m in peer_events) / 1e3
-        remote = moved * (ep - 1) / ep
         a2a = {"busbw_gbs": remote / t_x / 1e9, "nominal_gbs": 900.0,
                "frac_nominal": remote / t_x / 1e9 / 900.0, "ms_per_step": t_x * 1e3,
-               "bytes_per_step": moved, "remote_bytes_per_step": remote,
-               "return_bytes_in_gemm_epilogues": moved,
+               "remote_bytes_per_step": remote, "job_wire_bytes_per_step": job_wire,
                "impl": "NVLink peer memory: ep_dispatch push kernels + GEMM scatter epilogues (peer.py)"}
     # kept (token, expert) pairs of the last step, summed over ranks; each
     # pair costs 18*H*F flop fwd+bwd with SwiGLU (6PHF + 12PHF),
