@@ -55,6 +55,9 @@ B200MOE_API const char* b200moe_version(void);
 B200MOE_API const char* b200moe_last_error(void);
 /* 0 when the current device is sm_100 (B200); B200MOE_ENODEV otherwise. */
 B200MOE_API int b200moe_device_check(void);
+/* let kernels on the current device dereference device `peer`'s memory (the
+ * in-process multi-GPU world; already-enabled is not an error) */
+B200MOE_API int b200moe_enable_peer_access(int peer);
 
 /* ---------------------------------------------------------------- router */
 

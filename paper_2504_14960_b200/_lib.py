@@ -46,6 +46,7 @@ _SIGS = {
     "b200moe_version": [],
     "b200moe_last_error": [],
     "b200moe_device_check": [],
+    "b200moe_enable_peer_access": [I32],
     "b200moe_router_logits": [P, I32, P, I64, I64, I32, P, P],
     "b200moe_router_topk": [P, I64, I32, I32, I32, I32, P, P, P, P, P],
     "b200moe_dispatch_plan_ws": [I64, I32],
@@ -125,7 +126,7 @@ def check(rc: int, what: str) -> None:
 _LAUNCHES = {"b200moe_dispatch_plan": 3}
 _LAUNCHES["b200moe_router_wgrad"] = 2
 _LAUNCHES["b200moe_router_stats"] = 2
-_NO_LAUNCH = {"b200moe_version", "b200moe_last_error", "b200moe_device_check",
+_NO_LAUNCH = {"b200moe_version", "b200moe_last_error", "b200moe_device_check", "b200moe_enable_peer_access",
               "b200moe_dispatch_plan_ws", "b200moe_router_wgrad_ws", "b200moe_router_stats_ws"}
 _launches = 0
 

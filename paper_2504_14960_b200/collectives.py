@@ -8,11 +8,12 @@ collectives.py: VarBuffer :42-78, SimWorld.run :128-173, RankContext
 Two worlds implement it:
   * ``NcclWorld``  -- production: one process per GPU (torchrun), collectives
     over NCCL process groups built from the folded EP/ETP/EDP meshes.
-  * ``LocalWorld`` -- N simulated ranks as threads of one process sharing one
-    GPU (and its default stream); collectives are device copies performed by
-    the last rank to arrive, like SimWorld.  Used by the parity tests to run
-    multi-rank topologies on a single B200.  No kernel ever waits on another
-    rank's kernel, so emulated ranks cannot deadlock the GPU.
+  * ``LocalWorld`` -- N ranks as threads of one process, like SimWorld: all on
+    one GPU (the parity tests run multi-rank topologies on a single B200) or
+    one GPU each (``devices=[...]``: the in-process multi-GPU shim, peer
+    access enabled between the devices).  Collectives are device copies
+    performed by the last rank to arrive.  No kernel ever waits on another
+    rank's kernel, so the ranks cannot deadlock the GPUs.
 
 Both also provide the engine-level primitives ``p2p`` (a batch of row-chunk
 sends/receives) and ``gather_counts`` (all-gather of small int vectors to
@@ -81,9 +82,10 @@ class _Slot:
 
 
 class LocalWorld:
-    """N ranks as threads on one device (SimWorld analogue)."""
+    """N ranks as threads of one process (SimWorld analogue), on one device
+    or -- with ``devices`` -- one device per rank."""
 
-    def __init__(self, n_ranks: int, device=None):
+    def __init__(self, n_ranks: int, device=None, devices: Optional[Sequence] = None):
         if n_ranks < 1:
             raise ValidationError("n_ranks must be >= 1", constraint="n_ranks>=1")
         self.n_ranks = n_ranks
@@ -91,6 +93,15 @@ class LocalWorld:
         if dev.type == "cuda" and dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
+        self.devices = None
+        if devices is not None:
+            if len(devices) != n_ranks:
+                raise ValidationError(f"{len(devices)} devices for {n_ranks} ranks",
+                                      constraint="devices==ranks")
+            self.devices = [torch.device("cuda", torch.device(d).index if not isinstance(d, int) else d)
+                            for d in devices]
+            self.device = self.devices[0]
+            _enable_peer_access(self.devices)
         self._cond = threading.Condition()
         self._slots: Dict[tuple, _Slot] = {}
         self._seq: Dict[tuple, int] = {}
@@ -108,7 +119,7 @@ class LocalWorld:
 
         def runner(rank: int):
             try:
-                torch.cuda.set_device(self.device)
+                torch.cuda.set_device(self.device_of(rank))
                 results[rank] = program(LocalRankContext(self, rank))
             except _Aborted:
                 pass
@@ -132,6 +143,9 @@ class LocalWorld:
         if errors:
             raise errors[min(errors)]
         return results
+
+    def device_of(self, rank: int) -> torch.device:
+        return self.devices[rank] if self.devices is not None else self.device
 
     def _rendezvous(self, rank: int, group: Group, payload: Any,
                     compute: Callable[[Group, Dict[int, Any]], Dict[int, Any]]) -> Any:
@@ -166,6 +180,23 @@ class LocalWorld:
             if slot.remaining == 0:
                 del self._slots[skey]
         return out
+
+
+def _enable_peer_access(devices) -> None:
+    """Let kernels on every device dereference the others' memory (the peer
+    exchange stores into peer buffers directly)."""
+    from . import _lib as L
+
+    lib = L.load()
+    cur = torch.cuda.current_device()
+    try:
+        for a in devices:
+            torch.cuda.set_device(a)
+            for b in devices:
+                if a != b:
+                    L.check(lib.b200moe_enable_peer_access(b.index), "b200moe_enable_peer_access")
+    finally:
+        torch.cuda.set_device(cur)
 
 
 class _Aborted(BaseException):
@@ -328,10 +359,10 @@ class LocalRankContext(RankContext):
         def compute(g, payloads):
             total = payloads[g[0]].clone()
             for r in g[1:]:
-                total += payloads[r]
+                total += payloads[r].to(total.device)
             if op == "avg":
                 total /= len(g)
-            return {r: total.clone() for r in g}
+            return {r: total.to(payloads[r].device, copy=True) for r in g}
 
         return self.world._rendezvous(self.rank, group, values, compute)
 

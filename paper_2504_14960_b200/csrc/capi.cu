@@ -114,6 +114,26 @@ int b200moe_router_topk(const float* logits, int64_t T, int E, int k, int gate_f
                      S(stream));
 }
 
+int b200moe_enable_peer_access(int peer) {
+  int dev = 0, can = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("enable_peer_access: cannot query device %d -> %d", dev, peer);
+    return B200MOE_ENODEV;
+  }
+  if (!can) {
+    set_error("enable_peer_access: device %d cannot access device %d", dev, peer);
+    return B200MOE_EUNSUPPORTED;
+  }
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+    set_error("enable_peer_access: %s", cudaGetErrorString(e));
+    return B200MOE_ELAUNCH;
+  }
+  cudaGetLastError();  // clear "already enabled"
+  return B200MOE_OK;
+}
+
 size_t b200moe_dispatch_plan_ws(int64_t T, int E) { return plan_ws_bytes(T, E); }
 
 int b200moe_dispatch_plan(const int32_t* topk_idx, const float* gates, const uint8_t* kept_in,

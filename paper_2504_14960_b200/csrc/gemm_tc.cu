@@ -16,6 +16,8 @@
 // dW2 = act^T dy, dh = dy W2^T, dpre = dh*act', dW1 = x^T dpre, dx = dpre W1^T).
 #include <cuda.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace b200moe {
@@ -1210,14 +1212,19 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
                 : (b_mn ? gemm_tc_kernel<false, true, 2> : gemm_tc_kernel<false, false, 2>);
     smem = Cfg<2>::SMEM;
   }
-  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  // the shared-memory opt-in is per device and per kernel (thread-safe: a
+  // repeated set is harmless)
+  constexpr int MAX_DEV = 64;
+  static std::atomic<bool> attr_set[MAX_DEV][8];
+  int dev = 0;
+  cudaGetDevice(&dev);
   const int ki = (cg == 2 ? 4 : 0) + (a_mn ? 2 : 0) + (b_mn ? 1 : 0);
-  if (!attr_set[ki]) {
+  if (dev >= MAX_DEV || !attr_set[dev][ki].load()) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       set_error("gemm_tc: cannot set %d B dynamic shared memory", smem);
       return B200MOE_ELAUNCH;
     }
-    attr_set[ki] = true;
+    if (dev < MAX_DEV) attr_set[dev][ki].store(true);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

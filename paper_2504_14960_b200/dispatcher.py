@@ -741,7 +741,7 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
         b = blocks[rank]
         etp_idx, ep_idx, _, _ = topology.moe_coords(rank)
         w = weights_map[(ep_idx, etp_idx)]
-        dev = getattr(world, "device", torch.device("cuda"))
+        dev = world.device_of(rank) if hasattr(world, "device_of") else getattr(world, "device", torch.device("cuda"))
         dt = dtype or (b.values.dtype if b.values.dtype in (torch.float32, torch.bfloat16) else torch.float32)
         layer = RankLayer(params, w, topology, _rank_groups(topology, groups, rank), rank, dt, dev,
                           seq_len, check=check_finite_inputs, shared=shared_weights,
