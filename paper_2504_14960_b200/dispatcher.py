@@ -8,17 +8,23 @@ moe_backward :387-510).
 
 Per rank (SPMD), forward:
   K1 router (logits, top-k, capacity + plan as one counting sort)
-  K2 permute into send order            -- or straight into the padded GEMM
-                                           layout when EP = ETP = 1
-  EP all-to-all-v (counts exchanged once, rows land expert-major /
-  sender-minor, so the reference's receive regroup disappears)
-  ETP all-gather-v -> K3 grouped FFN -> ETP reduce-scatter-v
-  EP all-to-all-v back -> K2 gate-weighted combine
-Backward mirrors it (AG <-> RS swapped), then the router backward and the
-dW_g all-reduce over the world (expert grads over EDP).
+  one rank (EP = ETP = 1): K2 permute straight into the padded GEMM layout
+    -> K3 grouped FFN -> K2 gate-weighted combine
+  several ranks, bf16 (default): device-side exchange over NVLink peer
+    memory (peer.py): counts pushed to every member, receive layouts derived
+    on the device, token rows pushed into the owners' buffers (the ETP
+    all-gather folded in) -> K3 grouped FFN whose epilogue stores each
+    output row straight back into its sender's layout (the return
+    all-to-all and, per ETP member block, the reduce-scatter) -> combine
+  NCCL path (fp32 parity mode, B200MOE_EP_EXCHANGE=nccl): counts exchanged
+    once, all_to_all_single into the padded expert-major layout, ETP
+    all-gather-v / reduce-scatter-v as P2P, return all-to-all, combine
+Backward mirrors it, then the router backward and the dW_g all-reduce over
+the world (expert grads over EDP).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
@@ -27,6 +33,7 @@ import torch
 
 from . import _lib as L
 from . import experts as X
+from . import gemm_tc
 from . import kernels as K
 from .collectives import LocalWorld, RankContext
 from .errors import ValidationError
@@ -292,10 +299,8 @@ class RankLayer:
         # layer never synchronises with the host.  Sub-sequence dropping only
         # (the per-rank capacity bounds every segment).
         self.pad_to_capacity = pad_to_capacity
-        # overlap the EP all-to-all with the FFN of the rank's own rows
-        # (B200MOE_OVERLAP=0 selects the serial exchange)
-        import os
-
+        # NCCL path: overlap the EP all-to-all with the FFN of the rank's own
+        # rows (B200MOE_OVERLAP=0 selects the serial exchange)
         self.overlap = os.environ.get("B200MOE_OVERLAP", "1") != "0"
         self.params = params
         self.topo = topology
@@ -318,16 +323,14 @@ class RankLayer:
         if dtype == torch.bfloat16 and os.environ.get("B200MOE_ROUTER_TC", "1") != "0":
             self.wg_parts = params.device_w_g_parts(device)
         self.single = len(groups.ep) == 1 and len(groups.etp) == 1
-        # EP exchange: device-side over NVLink peer memory (bf16, ETP = 1), or
-        # NCCL all_to_all_single (B200MOE_EP_EXCHANGE=nccl, fp32, ETP > 1)
+        # EP / ETP exchange: device-side over NVLink peer memory (bf16; the
+        # return direction is the tensor-core GEMM's scatter epilogue), or
+        # NCCL (B200MOE_EP_EXCHANGE=nccl, and the fp32 parity mode)
         self.peer_tokens = peer_tokens
         self.peer_tag = peer_tag
         want = exchange or os.environ.get("B200MOE_EP_EXCHANGE", "peer")
         if want not in ("peer", "nccl"):
             raise ValidationError(f"unknown EP exchange {want!r}", constraint="exchange")
-        from . import gemm_tc
-
-        # (the return exchange is the tensor-core GEMM's scatter epilogue)
         self.use_peer = (want == "peer" and not self.single and len(groups.xch) > 1
                          and dtype == torch.bfloat16 and self.k <= 8 and gemm_tc.available()
                          and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
@@ -341,7 +344,7 @@ class RankLayer:
         if self.shared_pk is None:
             return None
         T = x.shape[0]
-        goff = torch.tensor([0, T], dtype=torch.int32).pin_memory().to(self.device, non_blocking=True)
+        goff = K._single_group(T, x.device)
         pre, h, y = X.ffn_forward(x, goff, 1, None, self.shared_pk, T)
         saved.update(s_pre=pre, s_h=h, s_goff=goff)
         return y
