@@ -133,3 +133,30 @@ def test_peer_buffers_reused_before_backward_fail_loudly():
     big, _ = _blocks((128, 64), H, 2)
     with pytest.raises(ValidationError, match="peer buffers"):
         B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("ep,etp", [(2, 2), (4, 1)])
+def test_peer_exchange_pad_to_capacity_matches_nccl(ep, etp):
+    """C3 flavour on the device exchange: CF = 1 with pad-to-capacity segments
+    (static local layout) against the NCCL path."""
+    world, E, k, H, F, seed = 4, 8, 2, 128, 256, 13
+    topo = B.ParallelTopology(world_size=world, ep=ep, etp=etp, tp=etp)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=1.0)
+    weights = B.init_expert_weights(E, H, F, etp, seed, ep_size=ep, activation="swiglu")
+    blocks, ups = _blocks((256, 256, 256, 256), H, seed)
+    runs = []
+    for xch in ("nccl", "peer"):
+        wld = B.LocalWorld(world)
+        outs, ctx = B.moe_forward(blocks, weights, topo, params, wld, dtype=torch.bfloat16,
+                                  exchange=xch, pad_to_capacity=True)
+        res = B.moe_backward(ups, ctx)
+        assert all(ctx.per_rank[r]["layer"].seg > 0 for r in range(world))
+        runs.append((outs, res))
+    (o0, r0), (o1, r1) = runs
+    for r in range(world):
+        torch.testing.assert_close(o1[r], o0[r], rtol=0, atol=0)
+        assert O.rel_err(r1.input_grads[r].float().cpu().numpy(),
+                         r0.input_grads[r].float().cpu().numpy()) < 1e-2
+    for key in r0.expert_grads:
+        for a, b in zip(r0.expert_grads[key][0], r1.expert_grads[key][0]):
+            assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-3
