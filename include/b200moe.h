@@ -201,10 +201,12 @@ typedef struct {
   const int32_t* group_end; /* nullable: group g = [group_off[g], group_end[g]) (gaps allowed) */
 } b200moe_gemm_args;
 
-/* Portable SIMT implementation (fp32 parity mode and cross-check). */
+/* Portable SIMT implementation (fp32 parity mode and cross-check) of the
+ * expert GEMMs, experts.py:130-172 batched over groups. */
 B200MOE_API int b200moe_gemm_simt(const b200moe_gemm_args* args, void* stream);
 
-/* Tensor-core grouped GEMM (tcgen05 + TMEM + TMA, bf16 in, fp32 accumulate)
+/* Tensor-core grouped GEMM (tcgen05 + TMEM + TMA, bf16 in, fp32 accumulate):
+ * the expert FFN GEMMs of experts.py:130-172 batched over groups,
  * with fused expert epilogues.  Operands:
  *   A K-major  [a_rows, lda]      (row = token, K contiguous)
  *   A MN-major [a_rows, lda]      (row = K index = token, M contiguous; grouped K)
@@ -295,7 +297,7 @@ B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, 
 B200MOE_API int b200moe_ep_reduce_parts(const void* parts, int nparts, int64_t part_stride, int64_t n,
                                         void* out, void* stream);
 
-/* Elementwise expert activations in the padded row layout, rows < group_off[G].
+/* Elementwise expert activations (experts.py:23-37) in the padded row layout, rows < group_off[G].
  * SwiGLU layout: pre has 2F columns, 64-column blocks of [32 gate | 32 up]. */
 B200MOE_API int b200moe_act_fwd(const void* pre, int dtype, int act, const int32_t* group_off, int G,
                     int64_t max_rows, int64_t F, void* h, void* stream);
