@@ -91,20 +91,22 @@ __global__ void __launch_bounds__(256) permute_bwd_kernel(
     for (int64_t c = lane; c < nv; c += 32) {
       Vec16<T> v;
       v.raw = ld_nc_v4(src + c * N);
+      // all k expert rows in flight before the first use
+      Vec16<T> y[KMAX];
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s)
+        if (rows[s] >= 0) y[s].raw = ld_nc_v4(y_rows + (int64_t)rows[s] * H + c * N);
 #pragma unroll
       for (int s = 0; s < KMAX; ++s) {
         if (rows[s] < 0) continue;
-        const int64_t off = (int64_t)rows[s] * H + c * N;
-        Vec16<T> y;
-        y.raw = ld_nc_v4(y_rows + off);
         Vec16<T> o;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           const float uv = to_f32(v.v[i]);
-          dot[s] = fmaf(uv, to_f32(y.v[i]), dot[s]);
+          dot[s] = fmaf(uv, to_f32(y[s].v[i]), dot[s]);
           o.v[i] = from_f32<T>(uv * g[s]);
         }
-        st_v4(dy_rows + off, o.raw);
+        st_v4(dy_rows + (int64_t)rows[s] * H + c * N, o.raw);
       }
     }
   } else {
