@@ -31,6 +31,7 @@ def main():
                     help="comma list of ENV=VAL[;ENV=VAL] settings timed interleaved, e.g. "
                          "'B200MOE_STORE_HINT=0,B200MOE_STORE_HINT=1'")
     ap.add_argument("--routed", action="store_true", help="uneven groups from a real routing")
+    ap.add_argument("--splitk", type=int, default=4, help="K slices of the split-K dgrad1 variant")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     R, E, H, F = a.rows, a.experts, a.hidden, a.ffn
@@ -65,6 +66,17 @@ def main():
     dw1 = torch.empty((E, 2 * F, H), dtype=torch.float32, device=dev)
     N1 = 2 * F
     fl_small = 2.0 * R * H * F
+    dx32 = torch.empty((R, H), dtype=torch.float32, device=dev)
+
+    def dgrad1_split(S):
+        # experiment: split K = N1 into S slices so one slice's operand
+        # panels of an expert fit L2; fp32 partials reduce-added by TMA
+        ks = N1 // S
+        for s in range(S):
+            gemm_tc.gemm(dpre[:, s * ks:(s + 1) * ks], pk.w1p[:, s * ks:(s + 1) * ks, :], dx32,
+                         grouped_dim=0, G=E, M=0, N=H, K=ks, a_sm=N1, a_sk=1, b_sg=N1 * H, b_sk=H,
+                         b_sn=1, c_sg=0, ldc=H, group_off=goff, max_rows=R, accumulate=s > 0)
+
     runs = [
         ("fwd1 swiglu", 2 * fl_small, lambda: gemm_tc.ffn1_fused(x, pk, pre, h, goff, E, None, R)),
         ("fwd2 store", fl_small, lambda: gemm_tc.gemm(
@@ -74,6 +86,7 @@ def main():
         ("dgrad1 store", 2 * fl_small, lambda: gemm_tc.gemm(
             dpre, pk.w1p, dx, grouped_dim=0, G=E, M=0, N=H, K=N1, a_sm=N1, a_sk=1, b_sg=N1 * H,
             b_sk=H, b_sn=1, c_sg=0, ldc=H, group_off=goff, max_rows=R)),
+        ("dgrad1 splitK", 2 * fl_small, lambda: dgrad1_split(a.splitk)),
         ("wgrad2 f32", fl_small, lambda: gemm_tc.gemm(
             dy, h, dw2, grouped_dim=1, G=E, M=H, N=F, K=0, a_sm=1, a_sk=H, b_sg=0, b_sk=F, b_sn=1,
             c_sg=H * F, ldc=F, group_off=goff, max_rows=R)),
