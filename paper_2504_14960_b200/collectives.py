@@ -119,7 +119,8 @@ class LocalWorld:
 
         def runner(rank: int):
             try:
-                torch.cuda.set_device(self.device_of(rank))
+                if self.device_of(rank).type == "cuda":
+                    torch.cuda.set_device(self.device_of(rank))
                 results[rank] = program(LocalRankContext(self, rank))
             except _Aborted:
                 pass
