@@ -131,8 +131,8 @@ def test_layer_upstream_shape_mismatch():
     H, E = 64, 4
     params = B.GatingParams(w_g=B.init_gating_matrix(H, E, 0), k=2)
     weights = B.init_expert_weights(E, H, 128, 1, 0, ep_size=2)
-    blocks = B.fabricate_token_blocks(topo, 64, 2, H, 0, device="cuda")
-    ups = B.fabricate_upstream(topo, 64, 2, H, 0, device="cuda")
+    _, blocks = B.fabricate_token_blocks(topo, 64, 2, H, 0)
+    _, ups = B.fabricate_upstream(topo, 64, 2, H, 0)
     outs, ctx = B.moe_forward(blocks, weights, topo, params, B.LocalWorld(2))
     with pytest.raises(ValidationError):
         B.moe_backward([u[:-1] for u in ups], ctx)
