@@ -13,9 +13,9 @@
 //                 rows; it keeps its own push offsets and its GEMM groups
 //   dispatch      one warp per token reads x[t] once and stores it straight
 //                 into the destination ranks' receive buffers    (+ barrier)
-//   ... grouped GEMM on the local receive buffer ...             (+ barrier)
-//   combine       one warp per token pulls its k expert rows from the peers
-//                 and gate-combines them
+//   ... grouped GEMM on the local receive buffer; its epilogue stores every
+//   expert row straight back to the sender's return buffer     (+ barrier)
+//   combine       local: each sender gate-combines its returned rows
 // Split sizes never leave the device.  The barrier is a flag exchange in the
 // symmetric buffer with system-scope release/acquire and a bounded spin
 // (a missing peer traps instead of hanging the GPU).
