@@ -567,6 +567,20 @@ __device__ __forceinline__ void load_row32_bf16(const void* base, int64_t off, f
 }
 
 // ------------------------------------------------------------------ kernel
+#ifdef B200MOE_WAIT_PROF
+// perf diagnosis build only: summed clock64 cycles per role
+// [0] MMA waiting for operands (full), [1] MMA waiting for a free accumulator
+// (tempty), [2] MMA warp lifetime, [3] producer waiting for a free stage,
+// [4] epilogue waiting for an accumulator (tfull), [5] epilogue lifetime,
+// [6] SwiGLU-bwd epilogue waiting for its pre chunk, [7] MMA CTAs
+__device__ unsigned long long g_wait_prof[8];
+#define WP_T0() const long long wp_t0 = clock64()
+#define WP_ADD(var) var += clock64() - wp_t0
+#else
+#define WP_T0()
+#define WP_ADD(var)
+#endif
+
 template <bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -645,12 +659,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      long long w_empty = 0;
+      (void)w_empty;
       for (int t = cid; t < total; t += ncl) {
         const Tile tl = decode(p, prefix, t);
         const int m0 = (int)tl.m0 + BM * (int)crank;
         const int n0 = (int)tl.n0 + C::B_CTA * (int)crank;
         for (int kb = 0; kb < tl.nkb; ++kb) {
-          mbar_wait(empty_bar + 8 * stage, phase ^ 1);
+          {
+            WP_T0();
+            mbar_wait(empty_bar + 8 * stage, phase ^ 1);
+            WP_ADD(w_empty);
+          }
           const uint32_t fb = full_bar + 8 * stage;
           if (crank == 0) mbar_expect_tx(fb, C::STAGE * CG);
           const uint32_t fb_tma = CG == 2 ? (fb & PEER_BIT_MASK) : fb;
@@ -681,6 +701,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+#ifdef B200MOE_WAIT_PROF
+      atomicAdd(&g_wait_prof[3], (unsigned long long)w_empty);
+#endif
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -691,13 +714,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      long long w_full = 0, w_tempty = 0;
+      (void)w_full;
+      (void)w_tempty;
+#ifdef B200MOE_WAIT_PROF
+      const long long life0 = clock64();
+#endif
       for (int t = cid; t < total; t += ncl) {
         const Tile tl = decode(p, prefix, t);
-        mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
+        {
+          WP_T0();
+          mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
+          WP_ADD(w_tempty);
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < tl.nkb; ++kb) {
-          mbar_wait(full_bar + 8 * stage, phase);
+          {
+            WP_T0();
+            mbar_wait(full_bar + 8 * stage, phase);
+            WP_ADD(w_full);
+          }
           tc_fence_after();
           const uint32_t a_s = sA + stage * C::A_BYTES;
           const uint32_t b_s = sB + stage * C::B_BYTES;
@@ -722,6 +759,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+#ifdef B200MOE_WAIT_PROF
+      atomicAdd(&g_wait_prof[0], (unsigned long long)w_full);
+      atomicAdd(&g_wait_prof[1], (unsigned long long)w_tempty);
+      atomicAdd(&g_wait_prof[2], (unsigned long long)(clock64() - life0));
+      atomicAdd(&g_wait_prof[7], 1ull);
+#endif
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------ epilogue input
@@ -754,9 +797,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t bwd_ctr = 0;  // SwiGLU-backward staging chunks consumed (matches warp 3)
     int acc = 0;
     uint32_t acc_phase = 0;
+    long long w_tfull = 0, w_pre = 0;
+    (void)w_tfull;
+    (void)w_pre;
+#ifdef B200MOE_WAIT_PROF
+    const long long elife0 = clock64();
+#endif
     for (int t = cid; t < total; t += ncl) {
       const Tile tl = decode(p, prefix, t);
-      mbar_wait(tfull_bar + 8 * acc, acc_phase);
+      {
+        WP_T0();
+        mbar_wait(tfull_bar + 8 * acc, acc_phase);
+        WP_ADD(w_tfull);
+      }
       tc_fence_after();
       const int64_t row = tl.m0 + row_in_tile;
       const bool live = row < tl.m_end && p.debug_nostore != 1;
@@ -911,7 +964,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t sl = ctr % C::NSTG;
             uint32_t v[32];
             tmem_ld32(t_row + c * 32, v);
-            if (p.debug_nostore != 3) mbar_wait(ld_bar + 8 * sl, (ctr / C::NSTG) & 1u);
+            if (p.debug_nostore != 3) {
+              WP_T0();
+              mbar_wait(ld_bar + 8 * sl, (ctr / C::NSTG) & 1u);
+              WP_ADD(w_pre);
+            }
             const uint32_t rowp = stg + sl * STG_BYTES + (uint32_t)r * 128;
             uint4 o[8];
 #pragma unroll
@@ -1054,6 +1111,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (acc == 0) acc_phase ^= 1;
     }
     if (threadIdx.x == 128) bulk_wait_all();  // staged stores done before smem is released
+#ifdef B200MOE_WAIT_PROF
+    if (lane == 0 && warp == 4) {
+      atomicAdd(&g_wait_prof[4], (unsigned long long)w_tfull);
+      atomicAdd(&g_wait_prof[5], (unsigned long long)(clock64() - elife0));
+      atomicAdd(&g_wait_prof[6], (unsigned long long)w_pre);
+    }
+#endif
   }
   tc_fence_before();
   if (CG == 2) cluster_sync();  // the peer may still arrive on our barriers
@@ -1291,3 +1355,16 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
 }
 
 }  // namespace b200moe
+
+#ifdef B200MOE_WAIT_PROF
+// perf diagnosis build only (not declared in include/b200moe.h)
+extern "C" B200MOE_API int b200moe_debug_wait_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, b200moe::tc::g_wait_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(b200moe::tc::g_wait_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

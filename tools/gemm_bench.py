@@ -32,6 +32,8 @@ def main():
                          "'B200MOE_STORE_HINT=0,B200MOE_STORE_HINT=1'")
     ap.add_argument("--routed", action="store_true", help="uneven groups from a real routing")
     ap.add_argument("--splitk", type=int, default=4, help="K slices of the split-K dgrad1 variant")
+    ap.add_argument("--wait-prof", action="store_true",
+                    help="library built with -DB200MOE_WAIT_PROF: print per-role barrier wait shares")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     R, E, H, F = a.rows, a.experts, a.hidden, a.ffn
@@ -116,6 +118,26 @@ def main():
             samples.append((pynvml.nvmlDeviceGetClockInfo(hdl, pynvml.NVML_CLOCK_SM),
                             pynvml.nvmlDeviceGetPowerUsage(hdl) / 1000.0))
             time.sleep(0.005)
+
+    if a.wait_prof:
+        import ctypes
+
+        from paper_2504_14960_b200 import _lib
+
+        lib = _lib.load()
+        buf = (ctypes.c_ulonglong * 8)()
+        for name, fl, fn in runs:
+            fn()
+            lib.b200moe_debug_wait_prof(buf, 1)
+            fn()
+            lib.b200moe_debug_wait_prof(buf, 1)
+            w = list(buf)
+            mma_life = max(w[2], 1)
+            epi_life = max(w[5], 1)
+            print(f"{name:20s} MMA waits: operands {w[0] / mma_life:6.1%}  accumulator {w[1] / mma_life:6.1%} | "
+                  f"producer waits for a stage {w[3] / 2 / mma_life:6.1%} | epilogue waits: accumulator "
+                  f"{w[4] / epi_life:6.1%}  pre chunk {w[6] / epi_life:6.1%} | MMA CTAs {w[7]}", flush=True)
+        return
 
     tot = {v: [0.0, 0.0] for v in variants}
     for name, fl, fn in runs:
