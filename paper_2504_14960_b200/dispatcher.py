@@ -722,7 +722,8 @@ def _validate(blocks, topology, params, seq_len):
 def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingParams, world,
                 seq_len: Optional[int] = None, workers: Optional[int] = None, *, dtype=None,
                 check_finite_inputs: bool = True, shared_weights: Optional[X.ExpertWeights] = None,
-                pad_to_capacity: bool = False, exchange: Optional[str] = None):
+                pad_to_capacity: bool = False, exchange: Optional[str] = None,
+                peer_tokens: Optional[int] = None, peer_tag=0):
     """Run the MoE layer forward on every rank of ``world`` (dispatcher.py:246-384).
 
     ``world`` is a LocalWorld (all ranks in this process) or an NcclWorld
@@ -730,7 +731,10 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
     ``dtype`` selects the compute precision (torch.float32 parity mode or
     torch.bfloat16); default: the dtype of the blocks' values (fp64 -> fp32).
     ``exchange`` picks the EP all-to-all: "peer" (device-side over NVLink
-    peer memory; bf16, ETP = 1) or "nccl"; default $B200MOE_EP_EXCHANGE or "peer".
+    peer memory; bf16) or "nccl"; default $B200MOE_EP_EXCHANGE or "peer".
+    The peer buffers are allocated on first use for the largest token block
+    of that call (or ``peer_tokens`` if larger); layers whose forward and
+    backward interleave need distinct ``peer_tag`` values (their own buffers).
     """
     groups = _validate(blocks, topology, params, seq_len)
     if hasattr(world, "setup_groups"):
@@ -749,8 +753,9 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
         layer = RankLayer(params, w, topology, _rank_groups(topology, groups, rank), rank, dt, dev,
                           seq_len, check=check_finite_inputs, shared=shared_weights,
                           pad_to_capacity=pad_to_capacity, exchange=exchange,
-                          peer_tokens=max((b_.values.shape[0] for b_ in blocks if b_ is not None),
-                                          default=0))
+                          peer_tokens=max([int(peer_tokens or 0)] + [b_.values.shape[0] for b_ in blocks
+                                                                     if b_ is not None]),
+                          peer_tag=peer_tag)
         out, saved = layer.forward(ctx, b.values, b.positions)
         saved["layer"] = layer
         return out, saved

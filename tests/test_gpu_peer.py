@@ -135,6 +135,40 @@ def test_peer_buffers_reused_before_backward_fail_loudly():
         B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
 
 
+def test_peer_tags_and_headroom():
+    """Interleaved layers (fwd A, fwd B, bwd A, bwd B) on distinct peer tags
+    give the results of running them one after the other, and buffers sized
+    with ``peer_tokens`` accept a later, larger token block."""
+    E, k, H, F = 8, 2, 64, 64
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, 1), k=k)
+    weights = B.init_expert_weights(E, H, F, 1, 1, ep_size=2, activation="swiglu")
+    blocks, ups = _blocks((64, 96), H, 1)
+    world = B.LocalWorld(2)
+    o_ref, c_ref = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16)
+    r_ref = B.moe_backward(ups, c_ref)
+    world = B.LocalWorld(2)
+    o_a, c_a = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16, peer_tag="a")
+    o_b, c_b = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16, peer_tag="b")
+    r_a = B.moe_backward(ups, c_a)
+    r_b = B.moe_backward(ups, c_b)
+    for r in range(2):
+        for o in (o_a, o_b):
+            torch.testing.assert_close(o[r], o_ref[r], rtol=0, atol=0)
+        for res in (r_a, r_b):
+            torch.testing.assert_close(res.input_grads[r], r_ref.input_grads[r], rtol=0, atol=0)
+    world = B.LocalWorld(2)
+    B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16, peer_tokens=256)
+    big, ups_big = _blocks((256, 200), H, 2)
+    outs, ctx = B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
+    res = B.moe_backward(ups_big, ctx)
+    o_n, c_n = B.moe_forward(big, weights, topo, params, B.LocalWorld(2), dtype=torch.bfloat16,
+                             exchange="nccl")
+    for r in range(2):
+        torch.testing.assert_close(outs[r], o_n[r], rtol=0, atol=0)
+    assert res.input_grads[0].shape == (256, H)
+
+
 @pytest.mark.parametrize("ep,etp", [(2, 2), (4, 1)])
 def test_peer_exchange_pad_to_capacity_matches_nccl(ep, etp):
     """C3 flavour on the device exchange: CF = 1 with pad-to-capacity segments
