@@ -37,7 +37,7 @@ from . import gemm_tc
 from . import kernels as K
 from .collectives import LocalWorld, RankContext
 from .errors import ValidationError
-from .router import (DROP_FULLSEQUENCE, GATE_CODES, PRIORITY_POSITION, GatingParams,
+from .router import (DROP_FULLSEQUENCE, GATE_CODES, GatingParams,
                      RoutingDecision, capacity_limit, check_finite, gather_full_sequence_decision,
                      kept_mask, routing_from_logits)
 from .topology import (GroupSets, ParallelTopology, check_pp_consistency,

@@ -30,12 +30,6 @@ ACT_SWIGLU = "swiglu"
 ACTIVATIONS = (ACT_RELU, ACT_GELU, ACT_SWIGLU)
 
 
-def _as_np(a) -> np.ndarray:
-    if isinstance(a, torch.Tensor):
-        return a.detach().cpu().double().numpy()
-    return np.asarray(a, dtype=np.float64)
-
-
 # --------------------------------------------------------------- packing
 def swiglu_interleave_cols(w1: torch.Tensor) -> torch.Tensor:
     """[H, 2F] = [gate | up]  ->  [2F, H] rows in 64-blocks [32 gate | 32 up]."""
@@ -46,14 +40,6 @@ def swiglu_interleave_cols(w1: torch.Tensor) -> torch.Tensor:
     g = w1[:, :F].T.reshape(F // 32, 32, H)
     u = w1[:, F:].T.reshape(F // 32, 32, H)
     return torch.stack([g, u], dim=1).reshape(F2, H)
-
-
-def swiglu_deinterleave_cols_rows(pre: torch.Tensor) -> torch.Tensor:
-    """Padded-layout activations [R, 2F] interleaved -> [R, 2F] = [gate | up]."""
-    R, F2 = pre.shape
-    F = F2 // 2
-    b = pre.reshape(R, F // 32, 2, 32)
-    return torch.cat([b[:, :, 0].reshape(R, F), b[:, :, 1].reshape(R, F)], dim=1)
 
 
 @dataclass

@@ -11,8 +11,6 @@ from __future__ import annotations
 import ctypes
 import os
 
-import torch
-
 from . import _lib as L
 
 EPI_STORE, EPI_SWIGLU_FWD, EPI_SWIGLU_BWD, EPI_ACT_FWD, EPI_ACT_BWD, EPI_SCATTER = range(6)

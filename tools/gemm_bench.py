@@ -15,7 +15,6 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2504_14960_b200 as B  # noqa: E402
-from paper_2504_14960_b200 import experts as X  # noqa: E402
 from paper_2504_14960_b200 import gemm_tc  # noqa: E402
 
 
