@@ -25,7 +25,6 @@ namespace b200moe {
 namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int STAGES = 4;
 constexpr int TMEM_COLS = 512;  // 2 accumulator buffers of BN fp32 columns
 constexpr int MAX_G = 512;
 constexpr int NUM_THREADS = 256;
