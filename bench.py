@@ -396,8 +396,13 @@ def main():
         dist.all_gather(allc, cnt)
         job_wire = wire_rows([c.reshape(ep, -1).cpu().numpy() for c in allc], topo) * H * 2
         t_x = sum(m for _, m in peer_events) / 1e3
+        # launch order within a step: forward push (x), then backward push
+        # (g*u, with the dgate dots against the returned rows)
+        per_dir = {f"{d}_gbs": remote / 2 / (m / 1e3) / 1e9
+                   for d, (_, m) in zip(("forward", "backward"), peer_events)} if len(peer_events) == 2 else None
         a2a = {"busbw_gbs": remote / t_x / 1e9, "nominal_gbs": 900.0,
                "frac_nominal": remote / t_x / 1e9 / 900.0, "ms_per_step": t_x * 1e3,
+               "per_push": per_dir,
                "remote_bytes_per_step": remote, "job_wire_bytes_per_step": job_wire,
                "impl": "NVLink peer memory: ep_dispatch push kernels + GEMM scatter epilogues (peer.py)"}
     # kept (token, expert) pairs of the last step, summed over ranks; each

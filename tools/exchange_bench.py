@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--topk", type=int, default=2)
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--hot", type=int, default=0,
+                    help="bf16 8192^3 matmuls run right before each timed push (GPU in its "
+                         "power-capped GEMM clock state, as inside a layer step)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
@@ -52,11 +55,16 @@ def main():
     per_ep = plan.counts.to(torch.int64).reshape(world, -1).sum(1).cpu().tolist()
     remote = sum(c for j, c in enumerate(per_ep) if j != rank) * H * 2
 
+    hot_a = torch.randn((8192, 8192), device=dev).to(torch.bfloat16) if a.hot else None
+
     def timed(fn):
         ms = []
         for _ in range(a.reps):
+            for _ in range(a.hot):
+                hot_a @ hot_a
             px.barrier()
-            torch.cuda.synchronize()
+            if not a.hot:
+                torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()
