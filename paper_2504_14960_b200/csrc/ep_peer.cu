@@ -32,10 +32,16 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ------------------------------------------------------------------ barrier
 // flags[p] on rank r = last epoch rank p announced to r.
 __global__ void ep_barrier_kernel(const uint64_t* __restrict__ peer_base, int64_t flag_off, int me,
-                                  int ep, uint32_t epoch) {
+                                  int ep, uint32_t epoch, uint64_t timeout_ns) {
   const int p = threadIdx.x;
   __threadfence_system();  // this rank's prior writes (local and remote) before the flags
   __syncthreads();
@@ -45,9 +51,13 @@ __global__ void ep_barrier_kernel(const uint64_t* __restrict__ peer_base, int64_
   }
   if (p < ep) {
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(peer_base[me] + flag_off) + p;
-    uint64_t spins = 0;
+    // bounded by wall time (a peer that died traps this rank after
+    // $B200MOE_BARRIER_TIMEOUT_S, default 60 s, instead of hanging its GPU);
+    // the legitimate wait is one GEMM's skew between ranks
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t spins = 0;
     while ((int32_t)(ld_acquire_sys(mine) - epoch) < 0) {
-      if (++spins > (1ull << 31)) {
+      if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > timeout_ns) {
         printf("b200moe ep_barrier: rank %d timed out waiting for rank %d (epoch %u)\n", me, p, epoch);
         __trap();
       }
@@ -261,7 +271,12 @@ int ep_reduce_parts(const void* parts, int nparts, int64_t stride, int64_t n, vo
 
 int ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep, uint32_t epoch,
                cudaStream_t st) {
-  ep_barrier_kernel<<<1, 32, 0, st>>>(peer_base, flag_off, me, ep, epoch);
+  static const uint64_t timeout_ns = [] {
+    const char* e = getenv("B200MOE_BARRIER_TIMEOUT_S");
+    const double s = e ? atof(e) : 60.0;
+    return (uint64_t)((s > 0 ? s : 60.0) * 1e9);
+  }();
+  ep_barrier_kernel<<<1, 32, 0, st>>>(peer_base, flag_off, me, ep, epoch, timeout_ns);
   B200MOE_CHECK_LAUNCH("ep_barrier");
   return B200MOE_OK;
 }

@@ -194,3 +194,32 @@ def test_peer_exchange_pad_to_capacity_matches_nccl(ep, etp):
     for key in r0.expert_grads:
         for a, b in zip(r0.expert_grads[key][0], r1.expert_grads[key][0]):
             assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-3
+
+
+_ABSENT_PEER = """
+import torch
+from paper_2504_14960_b200 import kernels as K
+buf = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+base = torch.tensor([buf.data_ptr(), buf.data_ptr()], dtype=torch.int64, device="cuda")
+K.ep_barrier(base, 0, 0, 2, 1)  # rank 1 never announces epoch 1
+torch.cuda.synchronize()
+print("NO TRAP")
+"""
+
+
+def test_barrier_with_an_absent_peer_traps_instead_of_hanging():
+    """A member that never reaches the flag barrier makes the waiting rank
+    trap after $B200MOE_BARRIER_TIMEOUT_S (a launch failure the host sees)
+    rather than spin forever (run in a subprocess: the trap poisons the
+    CUDA context)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, B200MOE_BARRIER_TIMEOUT_S="2", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _ABSENT_PEER], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode != 0
+    assert "NO TRAP" not in r.stdout
+    assert "timed out waiting for rank 1" in r.stdout + r.stderr
