@@ -223,3 +223,36 @@ def test_barrier_with_an_absent_peer_traps_instead_of_hanging():
     assert r.returncode != 0
     assert "NO TRAP" not in r.stdout
     assert "timed out waiting for rank 1" in r.stdout + r.stderr
+
+
+def test_peer_exchange_with_every_token_on_one_rank():
+    """Worst-case imbalance: every token picks experts 0 and 1, both on EP
+    rank 0, so rank 0 receives all 4 ranks' rows (the receive buffers'
+    worst-case capacity) and the other ranks' GEMMs get empty groups."""
+    world, E, k, H, F, seed = 4, 8, 2, 128, 256, 21
+    topo = B.ParallelTopology(world_size=world, ep=4)
+    wg = -np.ones((H, E)) / H
+    wg[:, 0] = 2.0 / H
+    wg[:, 1] = 1.0 / H
+    params = B.GatingParams(w_g=wg, k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=4, activation="swiglu")
+    rng = np.random.default_rng(seed)
+    blocks, ups = [], []
+    for r, n in enumerate((200, 160, 96, 256)):
+        x = np.abs(rng.standard_normal((n, H))) + 0.1
+        blocks.append(B.TokenBlock(torch.as_tensor(x, dtype=torch.float32).to("cuda", torch.bfloat16),
+                                   np.arange(n) + 1000 * r))
+        ups.append(torch.as_tensor(rng.standard_normal((n, H)), dtype=torch.float32).to("cuda", torch.bfloat16))
+    o0, c0, r0 = _run("nccl", topo, params, weights, blocks, ups)
+    o1, c1, r1 = _run("peer", topo, params, weights, blocks, ups)
+    for r in range(world):
+        assert set(c1.per_rank[r]["decision"].experts.unique().tolist()) == {0, 1}
+        torch.testing.assert_close(o1[r], o0[r], rtol=0, atol=0)
+        assert O.rel_err(r1.input_grads[r].float().cpu().numpy(),
+                         r0.input_grads[r].float().cpu().numpy()) < 1e-2
+    assert int(c1.per_rank[0]["pst"]["gcount"].sum()) == 2 * (200 + 160 + 96 + 256)
+    assert int(c1.per_rank[1]["pst"]["gcount"].sum()) == 0
+    for key in r0.expert_grads:
+        for a, b in zip(r0.expert_grads[key][0] + r0.expert_grads[key][1],
+                        r1.expert_grads[key][0] + r1.expert_grads[key][1]):
+            assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-3 or float(a.abs().max()) == 0.0
