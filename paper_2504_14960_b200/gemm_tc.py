@@ -14,6 +14,7 @@ import os
 from . import _lib as L
 
 EPI_STORE, EPI_SWIGLU_FWD, EPI_SWIGLU_BWD, EPI_ACT_FWD, EPI_ACT_BWD, EPI_SCATTER = range(6)
+MAX_GROUPS = 512  # csrc/gemm_tc.cu MAX_G
 P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
 
 
@@ -55,6 +56,8 @@ def _ok8(*vals) -> bool:
 
 def supports(**kw) -> bool:
     """Whether a SIMT-style argument set maps onto the tensor-core kernel."""
+    if not 1 <= int(kw.get("G", 1)) <= MAX_GROUPS:
+        return False
     if kw["grouped_dim"] == 0:
         if kw["a_sk"] != 1:
             return False
