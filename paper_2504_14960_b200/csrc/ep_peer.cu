@@ -276,6 +276,10 @@ int ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep, uint
     const double s = e ? atof(e) : 60.0;
     return (uint64_t)((s > 0 ? s : 60.0) * 1e9);
   }();
+  if (ep < 1 || ep > 32 || me < 0 || me >= ep) {  // one lane per member
+    set_error("ep_barrier: %d members (me=%d) outside [1, 32]", ep, me);
+    return B200MOE_EUNSUPPORTED;
+  }
   ep_barrier_kernel<<<1, 32, 0, st>>>(peer_base, flag_off, me, ep, epoch, timeout_ns);
   B200MOE_CHECK_LAUNCH("ep_barrier");
   return B200MOE_OK;
@@ -290,6 +294,10 @@ int ep_counts_push(const int32_t* counts, int me, int ep, int E, const uint64_t*
 
 int ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align, int64_t cap_rows,
               int32_t* seg_off, int32_t* goff, int32_t* gcount, cudaStream_t st) {
+  if (ep < 1 || ep > 32 || etp < 1) {  // one thread per destination EP index
+    set_error("ep_layout: ep=%d outside [1, 32] (etp=%d)", ep, etp);
+    return B200MOE_EUNSUPPORTED;
+  }
   ep_layout_kernel<<<1, 32, 0, st>>>(cnt_local, me, ep, etp, L, align, cap_rows, seg_off, goff, gcount);
   B200MOE_CHECK_LAUNCH("ep_layout");
   return B200MOE_OK;

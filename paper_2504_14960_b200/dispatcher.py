@@ -331,7 +331,7 @@ class RankLayer:
         want = exchange or os.environ.get("B200MOE_EP_EXCHANGE", "peer")
         if want not in ("peer", "nccl"):
             raise ValidationError(f"unknown EP exchange {want!r}", constraint="exchange")
-        self.use_peer = (want == "peer" and not self.single and len(groups.xch) > 1
+        self.use_peer = (want == "peer" and not self.single and 1 < len(groups.xch) <= 32
                          and dtype == torch.bfloat16 and self.k <= 8 and gemm_tc.available()
                          and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
 
