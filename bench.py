@@ -434,6 +434,8 @@ def main():
             "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
             "frac": achieved / sustained if achieved else None, "traffic": traffic(a.config),
             "peak_kind": f"{src} sustained bf16 (burst {burst})",
+            "frac_of_burst": achieved / burst if achieved and burst else None,
+            "frac_of_datasheet": achieved / 2250.0 if achieved else None,  # 2.25 PF dense bf16
             "algorithmic_flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
             "gemm_share_of_step": gemm_ms / ms if ms else None,
             "launches_ms": [[n, round(m, 4)] for n, m in per_launch],
