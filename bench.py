@@ -3,8 +3,10 @@
 Workload (N=1): Mixtral-8x7B MoE layer shape -- 8 experts top-2, hidden 4096,
 expert FFN 14336 (SwiGLU), 16384 tokens per GPU, dropless, bf16 -- all 8
 experts on the one GPU (EP=1).  N>1 (torchrun, one rank per GPU): EP=N with
-16384 tokens per GPU (weak scaling); dispatch/combine are device-side pushes
-and pulls over NVLink peer memory (B200MOE_EP_EXCHANGE=nccl: NCCL all-to-all-v).
+16384 tokens per GPU (weak scaling); the EP exchange is device-side over NVLink
+peer memory: a push kernel sends token rows to the expert owners and the second
+GEMM's epilogue stores the outputs back (B200MOE_EP_EXCHANGE=nccl: NCCL
+all-to-all-v).
 
 A step = router -> dispatch -> grouped SwiGLU FFN -> combine, then the full
 backward (input, router and expert weight gradients).  Synthetic N(0,1)
