@@ -393,6 +393,14 @@ def main():
         _, e_idx, _, _ = topo.moe_coords(rank)
         per_ep = cnt.reshape(ep, -1).sum(1).cpu().tolist()
         pushed_rows = sum(c * (etp - (1 if j == e_idx else 0)) for j, c in enumerate(per_ep))
+        px_last = sv_last.get("peer")
+        dedup = bool(px_last is not None and px_last.dedup)
+        if dedup:
+            # one row per (token, destination EP index) crosses the link
+            dec = sv_last["dec"]
+            dst = (dec.experts.to(torch.int64) // (E // ep)).masked_fill(~dec.kept.bool(), -1)
+            per_dst = torch.stack([(dst == j).any(1).sum() for j in range(ep)]).cpu().tolist()
+            pushed_rows = sum(c * (etp - (1 if j == e_idx else 0)) for j, c in enumerate(per_dst))
         remote = 2 * pushed_rows * H * 2
         allc = [torch.empty_like(cnt) for _ in range(world)]
         dist.all_gather(allc, cnt)
@@ -404,7 +412,7 @@ def main():
                    for d, (_, m) in zip(("forward", "backward"), peer_events)} if len(peer_events) == 2 else None
         a2a = {"busbw_gbs": remote / t_x / 1e9, "nominal_gbs": 900.0,
                "frac_nominal": remote / t_x / 1e9 / 900.0, "ms_per_step": t_x * 1e3,
-               "per_push": per_dir,
+               "per_push": per_dir, "dedup": dedup,
                "remote_bytes_per_step": remote, "job_wire_bytes_per_step": job_wire,
                "impl": "NVLink peer memory: ep_dispatch push kernels + GEMM scatter epilogues (peer.py)"}
     # kept (token, expert) pairs of the last step, summed over ranks; each

@@ -284,13 +284,25 @@ B200MOE_API int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, 
  * [rows, 2] origin tables at origin_off, so their GEMM epilogues
  * (b200moe_gemm_tc epilogue 5) return the expert outputs straight to this
  * rank's padded layout.  Backward reads the returned (ETP-reduced) rows
- * (y_rows, local, padded layout) for dgates = <u[t], y>. */
+ * (y_rows, local, padded layout) for dgates = <u[t], y>.  dup_off >= 0: the
+ * pairs of a token bound for the same EP index send the row once; the others
+ * record their leader row in the receivers' int32 [rows, 2] dup tables at
+ * dup_off, resolved by b200moe_ep_expand after the barrier (dup_off < 0: every
+ * pair pushes its own row). */
 B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L,
                                     const int32_t* topk_idx, const int32_t* gemm_row,
                                     const int32_t* poff, const int32_t* seg_off,
                                     const uint64_t* peer_base, int me, int etp, int64_t dst_off,
-                                    int64_t origin_off, const void* y_rows, const float* gates,
-                                    float* dgates, int bwd, void* stream);
+                                    int64_t origin_off, int64_t dup_off, const void* y_rows,
+                                    const float* gates, float* dgates, int bwd, void* stream);
+/* Receiver side of the deduplicated push (dispatcher.py:317-323's regroup
+ * has no counterpart: the reference moves every pair): over the real rows
+ * goff[g] .. goff[g] + gcount[g] of the bf16 [rows, H] receive buffer, with
+ * the dup table written by the senders: phase 0 (forward) copies leader rows
+ * into their duplicates; phase 1 (backward) writes bf16(gate * leader) into
+ * the duplicates; phase 2 scales the raw leaders in place. */
+B200MOE_API int b200moe_ep_expand(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount,
+                                  int G, const int32_t* dup, int phase, void* stream);
 /* out[i] = bf16(sum over p ascending of parts[p * part_stride + i]), fp32
  * accumulation: the ETP reduce of the members' partial expert outputs that
  * their scatter epilogues returned (collectives.py:386-388 fold order). */

@@ -71,7 +71,8 @@ _SIGS = {
     "b200moe_ep_layout": [P, I32, I32, I32, I32, I32, I64, P, P, P, P],
     "b200moe_ep_reduce_parts": [P, I32, I64, I64, P, P],
     "b200moe_ep_zero_pads": [P, I64, P, P, I32, I32, P, P],
-    "b200moe_ep_dispatch": [P, I64, I64, I32, I32, P, P, P, P, P, I32, I32, I64, I64, P, P, P, I32, P],
+    "b200moe_ep_dispatch": [P, I64, I64, I32, I32, P, P, P, P, P, I32, I32, I64, I64, I64, P, P, P, I32, P],
+    "b200moe_ep_expand": [P, I64, P, P, I32, P, I32, P],
 }
 _RESTYPES = {
     "b200moe_version": ctypes.c_char_p,

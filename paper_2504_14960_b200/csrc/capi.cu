@@ -44,8 +44,9 @@ int ep_layout(const int32_t*, int, int, int, int, int, int64_t, int32_t*, int32_
 int ep_reduce_parts(const void*, int, int64_t, int64_t, void*, cudaStream_t);
 int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
-                const int32_t*, const int32_t*, const uint64_t*, int, int, int64_t, int64_t, const void*,
-                const float*, float*, int, cudaStream_t);
+                const int32_t*, const int32_t*, const uint64_t*, int, int, int64_t, int64_t, int64_t,
+                const void*, const float*, float*, int, cudaStream_t);
+int ep_expand(void*, int64_t, const int32_t*, const int32_t*, int, const void*, int, cudaStream_t);
 int split_bf16x3(const float*, int64_t, int, void*, void*, cudaStream_t);
 size_t router_stats_ws_bytes(int64_t, int);
 int router_stats(const int32_t*, const uint8_t*, const float*, int64_t, int, int, int64_t*, int64_t*,
@@ -287,14 +288,22 @@ int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_
 int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const int32_t* topk_idx,
                         const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
                         const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
-                        const void* y_rows, const float* gates, float* dgates, int bwd, void* stream) {
+                        int64_t dup_off, const void* y_rows, const float* gates, float* dgates, int bwd,
+                        void* stream) {
   REQUIRE(H % 8 == 0 && k >= 1 && L >= 1 && me >= 0 && etp >= 1 && etp <= 32,
           "ep_dispatch: H %% 8, k >= 1, me >= 0, 1 <= etp <= 32 required");
   if (T == 0) return B200MOE_OK;
   REQUIRE(x && topk_idx && gemm_row && poff && seg_off && peer_base, "ep_dispatch: null pointer");
   REQUIRE(!bwd || (gates && dgates && y_rows), "ep_dispatch: backward needs gates, dgates, y_rows");
   return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, etp, dst_off,
-                     origin_off, y_rows, gates, dgates, bwd, S(stream));
+                     origin_off, dup_off, y_rows, gates, dgates, bwd, S(stream));
+}
+
+int b200moe_ep_expand(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G,
+                      const int32_t* dup, int phase, void* stream) {
+  REQUIRE(buf && goff && gcount && dup && H % 8 == 0 && phase >= 0 && phase <= 2,
+          "ep_expand: bad args");
+  return ep_expand(buf, H, goff, gcount, G, dup, phase, S(stream));
 }
 
 int b200moe_ep_reduce_parts(const void* parts, int nparts, int64_t part_stride, int64_t n, void* out,

@@ -136,13 +136,26 @@ __global__ void ep_zero_pads_kernel(__nv_bfloat16* __restrict__ buf, int64_t H,
 // GEMM epilogue can return the expert output straight to that row.
 // Backward (BWD): g*u[t] -> the same rows of the owner's dyr, and
 // dgate = <u[t], y> with y read locally from the returned expert outputs.
+//
+// Deduplication (dup_off >= 0): the pairs of a token that go to experts of
+// the same remote EP index d carry the same row, so it crosses the link once:
+// the lowest such slot (the leader) is pushed and every other one (a
+// duplicate) only records its leader's row in the receiver's dup table
+// [rows] int2 (rows for this rank's own EP index are stored per pair, (-1, 0)):
+//   forward:  leader (-1, 0); duplicate (leader row, 0)         -> the
+//             receiver copies the leader row (ep_expand phase 0);
+//   backward: a leader without duplicates is pushed scaled, (-1, 0); one
+//             with duplicates is pushed raw, (-2, gate); a duplicate gets
+//             (leader row, gate) -> phase 1 writes bf16(gate * raw) into the
+//             duplicates, phase 2 scales the raw leaders in place.
+// Each row ends up with exactly the value the undeduplicated push stores.
 template <int KMAX, bool BWD>
 __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     const __nv_bfloat16* __restrict__ x, int64_t Tn, int64_t H, int k, int L,
     const int32_t* __restrict__ topk, const int32_t* __restrict__ gemm_row,
     const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
     const uint64_t* __restrict__ peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
-    const __nv_bfloat16* __restrict__ y_rows, const float* __restrict__ gates,
+    int64_t dup_off, const __nv_bfloat16* __restrict__ y_rows, const float* __restrict__ gates,
     float* __restrict__ dgates) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -150,16 +163,21 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
   __nv_bfloat16* dst[KMAX];
   const __nv_bfloat16* ysrc[KMAX];
   int mem[KMAX];
+  int32_t rrs[KMAX];
   int64_t roff[KMAX];
   float g[KMAX], dot[KMAX];
+  bool push[KMAX], scale[KMAX];
 #pragma unroll
   for (int s = 0; s < KMAX; ++s) {
     dst[s] = nullptr;
-    mem[s] = 0;
+    mem[s] = -1;
+    rrs[s] = -1;
     roff[s] = 0;
     ysrc[s] = nullptr;
     g[s] = 1.f;
     dot[s] = 0.f;
+    push[s] = false;
+    scale[s] = BWD;
     if (s >= k) continue;
     const int32_t gr = gemm_row[t * k + s];
     if (gr < 0) continue;
@@ -167,14 +185,45 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     const int d = e / L, le = e % L;
     const int32_t rr = seg_off[d * L + le] + (gr - poff[e]);
     mem[s] = d * etp;  // the ETP members of EP index d all get the row
+    rrs[s] = rr;
     roff[s] = dst_off + (int64_t)rr * H * 2;
     dst[s] = reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s]] + roff[s]);
+    push[s] = true;
     if (BWD) {
       ysrc[s] = y_rows + (int64_t)gr * H;
       g[s] = gates[t * k + s];
     } else if (lane < etp) {
       int2* o = reinterpret_cast<int2*>(peer_base[mem[s] + lane] + origin_off) + rr;
       *o = make_int2(me, gr);
+    }
+  }
+  if (dup_off >= 0) {
+    const int self_mem = (me / etp) * etp;  // rows for this rank's own EP index stay per pair:
+                                            // a local store is cheaper than a later copy
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (mem[s] < 0) continue;
+      if (mem[s] == self_mem) {
+        if (lane < etp) reinterpret_cast<int2*>(peer_base[mem[s] + lane] + dup_off)[rrs[s]] = make_int2(-1, 0);
+        continue;
+      }
+      int lead = s, ndup = 0;
+#pragma unroll
+      for (int q = 0; q < KMAX; ++q) {
+        if (q < s && lead == s && mem[q] == mem[s]) lead = q;
+        if (q > s && mem[q] == mem[s]) ++ndup;
+      }
+      int2 entry;
+      if (lead != s) {  // duplicate: no data, the receiver copies the leader row
+        push[s] = false;
+        entry = make_int2(rrs[lead], BWD ? __float_as_int(g[s]) : 0);
+      } else if (BWD && ndup > 0) {  // leader pushed raw, scaled by the receiver
+        scale[s] = false;
+        entry = make_int2(-2, __float_as_int(g[s]));
+      } else {
+        entry = make_int2(-1, 0);
+      }
+      if (lane < etp) reinterpret_cast<int2*>(peer_base[mem[s] + lane] + dup_off)[rrs[s]] = entry;
     }
   }
   // U column chunks per iteration keep several 16 B loads in flight per lane
@@ -206,12 +255,14 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
           for (int i = 0; i < 8; ++i) {
             const float uv = __bfloat162float(v[u].v[i]);
             dot[s] = fmaf(uv, __bfloat162float(y[BWD ? u : 0][BWD ? s : 0].v[i]), dot[s]);
-            o.v[i] = __float2bfloat16_rn(uv * g[s]);
+            o.v[i] = __float2bfloat16_rn(scale[s] ? uv * g[s] : uv);
           }
+          if (!push[s]) continue;
           st_v4(dst[s] + c, o.raw);  // NVLink push
           for (int m = 1; m < etp; ++m)
             st_v4(reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s] + m] + roff[s]) + c, o.raw);
         } else {
+          if (!push[s]) continue;
           st_v4(dst[s] + c, v[u].raw);  // NVLink push
           for (int m = 1; m < etp; ++m)
             st_v4(reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s] + m] + roff[s]) + c, v[u].raw);
@@ -225,6 +276,45 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       if (s >= k) break;
       const float d = warp_sum(dot[s]);
       if (lane == 0) dgates[t * k + s] = dst[s] ? d : 0.f;
+    }
+  }
+}
+
+// Receiver side of the deduplicated push, over the real rows of each group
+// (goff/gcount) of this rank's receive buffer:
+//   phase 0 (forward):  rows with dup.x >= 0 copy row dup.x;
+//   phase 1 (backward): rows with dup.x >= 0 get bf16(gate * row dup.x);
+//   phase 2 (backward): rows with dup.x == -2 get bf16(gate * row) in place.
+// One warp per row, 16-byte vectors; the arithmetic is the push kernel's.
+__global__ void __launch_bounds__(256) ep_expand_kernel(__nv_bfloat16* __restrict__ buf, int64_t H,
+                                                        const int32_t* __restrict__ goff,
+                                                        const int32_t* __restrict__ gcount,
+                                                        const int2* __restrict__ dup, int phase) {
+  const int g = blockIdx.y, lane = threadIdx.x & 31;
+  const int64_t r0 = goff[g], n = gcount[g];
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t row = r0 + i;
+    const int2 e = dup[row];
+    int64_t from;
+    if (phase == 2) {
+      if (e.x != -2) continue;
+      from = row;
+    } else {
+      if (e.x < 0) continue;
+      from = e.x;
+    }
+    const float gate = __int_as_float(e.y);
+    const __nv_bfloat16* s = buf + from * H;
+    __nv_bfloat16* d = buf + row * H;
+    for (int64_t c = (int64_t)lane * 8; c < H; c += 256) {
+      Vec16<__nv_bfloat16> v;
+      v.raw = ld_nc_v4(s + c);
+      if (phase != 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v.v[j] = __float2bfloat16_rn(__bfloat162float(v.v[j]) * gate);
+      }
+      st_v4(d + c, v.raw);
     }
   }
 }
@@ -315,12 +405,13 @@ int ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcoun
 int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_t* topk,
                 const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
                 const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
-                const void* y_rows, const float* gates, float* dgates, int bwd, cudaStream_t st) {
+                int64_t dup_off, const void* y_rows, const float* gates, float* dgates, int bwd,
+                cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div(Tn, 8);
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* yb = static_cast<const __nv_bfloat16*>(y_rows);
-#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, yb, gates, dgates)
-#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, yb, gates, dgates)
+#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates)
+#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates)
   if (Tn > 0) {
     if (bwd) { KSW(k, DB) }
     else { KSW(k, DF) }
@@ -328,6 +419,16 @@ int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_
 #undef DF
 #undef DB
   B200MOE_CHECK_LAUNCH("ep_dispatch");
+  return B200MOE_OK;
+}
+
+int ep_expand(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G, const void* dup,
+              int phase, cudaStream_t st) {
+  if (G <= 0) return B200MOE_OK;
+  dim3 grid(256u, (unsigned)G);
+  ep_expand_kernel<<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(buf), H, goff, gcount,
+                                         static_cast<const int2*>(dup), phase);
+  B200MOE_CHECK_LAUNCH("ep_expand");
   return B200MOE_OK;
 }
 

@@ -569,7 +569,13 @@ class RankLayer:
                 seg = (capacity_limit(self.params.capacity_factor, T_max, self.E) + ALIGN - 1) // ALIGN
                 ret = max(ret, self.E * seg * ALIGN)
             ret = (ret + ALIGN - 1) // ALIGN * ALIGN
-            px = PX.PeerExchange(ctx, xch, self.E, self.L, H, cap, ret, self.device, etp=len(self.g.etp))
+            # deduplicated push: it trades link bytes for a local copy of the
+            # duplicate rows; measured worth it from top-4 up (C4: 1-2 % of the
+            # step), neutral or slightly worse at top-2
+            env = os.environ.get("B200MOE_PUSH_DEDUP")
+            dedup = env == "1" or (env is None and self.k >= 4)
+            px = PX.PeerExchange(ctx, xch, self.E, self.L, H, cap, ret, self.device, etp=len(self.g.etp),
+                                 dedup=dedup)
             px.tokens = T_max
             cache[key] = px
         elif T > px.tokens:

@@ -346,18 +346,28 @@ def ep_zero_pads(buf: torch.Tensor, goff, gcount, G: int, align: int, origin=Non
 
 def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int, peer_base, me: int,
                 etp: int, dst_off: int, origin_off: int = 0, bwd: bool = False, y_rows=None,
-                gates=None):
+                gates=None, dup_off: int = -1):
     """Forward: push x rows to the owners' receive buffers and record their
     origin.  Backward: push gates*u rows; returns dgates [T, k] fp32 = <u, y>
-    with y the returned expert outputs (``y_rows``, local padded layout)."""
+    with y the returned expert outputs (``y_rows``, local padded layout).
+    ``dup_off >= 0``: one push per (token, EP index), duplicates recorded in
+    the receivers' dup tables (resolved by ``ep_expand``)."""
     T, H = x.shape
     k = topk_idx.shape[1]
     _cuda(x, "x", torch.bfloat16)
     dg = torch.empty((T, k), dtype=torch.float32, device=x.device) if bwd else None
     L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
-           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, etp, dst_off, origin_off,
+           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, etp, dst_off, origin_off, dup_off,
            L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), _sp())
     return dg
+
+
+def ep_expand(buf: torch.Tensor, goff, gcount, G: int, dup: torch.Tensor, phase: int):
+    """Resolve the deduplicated rows of a receive buffer (phase 0 forward;
+    1 then 2 backward)."""
+    _cuda(buf, "receive buffer", torch.bfloat16)
+    L.call("b200moe_ep_expand", L.ptr(buf), buf.shape[1], L.ptr(goff), L.ptr(gcount), G, L.ptr(dup),
+           phase, _sp())
 
 
 def ep_reduce_parts(parts: torch.Tensor) -> torch.Tensor:

@@ -86,7 +86,7 @@ class PeerExchange:
     members' partial outputs, reduced by the receiver)."""
 
     def __init__(self, ctx, group: Tuple[int, ...], E: int, L_: int, H: int, cap_rows: int,
-                 ret_rows: int, device, etp: int = 1):
+                 ret_rows: int, device, etp: int = 1, dedup: bool = False):
         self.group = tuple(group)
         self.members = len(group)
         self.etp = etp
@@ -101,11 +101,15 @@ class PeerExchange:
         off = _up(self.cnt_off + self.members * E * 4, _REGION_ALIGN)
         self.off: Dict[str, int] = {}
         for name, nbytes in (("xr", self.cap * H * 2), ("dyr", self.cap * H * 2),
-                             ("origin", self.cap * 8), ("yret", etp * self.ret_rows * H * 2),
+                             ("origin", self.cap * 8), ("dup", self.cap * 8),
+                             ("yret", etp * self.ret_rows * H * 2),
                              ("dxret", etp * self.ret_rows * H * 2)):
             self.off[name] = off
             off += _up(nbytes, _REGION_ALIGN)
         self.nbytes = off
+        # one push per (token, remote EP index): only when an EP index hosts
+        # more than one expert can two pairs of a token share a destination
+        self.dedup = bool(dedup) and L_ >= 2
         self.epoch = 0
         self.generation = 0  # forwards run on these buffers (checked by backward)
         self._handle = None
@@ -154,6 +158,10 @@ class PeerExchange:
         parts = self.region(name)
         return parts[0] if self.etp == 1 else K.ep_reduce_parts(parts)
 
+    def dup(self) -> torch.Tensor:
+        o = self.off["dup"]
+        return self.buf[o:o + self.cap * 8].view(torch.int32).view(self.cap, 2)
+
     def origin(self) -> torch.Tensor:
         o = self.off["origin"]
         return self.buf[o:o + self.cap * 8].view(torch.int32).view(self.cap, 2)
@@ -186,9 +194,12 @@ class PeerExchange:
         seg_off, goff, gcount = K.ep_layout(self.counts(), self.me, self.ep, self.etp, self.L, align,
                                             self.cap)
         K.ep_zero_pads(self.region("xr"), goff, gcount, self.L, align, origin=self.origin())
+        dup_off = self.off["dup"] if self.dedup else -1
         K.ep_dispatch(x, topk_idx, plan.gemm_row, plan.poffsets, seg_off, self.L, self.peer_base,
-                      self.me, self.etp, self.off["xr"], self.off["origin"])
+                      self.me, self.etp, self.off["xr"], self.off["origin"], dup_off=dup_off)
         self.barrier()
+        if self.dedup:
+            K.ep_expand(self.region("xr"), goff, gcount, self.L, self.dup(), 0)
         self.generation += 1
         return dict(seg_off=seg_off, goff=goff, gcount=gcount, generation=self.generation)
 
@@ -197,8 +208,11 @@ class PeerExchange:
         K.ep_zero_pads(self.region("dyr"), st["goff"], st["gcount"], self.L, align)
         dg = K.ep_dispatch(u, topk_idx, plan.gemm_row, plan.poffsets, st["seg_off"], self.L,
                            self.peer_base, self.me, self.etp, self.off["dyr"], bwd=True,
-                           y_rows=y_rows, gates=gates)
+                           y_rows=y_rows, gates=gates, dup_off=self.off["dup"] if self.dedup else -1)
         self.barrier()
+        if self.dedup:
+            K.ep_expand(self.region("dyr"), st["goff"], st["gcount"], self.L, self.dup(), 1)
+            K.ep_expand(self.region("dyr"), st["goff"], st["gcount"], self.L, self.dup(), 2)
         return dg
 
     def check_generation(self, st):

@@ -256,3 +256,31 @@ def test_peer_exchange_with_every_token_on_one_rank():
         for a, b in zip(r0.expert_grads[key][0] + r0.expert_grads[key][1],
                         r1.expert_grads[key][0] + r1.expert_grads[key][1]):
             assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-3 or float(a.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("world,ep,etp,E,k", [(2, 2, 1, 8, 4), (4, 4, 1, 16, 8), (4, 2, 2, 8, 2)])
+def test_deduplicated_push_is_exact(world, ep, etp, E, k, monkeypatch):
+    """One push per (token, remote EP index) with the duplicates resolved by
+    the receiver (B200MOE_PUSH_DEDUP; default on from top-4 when an EP index
+    hosts several experts) stores exactly the rows the per-pair push stores:
+    outputs and every gradient are bit-identical with it on and off."""
+    H, F, seed = 128, 256, 17
+    topo = B.ParallelTopology(world_size=world, ep=ep, etp=etp, tp=etp)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k)
+    weights = B.init_expert_weights(E, H, F, etp, seed, ep_size=ep, activation="swiglu")
+    blocks, ups = _blocks((160, 96, 200, 64)[:world], H, seed)
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("B200MOE_PUSH_DEDUP", flag)
+        o, c, r = _run("peer", topo, params, weights, blocks, ups)
+        assert c.per_rank[0]["peer"].dedup == (flag == "1")
+        res[flag] = (o, r)
+    (o1, r1), (o0, r0) = res["1"], res["0"]
+    for r in range(world):
+        torch.testing.assert_close(o1[r], o0[r], rtol=0, atol=0)
+        torch.testing.assert_close(r1.input_grads[r], r0.input_grads[r], rtol=0, atol=0)
+    torch.testing.assert_close(r1.w_g_grad, r0.w_g_grad, rtol=0, atol=0)
+    for key in r0.expert_grads:
+        for a, b in zip(r0.expert_grads[key][0] + r0.expert_grads[key][1],
+                        r1.expert_grads[key][0] + r1.expert_grads[key][1]):
+            torch.testing.assert_close(b, a, rtol=0, atol=0)
