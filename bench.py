@@ -184,22 +184,109 @@ def cpu_reference_sample(a, n_tokens: int, reps: int = 1, warm: int = 0):
     return n_tokens / (sum(times) / len(times)), threads, times
 
 
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def moefold_sample(a, n_ranks: int, n_tokens: int, reps: int, warm: int):
+    """Time the UNMODIFIED reference (oracle/_ref/moefold, installed from
+    /root/reference by oracle/Makefile): moe_forward + moe_backward
+    (dispatcher.py:246-510) over SimWorld(n_ranks) on ``n_tokens`` tokens in
+    total, at the config's full E/k/H/F and its EP x ETP mesh.  The reference's
+    experts are ReLU MLPs (it has no SwiGLU and no shared expert), with its
+    own init distributions (experts.py:66-81; weights built per shard directly
+    to bound host memory and init time, which is excluded).  Returns
+    (tokens/s, threads, per-step seconds, ms of weight init) or None when the
+    reference is not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "moefold")):
+        return None
+    import numpy as np
+
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import moefold as M
+
+    c = a.cfg
+    etp = c["etp"] if n_ranks >= 2 else 1
+    ep = max(1, n_ranks // etp)
+    E, k, H, F = c["E"], c["k"], c["H"], c["F"]
+    topo = M.ParallelTopology(world_size=n_ranks, ep=ep, etp=etp, tp=etp)
+    t0 = time.perf_counter()
+    params = M.GatingParams(w_g=M.init_gating_matrix(H, E, 0), k=k, capacity_factor=c["cf"])
+    rng = np.random.default_rng([0, 1])
+    b = 1.0 / np.sqrt(H)
+    L_, Fs = E // ep, F // etp
+    weights = {}
+    for e_i in range(ep):
+        ids = tuple(range(e_i * L_, (e_i + 1) * L_))
+        for t_i in range(etp):
+            weights[(e_i, t_i)] = M.ExpertWeights(
+                ids, [rng.uniform(-b, b, size=(H, Fs)) for _ in ids],
+                [rng.uniform(-b, b, size=(Fs, H)) for _ in ids], "relu", t_i, etp)
+    per = max(1, n_tokens // n_ranks)
+    xr = np.random.default_rng([0, 2])
+    blocks = [M.TokenBlock(xr.standard_normal((per, H)), np.arange(r * per, (r + 1) * per))
+              for r in range(n_ranks)]
+    ups = [np.random.default_rng([0, 3, r]).standard_normal((per, H)) for r in range(n_ranks)]
+    init_ms = (time.perf_counter() - t0) * 1e3
+    times = []
+    for i in range(warm + reps):
+        t0 = time.perf_counter()
+        world = M.SimWorld(n_ranks)
+        _, fctx = M.moe_forward(blocks, weights, topo, params, world, seq_len=per)
+        M.moe_backward(ups, fctx)
+        dt = time.perf_counter() - t0
+        if i >= warm:
+            times.append(dt)
+    return per * n_ranks / (sum(times) / len(times)), threads, times, init_ms
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = 128
-    tok_s, threads, times = cpu_reference_sample(a, n, reps=a.steps, warm=a.warmup)
-    sample = (f"{n} tokens/step at H={a.hidden} F={a.ffn} SwiGLU top-{a.topk} (k experts "
-              f"materialised), numpy float64 oracle port, {threads} threads")
+    n_ranks = int(os.environ.get("WORLD_SIZE", a.gpus))
+    # a bounded slice per step (~2-4 s of 16-core work at Mixtral width), so
+    # the default 20+5-step run ends within a few minutes
+    n_tok = 512 if a.hidden * a.ffn >= 4096 * 14336 else 1024
+    got = moefold_sample(a, n_ranks, n_tok, reps=a.steps, warm=a.warmup)
+    if got is not None:
+        tok_s, threads, times, init_ms = got
+        sample = (f"{n_tok} tokens/step over SimWorld({n_ranks}) at E{a.experts} top-{a.topk} "
+                  f"H={a.hidden} F={a.ffn} (ReLU: the reference has no SwiGLU"
+                  + (", no shared expert" if a.cfg["shared"] else "") +
+                  f"), moefold.moe_forward+moe_backward from oracle/_ref (unmodified reference, "
+                  f"numpy float64, OpenBLAS {threads} threads, {cpu_model()}); weight init "
+                  f"{init_ms:.0f} ms excluded")
+        kind = "reference"
+    else:
+        n_tok = 128
+        tok_s, threads, times = cpu_reference_sample(a, n_tok, reps=a.steps, warm=a.warmup)
+        sample = (f"{n_tok} tokens/step at H={a.hidden} F={a.ffn} SwiGLU top-{a.topk} (k experts "
+                  f"materialised), numpy float64 oracle port, {threads} threads "
+                  f"(oracle/_ref missing)")
+        kind = "port"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT,
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": 1000.0 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(a),
-        "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample, "source": "oracle/_ref/moefold" if kind == "reference"
+                         else "oracle/moe_oracle.py"},
         "e2e": {"value": tok_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -208,7 +295,7 @@ def resolve(a):
     c = dict(CONFIGS[a.config])
     if a.tokens:
         c["T"] = a.tokens
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", a.gpus))
     c["etp_eff"] = c["etp"] if world >= 2 else 1
     c["ep_eff"] = max(1, world // c["etp_eff"])
     a.experts, a.topk, a.hidden, a.ffn = c["E"], c["k"], c["H"], c["F"]
@@ -231,8 +318,25 @@ def workload_config(a):
 
 
 # --------------------------------------------------------------- GPU arm
+def relaunch(a) -> int:
+    """`bench.py --gpus N` outside torchrun: re-run this script as N ranks
+    (one process per GPU) under torch.distributed.run and return its code."""
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl == "b200":
+        sys.exit(relaunch(a))
     resolve(a)
     if a.impl == "reference":
         run_reference(a)
@@ -389,7 +493,7 @@ def main():
         # time).  Exact bytes from the plan counts (peer.wire_rows semantics).
         from paper_2504_14960_b200.peer import wire_rows
 
-        cnt = sv_last["plan"].counts.to(torch.int64)
+        cnt = sv_last["plan_dev"].counts.to(torch.int64)
         _, e_idx, _, _ = topo.moe_coords(rank)
         per_ep = cnt.reshape(ep, -1).sum(1).cpu().tolist()
         pushed_rows = sum(c * (etp - (1 if j == e_idx else 0)) for j, c in enumerate(per_ep))
@@ -418,7 +522,7 @@ def main():
     # kept (token, expert) pairs of the last step, summed over ranks; each
     # pair costs 18*H*F flop fwd+bwd with SwiGLU (6PHF + 12PHF),
     # shared expert 18*T*H*Fs; per-GPU share of the whole job
-    kept = torch.tensor([float(sv_last["plan"].counts.sum())], device=dev)
+    kept = torch.tensor([float(sv_last["plan_dev"].counts.sum())], device=dev)
     # rows this rank's expert GEMMs processed (pairs routed to its experts)
     if sv_last.get("pst") is not None:
         local_pairs = float(sv_last["pst"]["gcount"].sum())
@@ -519,10 +623,22 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:
         n = 256
-        tok_s, threads, _ = cpu_reference_sample(a, n)
-        cpu = {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{n} tokens at H={a.hidden} F={a.ffn} SwiGLU top-{a.topk}, numpy float64 "
-                         f"oracle port of moe_forward+moe_backward, {threads} threads"}
+        got = moefold_sample(a, 1, n, reps=3, warm=1)
+        if got is not None:
+            tok_s, threads, times, _ = got
+            cpu = {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "source": "oracle/_ref/moefold",
+                   "sample": f"{n} tokens, SimWorld(1), E{a.experts} top-{a.topk} H={a.hidden} "
+                             f"F={a.ffn} ReLU (the reference has no SwiGLU), unmodified "
+                             f"moefold.moe_forward+moe_backward, numpy float64, {threads} threads "
+                             f"({cpu_model()}), mean of 3 reps after 1 warm-up"}
+        else:
+            tok_s, threads, _ = cpu_reference_sample(a, n, reps=3, warm=1)
+            cpu = {"value": tok_s, "unit": UNIT, "cores": threads, "kind": "port",
+                   "source": "oracle/moe_oracle.py",
+                   "sample": f"{n} tokens at H={a.hidden} F={a.ffn} SwiGLU top-{a.topk}, numpy "
+                             f"float64 oracle port of moe_forward+moe_backward, {threads} threads, "
+                             f"mean of 3 reps after 1 warm-up"}
 
     if rank == 0:
         print(json.dumps({

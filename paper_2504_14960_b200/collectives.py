@@ -15,20 +15,30 @@ Two worlds implement it:
     performed by the last rank to arrive.  No kernel ever waits on another
     rank's kernel, so the ranks cannot deadlock the GPUs.
 
+``SimWorld`` is a LocalWorld that also keeps the reference's wire ledger
+(TrafficRecord per collective, collectives.py:81-92, 104-126): the layer's
+implicit exchanges (the peer push, the scatter epilogue, NCCL) are charged
+exactly as the reference's all_to_all_v / all_gather_v / reduce_scatter_v /
+all_reduce would charge them, from the device-resident plan counts, which are
+read only when the ledger is inspected.  ``traffic_stats`` aggregates it by
+primitive and node span (collectives.py:452-466).
+
 Both also provide the engine-level primitives ``p2p`` (a batch of row-chunk
-sends/receives) and ``gather_counts`` (all-gather of small int vectors to
-host memory; the only host synchronisation of the dispatch).
+sends/receives), ``meta`` (exchange_meta that is not part of the reference
+call sequence) and ``gather_counts`` (all-gather of small int vectors to host
+memory).
 """
 from __future__ import annotations
 
 import threading
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Any, Callable, Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
 
 from .errors import ProtocolError, ValidationError
+from .topology import ClusterModel, classify_group_span
 
 Group = Tuple[int, ...]
 _STALL_TIMEOUT_S = 120.0
@@ -183,6 +193,126 @@ class LocalWorld:
         return out
 
 
+@dataclass(frozen=True)
+class TrafficRecord:
+    """One collective's wire elements per member, group order (collectives.py:81-92)."""
+
+    epoch: int
+    seq: int
+    group: Group
+    primitive: str
+    row_width: int
+    elements_sent: Tuple[int, ...]
+
+    @property
+    def total_elements(self) -> int:
+        return int(sum(self.elements_sent))
+
+
+def _host(v):
+    if callable(v):
+        v = v()
+    if isinstance(v, torch.Tensor):
+        v = v.detach().cpu().numpy()
+    return np.asarray(v, dtype=np.int64)
+
+
+def _wire(primitive: str, group: Group, width: int, pay: Dict[int, Any]) -> Tuple[int, ...]:
+    """Elements each member puts on the wire, by the reference's rules
+    (collectives.py:341-417): self traffic is free, all_gather_v charges
+    own_rows * (n-1), reduce_scatter_v total - own partition, all_reduce the
+    ring 2(n-1)/n of the buffer."""
+    n = len(group)
+    vals = [_host(pay[r]) for r in group]
+    if primitive == "all_to_all_v":
+        return tuple(int((v.sum() - v[i]) * width) for i, v in enumerate(vals))
+    if primitive == "all_gather_v":
+        return tuple(int(v.sum()) * (n - 1) * width for v in vals)
+    if primitive == "reduce_scatter_v":
+        total = sum(int(v.sum()) for v in vals)
+        return tuple((total - int(v.sum())) * width for v in vals)
+    if primitive == "all_reduce":
+        return tuple(int(round(int(v.sum()) * 2 * (n - 1) / n)) if n > 1 else 0 for v in vals)
+    raise ValidationError(f"unknown primitive {primitive!r}", constraint="primitive")
+
+
+class SimWorld(LocalWorld):
+    """LocalWorld plus the reference's traffic ledger (collectives.py:104-126).
+
+    Every rank deposits its share of each collective through ``account`` in
+    the reference's call order; a deposit is an int, a host array, a device
+    tensor or a callable returning one, resolved only when ``ledger`` is read
+    (so the layer never synchronises for the accounting).  ``run`` may be
+    called repeatedly (forward, then backward); the ledger accumulates."""
+
+    def __init__(self, n_ranks: int, device=None, devices: Optional[Sequence] = None):
+        super().__init__(n_ranks, device=device, devices=devices)
+        self._acct_lock = threading.Lock()
+        self._acct: Dict[tuple, list] = {}
+        self._acct_seq: Dict[tuple, int] = {}
+
+    def account(self, rank: int, group: Group, primitive: Optional[str], width: int = 1,
+                payload: Any = 0) -> None:
+        """Rank ``rank``'s contribution to its next collective on ``group``;
+        ``primitive`` None stands for an exchange_meta (it takes a sequence
+        number, like the reference's rendezvous, but is not wire-accounted)."""
+        group = tuple(group)
+        _check_group(rank, group)
+        with self._acct_lock:
+            key = (self._epoch, group, rank)
+            seq = self._acct_seq.get(key, 0)
+            self._acct_seq[key] = seq + 1
+            if primitive is None:
+                return
+            slot = self._acct.setdefault((self._epoch, seq, group), [primitive, int(width), {}])
+            if slot[0] != primitive:
+                raise ProtocolError(f"{primitive}: rank {rank} disagrees with {slot[0]} on group {group} "
+                                    f"(round {seq})")
+            slot[2][rank] = payload
+
+    @property
+    def ledger(self) -> List[TrafficRecord]:
+        """Traffic records in a deterministic order (round, then group)."""
+        out = []
+        with self._acct_lock:
+            items = sorted(self._acct.items())
+        for (epoch, seq, group), (prim, width, pay) in items:
+            if len(pay) != len(group):
+                raise ProtocolError(f"{prim} on {group} (round {seq}): ranks "
+                                    f"{sorted(set(group) - set(pay))} never contributed")
+            out.append(TrafficRecord(epoch, seq, group, prim, width, _wire(prim, group, width, pay)))
+        return out
+
+
+@dataclass
+class TrafficStats:
+    """Ledger bytes aggregated by primitive and span (collectives.py:440-450)."""
+
+    by_primitive_span: Dict[Tuple[str, str], float] = field(default_factory=dict)
+
+    def bytes_for(self, primitive: str, span: Optional[str] = None) -> float:
+        if span is not None:
+            return self.by_primitive_span.get((primitive, span), 0.0)
+        return sum(v for (p, _), v in self.by_primitive_span.items() if p == primitive)
+
+    @property
+    def total_bytes(self) -> float:
+        return sum(self.by_primitive_span.values())
+
+
+def traffic_stats(world: SimWorld, cluster: Optional[ClusterModel] = None,
+                  elem_bytes: float = 8.0) -> TrafficStats:
+    """Per-primitive, per-span byte totals of ``world``'s ledger
+    (collectives.py:452-466); ``elem_bytes`` converts elements to bytes
+    (2 for the bf16 rows the B200 path actually moves)."""
+    cluster = cluster or ClusterModel()
+    stats = TrafficStats()
+    for rec in world.ledger:
+        key = (rec.primitive, classify_group_span(rec.group, cluster).span)
+        stats.by_primitive_span[key] = stats.by_primitive_span.get(key, 0.0) + rec.total_elements * elem_bytes
+    return stats
+
+
 def _enable_peer_access(devices) -> None:
     """Let kernels on every device dereference the others' memory (the peer
     exchange stores into peer buffers directly)."""
@@ -239,6 +369,7 @@ class RankContext:
             raise ProtocolError(f"all_to_all_v: rank {self.rank} supplied {len(send.counts)} counts "
                                 f"for a group of {len(group)}")
         w = send.row_width
+        self.account(group, "all_to_all_v", w, send.counts.copy())
         all_counts = self.gather_counts(group, torch.as_tensor(send.counts, dtype=torch.int64))
         me = group.index(self.rank)
         recv_counts = all_counts[:, me]
@@ -254,6 +385,7 @@ class RankContext:
         if len(send.counts) != 1:
             raise ProtocolError(f"all_gather_v: rank {self.rank} must supply a single row count")
         w = send.row_width
+        self.account(group, "all_gather_v", w, int(send.counts[0]))
         counts = self.gather_counts(group, torch.as_tensor(send.counts, dtype=torch.int64))[:, 0]
         out = torch.empty((int(counts.sum()), w), dtype=send.values.dtype, device=send.values.device)
         off = np.concatenate(([0], np.cumsum(counts)))
@@ -275,6 +407,7 @@ class RankContext:
         off = np.concatenate(([0], np.cumsum(counts)))
         me = group.index(self.rank)
         mine = counts[me]
+        self.account(group, "reduce_scatter_v", row_width, int(mine))
         parts = [torch.empty((int(mine), row_width), dtype=vals.dtype, device=vals.device)
                  for _ in group]
         sends = [(group[j], vals[off[j]:off[j + 1]]) for j in range(len(group))]
@@ -288,10 +421,26 @@ class RankContext:
     def all_reduce(self, group: Group, values: torch.Tensor, op: str = "sum") -> torch.Tensor:
         if op not in ("sum", "avg"):
             raise ValidationError(f"all_reduce op must be sum or avg, got {op!r}", constraint="op")
+        self.account(group, "all_reduce", 1, int(values.numel()))
         return self._all_reduce(group, values, op)
 
     def exchange_meta(self, group: Group, payload: Any) -> Dict[int, Any]:
+        """All-gather of host objects (collectives.py:420-423); on a SimWorld
+        it takes a ledger sequence number like the reference's rendezvous."""
+        self.account(group, None)
+        return self.meta(group, payload)
+
+    def meta(self, group: Group, payload: Any) -> Dict[int, Any]:
+        """exchange_meta for the engine's own bookkeeping (buffer agreement,
+        host barriers): not part of the reference's call sequence."""
         raise NotImplementedError
+
+    def account(self, group: Group, primitive: Optional[str], width: int = 1, payload: Any = 0) -> None:
+        """Charge this rank's share of a collective to the world's ledger
+        (SimWorld only; a no-op elsewhere).  See SimWorld.account."""
+        acct = getattr(self.world, "account", None)
+        if acct is not None:
+            acct(self.rank, group, primitive, width, payload)
 
     # engine primitives ---------------------------------------------------
     def p2p(self, group: Group, sends: List[Tuple[int, torch.Tensor]],
@@ -325,13 +474,13 @@ class LocalRankContext(RankContext):
         self.rank = rank
         self.n_ranks = world.n_ranks
 
-    def exchange_meta(self, group, payload):
+    def meta(self, group, payload):
         return self.world._rendezvous(self.rank, group, payload,
                                       lambda g, p: {r: dict(p) for r in g})
 
     def gather_counts(self, group, counts):
         host = counts.detach().to("cpu", torch.int64).numpy().copy()
-        got = self.exchange_meta(group, host)
+        got = self.meta(group, host)
         return np.stack([np.asarray(got[r]).ravel() for r in group])
 
     def p2p(self, group, sends, recvs):
@@ -415,7 +564,7 @@ class NcclRankContext(RankContext):
         self.rank = world.rank
         self.n_ranks = world.n_ranks
 
-    def exchange_meta(self, group, payload):
+    def meta(self, group, payload):
         _check_group(self.rank, group)
         objs: List[Any] = [None] * len(group)
         self.world.dist.all_gather_object(objs, payload, group=self.world.pg(group))

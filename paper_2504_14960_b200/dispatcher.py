@@ -83,8 +83,25 @@ class DispatchPlan:
     ep_size: int
     local_experts: int
     pair_gates: Optional[torch.Tensor] = None  # [n,k] fp32 device
-    recv_counts: Optional[np.ndarray] = None
+    # rows received per (EP sender, local expert) in the dispatch all-to-all
+    # (dispatcher.py:313-316): a device tensor or host array, read lazily
+    recv_src: object = None
     _host: Dict = field(default_factory=dict, repr=False)
+
+    @property
+    def recv_counts(self) -> Optional[np.ndarray]:
+        if self.recv_src is None:
+            return None
+        if "recv" not in self._host:
+            r = self.recv_src
+            r = r.detach().cpu().numpy() if isinstance(r, torch.Tensor) else np.asarray(r)
+            self._host["recv"] = r.astype(np.int64).reshape(self.ep_size, self.local_experts)
+        return self._host["recv"]
+
+    @recv_counts.setter
+    def recv_counts(self, value):
+        self.recv_src = value
+        self._host.pop("recv", None)
 
     def _offsets(self) -> np.ndarray:
         if "off" not in self._host:
@@ -389,7 +406,7 @@ class RankLayer:
             plan = K.dispatch_plan(dec.experts, dec.gates, E, cap=0, kept_in=kept_in)
         self.seg = seg
         self.align = -seg if seg else ALIGN
-        saved = {"x": x, "dec": dec, "plan": plan, "logits": logits}
+        saved = {"x": x, "dec": dec, "plan_dev": plan, "logits": logits}
         if self.single:
             # padded expert-major layout straight from the plan; group sizes stay on device
             if seg:
@@ -405,8 +422,44 @@ class RankLayer:
             out = K.combine(y, plan.gemm_row, T, gates=dec.gates, out=ys, accumulate=ys is not None)
             saved.update(xp=xp, pre=pre, h=h, y=y, goff=goff, G=E, gexp=None, R=R,
                          pair_row=plan.gemm_row)
+            self._finish_forward(ctx, saved, plan.counts)
             return out, saved
-        return self._forward_exchange(ctx, x, dec, plan, saved)
+        out, saved = self._forward_exchange(ctx, x, dec, plan, saved)
+        if "xpl" in saved:
+            recv = saved["xpl"].recv_counts
+        else:
+            px = saved["peer"]
+            te, ep_idx = px.te, px.me // px.etp
+            recv = px.counts().view(px.members, E)[te::px.etp, ep_idx * self.L:(ep_idx + 1) * self.L].clone()
+        self._finish_forward(ctx, saved, recv)
+        return out, saved
+
+    # ---- the reference-facing DispatchPlan and the wire ledger.  The layer's
+    # exchanges are charged to a SimWorld ledger in the reference's call order
+    # (dispatcher.py:309-361 forward, 425-468 backward): EP all_to_all_v,
+    # exchange_meta, [ETP all_gather_v, exchange_meta, reduce_scatter_v], EP
+    # all_to_all_v back; the counts stay on the device until the ledger is read.
+    def _finish_forward(self, ctx, saved, recv):
+        plan, dec = saved["plan_dev"], saved["dec"]
+        ep = len(self.g.ep)
+        saved["plan"] = DispatchPlan(plan, dec.n_tokens, self.k, ep, self.L, pair_gates=dec.gates,
+                                     recv_src=recv)
+        self._account(ctx, saved["plan"], meta=True)
+
+    def _account(self, ctx, dplan: "DispatchPlan", meta: bool):
+        if ctx is None or getattr(ctx.world, "account", None) is None:
+            return
+        H, ep, L_ = self.pk.hidden, dplan.ep_size, dplan.local_experts
+        cnt = dplan.dev.counts
+        ctx.account(self.g.ep, "all_to_all_v", H, lambda: cnt.view(ep, L_).sum(1))
+        if meta:
+            ctx.account(self.g.ep, None)
+        if len(self.g.etp) > 1:
+            ctx.account(self.g.etp, "all_gather_v", H, lambda: dplan.recv_counts.sum())
+            if meta:
+                ctx.account(self.g.etp, None)
+            ctx.account(self.g.etp, "reduce_scatter_v", H, lambda: dplan.recv_counts.sum())
+        ctx.account(self.g.ep, "all_to_all_v", H, lambda: dplan.recv_counts.sum(1))
 
     # ------------------------------------------------------- EP / ETP exchange
     # Rows are permuted straight into the padded per-global-expert layout,
@@ -562,7 +615,7 @@ class RankLayer:
             # buffer layout must be identical on every member: agree on the
             # largest token block once, when the buffers are created
             T_max = max(int(self.peer_tokens or 0), T)
-            T_max = max(int(v) for v in ctx.exchange_meta(xch, T_max).values())
+            T_max = max(int(v) for v in ctx.meta(xch, T_max).values())
             cap = PX.capacity_rows(len(xch), T_max, self.k, self.L, ALIGN)
             ret = T_max * self.k + self.E * (ALIGN - 1)  # this rank's padded pair layout
             if self.pad_to_capacity and not self.params.dropless:
@@ -640,12 +693,13 @@ class RankLayer:
     # ---------------------------------------------------------------- bwd
     def backward(self, ctx, u: torch.Tensor, sv: dict):
         p = self.params
-        x, dec, plan = sv["x"], sv["dec"], sv["plan"]
+        x, dec, plan = sv["x"], sv["dec"], sv["plan_dev"]
         T, H = x.shape
         u = u.to(self.device, self.dtype).contiguous()
         if tuple(u.shape) != tuple(x.shape):
             raise ValidationError(f"upstream shape {tuple(u.shape)} does not match input {tuple(x.shape)}",
                                   constraint="upstream-shape")
+        self._account(ctx, sv["plan"], meta=False)
         E = self.E
         if self.single:
             dyp, dgates = K.permute_bwd(u, sv["pair_row"], dec.gates, sv["y"], poffsets=plan.poffsets,
@@ -795,6 +849,8 @@ def moe_backward(upstream, context: ForwardContext, workers: Optional[int] = Non
         dx, dwg, dw1p, dw2p = layer.backward(ctx, u, sv)
         if topology.world_size > 1:
             dwg = ctx.all_reduce(world_group, dwg, "sum")
+        else:  # the reference all-reduces over a world of one too (a zero-byte ledger record)
+            ctx.account(world_group, "all_reduce", 1, dwg.numel())
         if len(layer.g.edp) > 1:
             flat = torch.cat([dw1p.reshape(-1), dw2p.reshape(-1)])
             red = ctx.all_reduce(layer.g.edp, flat, "sum")

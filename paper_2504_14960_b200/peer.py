@@ -26,7 +26,7 @@ receive layouts on the device.  On an NcclWorld the buffer comes from torch
 symmetric memory (one mapping per peer over NVLink) and ranks synchronise
 with a flag barrier kernel.  On a LocalWorld (ranks as threads on one GPU)
 each rank owns an ordinary device buffer, the addresses are exchanged with
-exchange_meta and the barrier is a host rendezvous after a stream
+ctx.meta and the barrier is a host rendezvous after a stream
 synchronize -- the same kernels run on both.
 """
 from __future__ import annotations
@@ -137,7 +137,7 @@ class PeerExchange:
 
     def _init_local(self, ctx):
         self.buf = torch.zeros((self.nbytes,), dtype=torch.uint8, device=self.device)
-        got = ctx.exchange_meta(self.group, self.buf.data_ptr())
+        got = ctx.meta(self.group, self.buf.data_ptr())
         self.peer_base = torch.tensor([int(got[r]) for r in self.group], dtype=torch.int64,
                                       device=self.device)
         torch.cuda.current_stream().synchronize()
@@ -183,7 +183,7 @@ class PeerExchange:
             K.ep_barrier(self.peer_base, 0, self.me, self.members, self.epoch)
         else:
             torch.cuda.current_stream().synchronize()
-            self.ctx.exchange_meta(self.group, None)
+            self.ctx.meta(self.group, None)
 
     # ------------------------------------------------------------ steps
     def forward_dispatch(self, x, topk_idx, plan, align: int):

@@ -134,6 +134,24 @@ class RoutingDecision:
     scores: Optional[torch.Tensor] = None
     gates_f64: Optional[torch.Tensor] = None
 
+    def __post_init__(self):
+        # reference callers build decisions from numpy arrays (router.py:77-109);
+        # they move to the device once here, device tensors pass through
+        dev = next((t.device for t in (self.experts, self.gates, self.kept)
+                    if isinstance(t, torch.Tensor) and t.is_cuda), None) or _device_default()
+
+        def conv(v, dtype):
+            if v is None or isinstance(v, torch.Tensor):
+                return v
+            return torch.as_tensor(np.asarray(v)).to(dev, dtype).contiguous()
+
+        self.experts = conv(self.experts, torch.int32)
+        self.gates = conv(self.gates, torch.float32)
+        self.kept = conv(self.kept, torch.bool)
+        self.scores = conv(self.scores, torch.float32)
+        if not isinstance(self.positions, torch.Tensor):
+            self.positions = torch.as_tensor(np.asarray(self.positions), dtype=torch.int64)
+
     @property
     def n_tokens(self) -> int:
         return self.experts.shape[0]

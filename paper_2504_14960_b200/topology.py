@@ -151,3 +151,43 @@ def sequence_group(topology: ParallelTopology, rank: int) -> Group:
     _, _, d, p = topology.attn_coords(rank)
     return tuple(r for r in range(topology.world_size)
                  if topology.attn_coords(r)[2:] == (d, p))
+
+
+SPAN_INTRA = "intra"
+SPAN_INTER = "inter"
+
+
+@dataclass(frozen=True)
+class ClusterModel:
+    """Node size for span classification of rank groups (topology.py:148-165).
+    Defaults describe one 8 x B200 NVLink-5 / NVSwitch node: 900 GB/s per
+    GPU per direction inside the node."""
+
+    node_size: int = 8
+    intra_bw: float = 900e9
+    inter_bw: float = 50e9
+    per_link_latency_s: float = 5e-6
+    peak_flops: float = 2250e12
+
+    def __post_init__(self):
+        if self.node_size < 1:
+            raise ValidationError("node_size must be >= 1", constraint="node_size>=1")
+        if self.intra_bw <= 0 or self.inter_bw <= 0:
+            raise ValidationError("bandwidths must be > 0", constraint="bw>0")
+        if self.inter_bw > self.intra_bw:
+            raise ValidationError("inter_bw must not exceed intra_bw", constraint="inter_bw<=intra_bw")
+
+
+@dataclass(frozen=True)
+class GroupSpan:
+    span: str  # SPAN_INTRA or SPAN_INTER
+    node_count: int
+
+
+def classify_group_span(group: Group, cluster: ClusterModel) -> GroupSpan:
+    """Whether a rank group fits in one node; ranks fill nodes in contiguous
+    blocks of node_size (topology.py:237-245)."""
+    if len(group) == 0:
+        raise ValidationError("cannot classify an empty group", constraint="group-nonempty")
+    nodes = {r // cluster.node_size for r in group}
+    return GroupSpan(SPAN_INTRA if len(nodes) == 1 else SPAN_INTER, len(nodes))

@@ -26,3 +26,12 @@ def golden():
         return cache[name]
 
     return load
+
+
+@pytest.fixture(scope="session")
+def ledgers():
+    """Per golden layer case, the reference SimWorld ledger (make_golden.py)."""
+    import json
+
+    with open(os.path.join(GOLDEN, "ledger.json")) as f:
+        return json.load(f)

@@ -200,7 +200,13 @@ def layer_cases():
                 rows[rec.primitive] += rec.total_elements // rec.row_width
         out[pre + "ledger_rows"] = np.array([rows["all_to_all_v"], rows["all_gather_v"],
                                              rows["reduce_scatter_v"]], dtype=np.int64)
+        # the whole ledger, record by record (forward epoch 1, backward epoch 2)
+        LEDGERS[pre.rstrip("_")] = [[rec.epoch, rec.seq, list(rec.group), rec.primitive, rec.row_width,
+                                     list(rec.elements_sent)] for rec in world.ledger]
     return out
+
+
+LEDGERS = {}
 
 
 def topology_cases():
@@ -235,6 +241,10 @@ def main():
     np.savez_compressed(os.path.join(OUT, "capacity_plan.npz"), **capacity_cases())
     np.savez_compressed(os.path.join(OUT, "experts.npz"), **expert_cases())
     np.savez_compressed(os.path.join(OUT, "layer.npz"), **layer_cases())
+    import json
+
+    with open(os.path.join(OUT, "ledger.json"), "w") as f:
+        json.dump(LEDGERS, f)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -155,9 +155,9 @@ def test_full_size_layer_vs_fp32_reference(name):
     assert O.rel_err(dec.gates.cpu().numpy(), r.gates) < 1e-6
     plan = O.build_dispatch_plan(r.experts, r.gates, r.kept, 1, L.c["E"])
     P = plan.permutation.size
-    assert int(sv["plan"].offsets[-1]) == P
-    np.testing.assert_array_equal(sv["plan"].perm[:P].cpu().numpy(), plan.permutation)
-    np.testing.assert_array_equal(sv["plan"].counts.cpu().numpy(), plan.send_counts.reshape(-1))
+    assert int(sv["plan_dev"].offsets[-1]) == P
+    np.testing.assert_array_equal(sv["plan_dev"].perm[:P].cpu().numpy(), plan.permutation)
+    np.testing.assert_array_equal(sv["plan_dev"].counts.cpu().numpy(), plan.send_counts.reshape(-1))
     # floats against the fp32 restatement
     ro, rdx, rdwg, rdw1, rdw2 = reference_layer(L, dec, L.u)
     errs = {"out": _rel(out.float(), ro), "dx": _rel(dx.float(), rdx), "dw_g": _rel(dwg.float(), rdwg),

@@ -133,19 +133,33 @@ def _run_layer_case(d, c, dtype, act=None):
     x, u = d[c + "_x"], d[c + "_u"]
     positions = [d[c + f"_positions{r}"] for r in range(w)]
     blocks = [B.TokenBlock(t(x[p], dtype), p) for p in positions]
-    world = B.LocalWorld(w)
+    world = B.SimWorld(w)
     outs, ctx = B.moe_forward(blocks, weights, topo, params, world, seq_len=seq)
     res = B.moe_backward([t(u[p], dtype) for p in positions], ctx)
     return meta, params, positions, outs, ctx, res
 
 
-def test_layer_cases_match_reference_fp32(golden):
+def _check_ledger(golden_ledgers, c, ctx):
+    """The SimWorld wire ledger equals the reference's record for record
+    (epoch, round, group, primitive, row width, elements per member)."""
+    got = [[r.epoch, r.seq, list(r.group), r.primitive, r.row_width, list(r.elements_sent)]
+           for r in ctx.world.ledger]
+    assert got == golden_ledgers[c], c
+    # recv_counts filled after the exchange (dispatcher.py:313-316): pairs sent == received
+    w = len(ctx.per_rank)
+    sent = sum(int(ctx.per_rank[r]["plan"].send_counts.sum()) for r in range(w))
+    recv = sum(int(ctx.per_rank[r]["plan"].recv_counts.sum()) for r in range(w))
+    assert sent == recv, c
+
+
+def test_layer_cases_match_reference_fp32(golden, ledgers):
     """moe_forward/moe_backward (fp32 mode) on every golden topology, ranks
     simulated on one GPU, vs the reference's own outputs and gradients."""
     d = golden("layer")
     tol = FP32_TOL
     for c in _cases(d, "l"):
         meta, params, positions, outs, ctx, res = _run_layer_case(d, c, torch.float32)
+        _check_ledger(ledgers, c, ctx)
         w, E, k = meta[0], meta[5], meta[6]
         x = d[c + "_x"]
         y = np.zeros_like(x)
@@ -172,12 +186,13 @@ def test_layer_cases_match_reference_fp32(golden):
             assert O.rel_err(g2.cpu().numpy(), d[c + "_dw2"][e]) < tol, (c, e)
 
 
-def test_layer_cases_bf16_vs_oracle_with_gpu_logits(golden):
+def test_layer_cases_bf16_vs_oracle_with_gpu_logits(golden, ledgers):
     """bf16 mode on the golden topologies vs the pinned oracle fed the GPU's own
     logits and the bf16-rounded inputs (routing bit-exact, values 2e-2)."""
     d = golden("layer")
     for c in _cases(d, "l"):
         meta, params, positions, outs, ctx, res = _run_layer_case(d, c, torch.bfloat16, "gelu")
+        _check_ledger(ledgers, c, ctx)
         w, E, k, seq, full = meta[0], meta[5], meta[6], meta[9], meta[12]
         cf = float(d[c + "_cf"][0])
         cfg = O.LayerConfig(k=k, gate_fn=params.gate_fn, renormalize=params.renormalize_topk,
@@ -237,8 +252,8 @@ def test_c1_shape_layer_vs_oracle(act, dtype, tol, cf):
         # relu' as the GPU saw it (pre within rounding of 0 may flip sign)
         sv = ctx.per_rank[0]
         pre = sv["pre"].float().cpu().numpy()
-        poff = sv["plan"].poffsets.cpu().numpy()
-        cnt = sv["plan"].counts.cpu().numpy()
+        poff = sv["plan_dev"].poffsets.cpu().numpy()
+        cnt = sv["plan_dev"].counts.cpu().numpy()
         masks = {e: pre[poff[e]:poff[e] + cnt[e]] > 0 for e in range(E)}
     g = O.layer_backward(uin, st, experts, cfg, w_g=wg, relu_masks=masks)
     dec = ctx.per_rank[0]["decision"]

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,memory.total --format=csv > gpurun_out/r2a_smi.txt; nproc >> gpurun_out/r2a_smi.txt; free -g >> gpurun_out/r2a_smi.txt
+timeout 300 python tools/router_bench.py --config c2 > gpurun_out/r2a_router_c2.log 2>&1
+timeout 300 python tools/router_bench.py --config c4 > gpurun_out/r2a_router_c4.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2a_pytest.log 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/r2a_bench.log 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2a_ref.log 2>&1
+tail -3 gpurun_out/r2a_pytest.log
