@@ -68,10 +68,26 @@ B200MOE_API int b200moe_router_logits(const void* x, int x_dtype, const float* w
 /* scores = softmax/sigmoid(logits) (fp64 internally, stored fp32),
  * topk_idx[T,k] best first with ties to the lower expert id, gates[T,k] raw
  * or renormalised over the k winners.  gates_f64 (nullable) receives the
- * float64 gates, used as the probability-priority key.  -- router.py:112-162 */
+ * float64 gates, used as the probability-priority key.  A token with a
+ * non-finite logit sets bit 0 of *status (nullable) and gets the placeholder
+ * routing 0..k-1 (the host raises NumericError, router.py:141-144).
+ *                                                       -- router.py:112-162 */
 B200MOE_API int b200moe_router_topk(const float* logits, int64_t T, int E, int k, int gate_fn, int renorm,
                         float* scores, int32_t* topk_idx, float* gates, double* gates_f64,
-                        void* stream);
+                        int32_t* status, void* stream);
+
+/* Fused router forward for bf16 tokens on the tensor cores: logits = x @ W_g
+ * (tcgen05, x read once by TMA), then the b200moe_router_topk arithmetic in
+ * the same kernel for E <= 32 (a second launch for 32 < E <= 64).  w_parts
+ * is bf16 [NP, H], rows p*EP + e holding the exact three-way split
+ * hi + mid + lo of W_g^T (EP = E rounded up to 8/16/32/64, NP =
+ * b200moe_router_fwd_tc_np(E), zero padded).  status is required.
+ *                                        -- router.py:141-162 (compute_gates) */
+B200MOE_API int b200moe_router_fwd_tc_np(int E);
+B200MOE_API int b200moe_router_fwd_tc(const void* x, int64_t T, int64_t H, const void* w_parts, int E, int k,
+                                      int gate_fn, int renorm, float* logits, float* scores,
+                                      int32_t* topk_idx, float* gates, double* gates_f64, int32_t* status,
+                                      void* stream);
 
 /* Workspace bytes needed by b200moe_dispatch_plan for T tokens, E experts. */
 B200MOE_API size_t b200moe_dispatch_plan_ws(int64_t T, int E);
@@ -258,9 +274,13 @@ B200MOE_API int b200moe_gemm_tc(const b200moe_tc_gemm_args* args, void* stream);
  * member; regions are addressed by byte offsets.  No call synchronises the
  * host. */
 
-/* row `me` of every member's [members, E] int32 count matrix := counts[E] */
+/* row `me` of every member's [members, E] int32 count matrix := counts[E];
+ * when *status (nullable) is non-zero -- this rank's step already failed --
+ * an abort marker (-1 entries) instead, so that the whole group fails the
+ * step together (every rank still completes its barriers and raises). */
 B200MOE_API int b200moe_ep_counts_push(const int32_t* counts, int me, int members, int E,
-                                       const uint64_t* peer_base, int64_t cnt_off, void* stream);
+                                       const uint64_t* peer_base, int64_t cnt_off, const int32_t* status,
+                                       void* stream);
 /* cross-GPU barrier over the members: flag exchange at flag_off with
  * system-scope release/acquire; epoch must increase by one per call (bounded
  * spin, traps if a peer never arrives). */
@@ -270,10 +290,11 @@ B200MOE_API int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, 
  * (me, le) in EP index d's receive buffers -- the same on its etp members),
  * goff[L+1] / gcount[L] (this rank's GEMM groups: one per local expert,
  * senders contiguous in member order, the group padded to align rows).
+ * Marker rows count as empty and set bit 1 of *status (nullable).
  * Traps if a layout exceeds cap_rows. */
 B200MOE_API int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align,
                                   int64_t cap_rows, int32_t* seg_off, int32_t* goff, int32_t* gcount,
-                                  void* stream);
+                                  int32_t* status, void* stream);
 /* zero the pad rows of this rank's receive buffer (bf16 [rows, H]); with
  * origin (int32 [rows, 2]) also mark them "no origin" for the scatter epilogue */
 B200MOE_API int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount,
@@ -288,13 +309,15 @@ B200MOE_API int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, 
  * pairs of a token bound for the same EP index send the row once; the others
  * record their leader row in the receivers' int32 [rows, 2] dup tables at
  * dup_off, resolved by b200moe_ep_expand after the barrier (dup_off < 0: every
- * pair pushes its own row). */
+ * pair pushes its own row).  Nothing is pushed when *status (nullable) is
+ * non-zero (a failed step). */
 B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L,
                                     const int32_t* topk_idx, const int32_t* gemm_row,
                                     const int32_t* poff, const int32_t* seg_off,
                                     const uint64_t* peer_base, int me, int etp, int64_t dst_off,
                                     int64_t origin_off, int64_t dup_off, const void* y_rows,
-                                    const float* gates, float* dgates, int bwd, void* stream);
+                                    const float* gates, float* dgates, int bwd, const int32_t* status,
+                                    void* stream);
 /* Receiver side of the deduplicated push (dispatcher.py:317-323's regroup
  * has no counterpart: the reference moves every pair): over the real rows
  * goff[g] .. goff[g] + gcount[g] of the bf16 [rows, H] receive buffer, with

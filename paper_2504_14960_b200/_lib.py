@@ -48,7 +48,9 @@ _SIGS = {
     "b200moe_device_check": [],
     "b200moe_enable_peer_access": [I32],
     "b200moe_router_logits": [P, I32, P, I64, I64, I32, P, P],
-    "b200moe_router_topk": [P, I64, I32, I32, I32, I32, P, P, P, P, P],
+    "b200moe_router_topk": [P, I64, I32, I32, I32, I32, P, P, P, P, P, P],
+    "b200moe_router_fwd_tc_np": [I32],
+    "b200moe_router_fwd_tc": [P, I64, I64, P, I32, I32, I32, I32, P, P, P, P, P, P, P],
     "b200moe_dispatch_plan_ws": [I64, I32],
     "b200moe_dispatch_plan": [P, P, P, P, I64, I32, I32, I64, I32, P, SZ, P, P, P, P, P, P, P, P, P],
     "b200moe_capacity_by_gate": [P, P, P, P, I64, I32, I32, I64, P, P],
@@ -66,12 +68,12 @@ _SIGS = {
     "b200moe_router_stats_ws": [I64, I32],
     "b200moe_router_stats": [P, P, P, I64, I32, I32, P, P, P, P, SZ, P],
     "b200moe_sum_parts": [P, I64, I64, I32, P, P],
-    "b200moe_ep_counts_push": [P, I32, I32, I32, P, I64, P],
+    "b200moe_ep_counts_push": [P, I32, I32, I32, P, I64, P, P],
     "b200moe_ep_barrier": [P, I64, I32, I32, ctypes.c_uint32, P],
-    "b200moe_ep_layout": [P, I32, I32, I32, I32, I32, I64, P, P, P, P],
+    "b200moe_ep_layout": [P, I32, I32, I32, I32, I32, I64, P, P, P, P, P],
     "b200moe_ep_reduce_parts": [P, I32, I64, I64, P, P],
     "b200moe_ep_zero_pads": [P, I64, P, P, I32, I32, P, P],
-    "b200moe_ep_dispatch": [P, I64, I64, I32, I32, P, P, P, P, P, I32, I32, I64, I64, I64, P, P, P, I32, P],
+    "b200moe_ep_dispatch": [P, I64, I64, I32, I32, P, P, P, P, P, I32, I32, I64, I64, I64, P, P, P, I32, P, P],
     "b200moe_ep_expand": [P, I64, P, P, I32, P, I32, P],
 }
 _RESTYPES = {
@@ -128,6 +130,7 @@ _LAUNCHES = {"b200moe_dispatch_plan": 3}
 _LAUNCHES["b200moe_router_wgrad"] = 2
 _LAUNCHES["b200moe_router_stats"] = 2
 _NO_LAUNCH = {"b200moe_version", "b200moe_last_error", "b200moe_device_check", "b200moe_enable_peer_access",
+              "b200moe_router_fwd_tc_np",
               "b200moe_dispatch_plan_ws", "b200moe_router_wgrad_ws", "b200moe_router_stats_ws"}
 _launches = 0
 
@@ -196,6 +199,8 @@ def call(name: str, *args) -> None:
         n = _LAUNCHES.get(name, 1)
         if name in ("b200moe_permute", "b200moe_permute_bwd") and args[-5]:
             n += 1  # alignment-padding zero kernel
+        if name == "b200moe_router_fwd_tc" and args[4] > 32:
+            n += 1  # the warp-per-token top-k follows the tensor-core logits
         note_launches(n)
 
 

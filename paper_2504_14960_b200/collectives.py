@@ -93,9 +93,16 @@ class _Slot:
 
 class LocalWorld:
     """N ranks as threads of one process (SimWorld analogue), on one device
-    or -- with ``devices`` -- one device per rank."""
+    or -- with ``devices`` -- one device per rank.
 
-    def __init__(self, n_ranks: int, device=None, devices: Optional[Sequence] = None):
+    ``device_barrier``: every rank issues its work on its own CUDA stream and
+    the peer exchange synchronises ranks with the device-side flag barrier
+    (ep_barrier_kernel) instead of a host rendezvous -- the production
+    (NcclWorld) synchronisation path, runnable on a single GPU.  Host-side
+    collectives then synchronise the ranks' streams around every exchange."""
+
+    def __init__(self, n_ranks: int, device=None, devices: Optional[Sequence] = None,
+                 device_barrier: bool = False):
         if n_ranks < 1:
             raise ValidationError("n_ranks must be >= 1", constraint="n_ranks>=1")
         self.n_ranks = n_ranks
@@ -117,6 +124,10 @@ class LocalWorld:
         self._seq: Dict[tuple, int] = {}
         self._epoch = 0
         self._failure: Optional[BaseException] = None
+        self.device_barrier = bool(device_barrier)
+        self._streams = None
+        if self.device_barrier and self.device.type == "cuda":
+            self._streams = [torch.cuda.Stream(device=self.device_of(r)) for r in range(n_ranks)]
 
     def run(self, program: Callable[["RankContext"], Any], *, workers: Optional[int] = None) -> List[Any]:
         with self._cond:
@@ -131,7 +142,14 @@ class LocalWorld:
             try:
                 if self.device_of(rank).type == "cuda":
                     torch.cuda.set_device(self.device_of(rank))
-                results[rank] = program(LocalRankContext(self, rank))
+                if self._streams is not None:
+                    s = self._streams[rank]
+                    s.wait_stream(torch.cuda.current_stream())  # inputs made on the caller's stream
+                    with torch.cuda.stream(s):
+                        results[rank] = program(LocalRankContext(self, rank))
+                    torch.cuda.current_stream().wait_stream(s)
+                else:
+                    results[rank] = program(LocalRankContext(self, rank))
             except _Aborted:
                 pass
             except BaseException as exc:  # noqa: BLE001
@@ -161,6 +179,10 @@ class LocalWorld:
     def _rendezvous(self, rank: int, group: Group, payload: Any,
                     compute: Callable[[Group, Dict[int, Any]], Dict[int, Any]]) -> Any:
         _check_group(rank, group)
+        if self._streams is not None:
+            # ranks run on their own streams: a payload (or a device result
+            # computed by the last arrival) is complete before it crosses over
+            torch.cuda.current_stream().synchronize()
         with self._cond:
             if self._failure is not None:
                 raise _Aborted()
@@ -172,6 +194,8 @@ class LocalWorld:
             slot.payloads[rank] = payload
             if len(slot.payloads) == len(group):
                 slot.results = compute(group, slot.payloads)
+                if self._streams is not None:
+                    torch.cuda.current_stream().synchronize()
                 slot.remaining = len(group)
                 slot.payloads = {}
                 self._cond.notify_all()

@@ -19,7 +19,10 @@ void set_error(const char* fmt, ...) {
 // kernels (defined in the other translation units)
 int router_logits(const void*, int, const float*, int64_t, int64_t, int, float*, cudaStream_t);
 int router_topk(const float*, int64_t, int, int, int, int, float*, int32_t*, float*, double*,
-                cudaStream_t);
+                int32_t*, cudaStream_t);
+int router_fwd_tc_np(int);
+int router_fwd_tc(const void*, int64_t, int64_t, const void*, int, int, int, int, float*, float*,
+                  int32_t*, float*, double*, int32_t*, cudaStream_t);
 size_t plan_ws_bytes(int64_t, int);
 int dispatch_plan(const int32_t*, const float*, const uint8_t*, const int32_t*, int64_t, int, int,
                   int64_t, int, void*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*,
@@ -39,13 +42,14 @@ int combine(const void*, int, int64_t, int64_t, int, const int32_t*, const float
 int gemm_simt(const b200moe_gemm_args*, cudaStream_t);
 int gemm_tc(const b200moe_tc_gemm_args*, cudaStream_t);
 int ep_barrier(const uint64_t*, int64_t, int, int, uint32_t, cudaStream_t);
-int ep_counts_push(const int32_t*, int, int, int, const uint64_t*, int64_t, cudaStream_t);
-int ep_layout(const int32_t*, int, int, int, int, int, int64_t, int32_t*, int32_t*, int32_t*, cudaStream_t);
+int ep_counts_push(const int32_t*, int, int, int, const uint64_t*, int64_t, const int32_t*, cudaStream_t);
+int ep_layout(const int32_t*, int, int, int, int, int, int64_t, int32_t*, int32_t*, int32_t*, int32_t*,
+              cudaStream_t);
 int ep_reduce_parts(const void*, int, int64_t, int64_t, void*, cudaStream_t);
 int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
                 const int32_t*, const int32_t*, const uint64_t*, int, int, int64_t, int64_t, int64_t,
-                const void*, const float*, float*, int, cudaStream_t);
+                const void*, const float*, float*, int, const int32_t*, cudaStream_t);
 int ep_expand(void*, int64_t, const int32_t*, const int32_t*, int, const void*, int, cudaStream_t);
 int split_bf16x3(const float*, int64_t, int, void*, void*, cudaStream_t);
 size_t router_stats_ws_bytes(int64_t, int);
@@ -104,15 +108,35 @@ int b200moe_router_logits(const void* x, int x_dtype, const float* w_g, int64_t 
 
 int b200moe_router_topk(const float* logits, int64_t T, int E, int k, int gate_fn, int renorm,
                         float* scores, int32_t* topk_idx, float* gates, double* gates_f64,
-                        void* stream) {
+                        int32_t* status, void* stream) {
   REQUIRE(E >= 1 && k >= 1 && k <= E, "1<=k<=E violated (k=%d, E=%d)", k, E);
   REQUIRE(k <= 32, "router_topk: k=%d > 32 unsupported", k);
   REQUIRE(gate_fn == B200MOE_GATE_SOFTMAX || gate_fn == B200MOE_GATE_SIGMOID,
           "unknown gate_fn %d", gate_fn);
   if (T == 0) return B200MOE_OK;
   REQUIRE(logits && scores && topk_idx && gates, "router_topk: null pointer");
-  return router_topk(logits, T, E, k, gate_fn, renorm, scores, topk_idx, gates, gates_f64,
+  return router_topk(logits, T, E, k, gate_fn, renorm, scores, topk_idx, gates, gates_f64, status,
                      S(stream));
+}
+
+int b200moe_router_fwd_tc_np(int E) { return router_fwd_tc_np(E); }
+
+int b200moe_router_fwd_tc(const void* x, int64_t T, int64_t H, const void* w_parts, int E, int k,
+                          int gate_fn, int renorm, float* logits, float* scores, int32_t* topk_idx,
+                          float* gates, double* gates_f64, int32_t* status, void* stream) {
+  REQUIRE(E >= 1 && k >= 1 && k <= E, "1<=k<=E violated (k=%d, E=%d)", k, E);
+  REQUIRE(router_fwd_tc_np(E) > 0, "router_fwd_tc: E=%d > 64 unsupported", E);
+  REQUIRE(k <= 32, "router_fwd_tc: k=%d > 32 unsupported", k);
+  REQUIRE(gate_fn == B200MOE_GATE_SOFTMAX || gate_fn == B200MOE_GATE_SIGMOID,
+          "unknown gate_fn %d", gate_fn);
+  REQUIRE(T >= 0 && H >= 64 && H % 8 == 0, "router_fwd_tc: bad shape T=%lld H=%lld", (long long)T,
+          (long long)H);
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(x && w_parts && logits && scores && topk_idx && gates && status,
+          "router_fwd_tc: null pointer");
+  REQUIRE(((uintptr_t)x & 15) == 0 && ((uintptr_t)w_parts & 15) == 0, "router_fwd_tc: misaligned operand");
+  return router_fwd_tc(x, T, H, w_parts, E, k, gate_fn, renorm, logits, scores, topk_idx, gates,
+                       gates_f64, status, S(stream));
 }
 
 int b200moe_enable_peer_access(int peer) {
@@ -259,10 +283,10 @@ int b200moe_gemm_tc(const b200moe_tc_gemm_args* a, void* stream) {
 }
 
 int b200moe_ep_counts_push(const int32_t* counts, int me, int ep, int E, const uint64_t* peer_base,
-                           int64_t cnt_off, void* stream) {
+                           int64_t cnt_off, const int32_t* status, void* stream) {
   REQUIRE(counts && peer_base && ep >= 1 && ep <= 32 && me >= 0 && me < ep && E >= 1,
           "ep_counts_push: bad args");
-  return ep_counts_push(counts, me, ep, E, peer_base, cnt_off, S(stream));
+  return ep_counts_push(counts, me, ep, E, peer_base, cnt_off, status, S(stream));
 }
 
 int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep, uint32_t epoch,
@@ -272,11 +296,11 @@ int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int 
 }
 
 int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align, int64_t cap_rows,
-                      int32_t* seg_off, int32_t* goff, int32_t* gcount, void* stream) {
+                      int32_t* seg_off, int32_t* goff, int32_t* gcount, int32_t* status, void* stream) {
   REQUIRE(cnt_local && seg_off && goff && gcount && ep >= 1 && etp >= 1 && ep * etp <= 32 && L >= 1 &&
               align >= 1 && me >= 0 && me < ep * etp && cap_rows >= 0 && cap_rows < (1ll << 31),
           "ep_layout: bad args");
-  return ep_layout(cnt_local, me, ep, etp, L, align, cap_rows, seg_off, goff, gcount, S(stream));
+  return ep_layout(cnt_local, me, ep, etp, L, align, cap_rows, seg_off, goff, gcount, status, S(stream));
 }
 
 int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G,
@@ -289,14 +313,14 @@ int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const
                         const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
                         const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
                         int64_t dup_off, const void* y_rows, const float* gates, float* dgates, int bwd,
-                        void* stream) {
+                        const int32_t* status, void* stream) {
   REQUIRE(H % 8 == 0 && k >= 1 && L >= 1 && me >= 0 && etp >= 1 && etp <= 32,
           "ep_dispatch: H %% 8, k >= 1, me >= 0, 1 <= etp <= 32 required");
   if (T == 0) return B200MOE_OK;
   REQUIRE(x && topk_idx && gemm_row && poff && seg_off && peer_base, "ep_dispatch: null pointer");
   REQUIRE(!bwd || (gates && dgates && y_rows), "ep_dispatch: backward needs gates, dgates, y_rows");
   return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, etp, dst_off,
-                     origin_off, dup_off, y_rows, gates, dgates, bwd, S(stream));
+                     origin_off, dup_off, y_rows, gates, dgates, bwd, status, S(stream));
 }
 
 int b200moe_ep_expand(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G,

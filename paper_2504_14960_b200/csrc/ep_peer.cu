@@ -68,12 +68,18 @@ __global__ void ep_barrier_kernel(const uint64_t* __restrict__ peer_base, int64_
 }
 
 // ------------------------------------------------------------------ counts
+// A rank whose step already failed (status != 0: non-finite router input,
+// oversized block) pushes an abort marker (-1 in every entry) instead of its
+// counts; every member then lays out the step without it and skips its
+// pushes, so all ranks finish the step's barriers and raise on the host.
 __global__ void ep_counts_push_kernel(const int32_t* __restrict__ counts, int me, int ep, int E,
-                                      const uint64_t* __restrict__ peer_base, int64_t cnt_off) {
+                                      const uint64_t* __restrict__ peer_base, int64_t cnt_off,
+                                      const int32_t* __restrict__ status) {
+  const bool abort = status && *status != 0;
   for (int i = threadIdx.x; i < ep * E; i += blockDim.x) {
     const int p = i / E, e = i % E;
     int32_t* dst = reinterpret_cast<int32_t*>(peer_base[p] + cnt_off) + me * E + e;
-    *dst = counts[e];
+    *dst = abort ? -1 : counts[e];
   }
 }
 
@@ -91,17 +97,25 @@ __global__ void ep_counts_push_kernel(const int32_t* __restrict__ counts, int me
 // goff[L] = end.  A layout beyond cap_rows (the buffer size) traps.
 __global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int me, int ep, int etp, int L,
                                  int align, int64_t cap_rows, int32_t* __restrict__ seg_off,
-                                 int32_t* __restrict__ goff, int32_t* __restrict__ gcount) {
+                                 int32_t* __restrict__ goff, int32_t* __restrict__ gcount,
+                                 int32_t* __restrict__ status) {
   const int E = ep * L, nmem = ep * etp;
   const int d = threadIdx.x;  // one thread per destination EP index
   if (d >= ep) return;
   const bool mine = d == me / etp;
+  if (d == 0 && status) {  // an aborted member (marker row, see counts_push) fails the step
+    for (int s = 0; s < nmem; ++s)
+      if (cnt[s * E] < 0) {
+        atomicOr(status, 2);
+        break;
+      }
+  }
   int64_t run = 0;
   for (int le = 0; le < L; ++le) {
     int64_t tot = 0;
     for (int s = 0; s < nmem; ++s) {
       if (s == me) seg_off[d * L + le] = (int32_t)(run + tot);
-      tot += cnt[s * E + d * L + le];
+      tot += max(cnt[s * E + d * L + le], 0);
     }
     if (mine) {
       goff[le] = (int32_t)run;
@@ -156,10 +170,11 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
     const uint64_t* __restrict__ peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
     int64_t dup_off, const __nv_bfloat16* __restrict__ y_rows, const float* __restrict__ gates,
-    float* __restrict__ dgates) {
+    float* __restrict__ dgates, const int32_t* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= Tn) return;
+  if (status && *status != 0) return;  // failed step: nothing is pushed (see counts_push)
   __nv_bfloat16* dst[KMAX];
   const __nv_bfloat16* ysrc[KMAX];
   int mem[KMAX];
@@ -376,19 +391,19 @@ int ep_barrier(const uint64_t* peer_base, int64_t flag_off, int me, int ep, uint
 }
 
 int ep_counts_push(const int32_t* counts, int me, int ep, int E, const uint64_t* peer_base,
-                   int64_t cnt_off, cudaStream_t st) {
-  ep_counts_push_kernel<<<1, 256, 0, st>>>(counts, me, ep, E, peer_base, cnt_off);
+                   int64_t cnt_off, const int32_t* status, cudaStream_t st) {
+  ep_counts_push_kernel<<<1, 256, 0, st>>>(counts, me, ep, E, peer_base, cnt_off, status);
   B200MOE_CHECK_LAUNCH("ep_counts_push");
   return B200MOE_OK;
 }
 
 int ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align, int64_t cap_rows,
-              int32_t* seg_off, int32_t* goff, int32_t* gcount, cudaStream_t st) {
+              int32_t* seg_off, int32_t* goff, int32_t* gcount, int32_t* status, cudaStream_t st) {
   if (ep < 1 || ep > 32 || etp < 1) {  // one thread per destination EP index
     set_error("ep_layout: ep=%d outside [1, 32] (etp=%d)", ep, etp);
     return B200MOE_EUNSUPPORTED;
   }
-  ep_layout_kernel<<<1, 32, 0, st>>>(cnt_local, me, ep, etp, L, align, cap_rows, seg_off, goff, gcount);
+  ep_layout_kernel<<<1, 32, 0, st>>>(cnt_local, me, ep, etp, L, align, cap_rows, seg_off, goff, gcount, status);
   B200MOE_CHECK_LAUNCH("ep_layout");
   return B200MOE_OK;
 }
@@ -406,12 +421,12 @@ int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_
                 const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
                 const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
                 int64_t dup_off, const void* y_rows, const float* gates, float* dgates, int bwd,
-                cudaStream_t st) {
+                const int32_t* status, cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div(Tn, 8);
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* yb = static_cast<const __nv_bfloat16*>(y_rows);
-#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates)
-#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates)
+#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates, status)
+#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates, status)
   if (Tn > 0) {
     if (bwd) { KSW(k, DB) }
     else { KSW(k, DF) }

@@ -223,16 +223,33 @@ __global__ void __launch_bounds__(256) topk_kernel(const float* __restrict__ log
                                                    float* __restrict__ scores,
                                                    int32_t* __restrict__ topk_idx,
                                                    float* __restrict__ gates,
-                                                   double* __restrict__ gates64) {
+                                                   double* __restrict__ gates64,
+                                                   int32_t* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= Tn) return;
   double s[NPL];
   const float* row = logits + t * E;
+  bool bad = false;
 #pragma unroll
   for (int j = 0; j < NPL; ++j) {
     const int e = lane + 32 * j;
     s[j] = (e < E) ? (double)row[e] : -DBL_MAX;
+    bad |= e < E && !isfinite(row[e]);
+  }
+  // non-finite logits (router.py:141-144): flag, and a valid placeholder
+  // routing 0..k-1 so that nothing downstream indexes out of range
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0 && status) atomicOr(status, 1);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (lane + 32 * j < E) scores[t * E + lane + 32 * j] = 0.f;
+    if (lane < k) {
+      topk_idx[t * k + lane] = lane;
+      gates[t * k + lane] = 0.f;
+      if (gates64) gates64[t * k + lane] = 0.0;
+    }
+    return;
   }
   if (gate_fn == B200MOE_GATE_SOFTMAX) {
     double m = -DBL_MAX;
@@ -774,9 +791,11 @@ int router_logits(const void* x, int dt, const float* wg, int64_t Tn, int64_t H,
 }
 
 int router_topk(const float* logits, int64_t Tn, int E, int k, int gate_fn, int renorm,
-                float* scores, int32_t* idx, float* gates, double* gates64, cudaStream_t st) {
+                float* scores, int32_t* idx, float* gates, double* gates64, int32_t* status,
+                cudaStream_t st) {
+  if (Tn == 0) return B200MOE_OK;
   const unsigned grid = (unsigned)ceil_div(Tn, 8);
-#define TK(NPL) topk_kernel<NPL><<<grid, 256, 0, st>>>(logits, Tn, E, k, gate_fn, renorm, scores, idx, gates, gates64)
+#define TK(NPL) topk_kernel<NPL><<<grid, 256, 0, st>>>(logits, Tn, E, k, gate_fn, renorm, scores, idx, gates, gates64, status)
   if (E <= 32) TK(1);
   else if (E <= 64) TK(2);
   else if (E <= 128) TK(4);

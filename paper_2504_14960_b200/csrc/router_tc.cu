@@ -1,0 +1,281 @@
+// K1 fused router forward on the 5th-gen tensor cores (sm_100a):
+//
+//   logits = x @ W_g       (router.py:145)  tcgen05.mma, x streamed once by TMA
+//   scores = softmax/sigmoid(logits) in float64    (router.py:146-149)
+//   top-k  (score desc, expert id asc), gates raw or renormalised (:150-153)
+//
+// W_g is fp32; it enters the MMA as three bf16 parts hi + mid + lo == W_g
+// exactly (split on the host once, GatingParams.device_w_g_tc), stacked as
+// the N dimension: B = [hi | mid | lo] ([NP, H], rows p*EP + e, zero padded
+// to NP = round_up(3 EP, 16)).  bf16 x bf16 products are exact in fp32, so
+// the accumulator holds the three partial dot products of the fp32 logit,
+// which the epilogue folds in fixed order (hi + mid) + lo.
+//
+// One CTA per 128-token tile (M = 128, N = NP, K = H): warp 0 lane 0 is the
+// TMA producer (x tile 128 x 64 + the W parts 64 x NP per stage, 128B
+// swizzle), warp 1 lane 0 issues tcgen05.mma into a [128 x NP] fp32 TMEM
+// accumulator, warp 2 owns the TMEM allocation, warps 4..7 are the epilogue:
+// one thread per token reads its accumulator row (tcgen05.ld), and for
+// E <= 32 does softmax/sigmoid and the top-k in registers (logits, scores,
+// ids and gates written once); for larger E it writes the logits and the
+// warp-per-token top-k kernel follows (router.cu).
+//
+// Non-finite logits (non-finite tokens or gating weights, router.py:141-144)
+// set bit 0 of *status and the token gets the valid placeholder routing
+// 0..k-1, so nothing downstream indexes out of range; the host raises
+// NumericError when it reads the status (dispatcher.py, no blocking check).
+#include "tcgen05.cuh"
+
+namespace b200moe {
+
+int router_topk(const float*, int64_t, int, int, int, int, float*, int32_t*, float*, double*, int32_t*,
+                cudaStream_t);
+
+namespace rtc {
+using namespace tc;
+
+constexpr int BM = 128, BK = 64;
+
+__host__ __device__ constexpr int np_of(int ep) { return (3 * ep + 15) / 16 * 16; }
+__host__ __device__ constexpr int tmem_cols(int np) { return np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256; }
+
+// kind::f16 instruction descriptor: bf16 A/B (K-major), fp32 D, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_n(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+struct Args {
+  int64_t T;
+  int E, k, gate_fn, renorm, nkb, stages;
+  float* logits;
+  float* scores;
+  int32_t* idx;
+  float* gates;
+  double* gates64;
+  int32_t* status;
+};
+
+template <int EP>
+__device__ __forceinline__ void epilogue_row(const Args& a, int64_t t, const float (&lg)[EP]) {
+  const int E = a.E, k = a.k;
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < EP; ++e)
+    if (e < E) bad |= !isfinite(lg[e]);
+  float* lrow = a.logits + t * E;
+#pragma unroll
+  for (int e = 0; e < EP; ++e)
+    if (e < E) lrow[e] = lg[e];
+  if (EP > 32) return;  // logits only; router_topk follows
+  if (bad) {
+    if (a.status) atomicOr(a.status, 1);
+    for (int e = 0; e < E; ++e) a.scores[t * E + e] = 0.f;
+    for (int s = 0; s < k; ++s) {
+      a.idx[t * k + s] = s;
+      a.gates[t * k + s] = 0.f;
+      if (a.gates64) a.gates64[t * k + s] = 0.0;
+    }
+    return;
+  }
+  double s[EP];
+  if (a.gate_fn == B200MOE_GATE_SOFTMAX) {
+    double m = -1.0e308;
+#pragma unroll
+    for (int e = 0; e < EP; ++e)
+      if (e < E) m = fmax(m, (double)lg[e]);
+    double sum = 0.0;
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+      s[e] = e < E ? exp((double)lg[e] - m) : 0.0;
+      sum += s[e];
+    }
+#pragma unroll
+    for (int e = 0; e < EP; ++e) s[e] = s[e] / sum;
+  } else {
+#pragma unroll
+    for (int e = 0; e < EP; ++e) s[e] = e < E ? 1.0 / (1.0 + exp(-(double)lg[e])) : 0.0;
+  }
+  float* srow = a.scores + t * E;
+#pragma unroll
+  for (int e = 0; e < EP; ++e)
+    if (e < E) srow[e] = (float)s[e];
+  // k rounds of arg-max over (score desc, id asc): strict > in ascending id
+  // order keeps the lower id on ties (the stable argsort of router.py:123)
+  uint64_t taken = 0;
+  double raw[32];
+  double raw_sum = 0.0;
+  for (int r = 0; r < k; ++r) {
+    double best = -1.0;
+    int bid = 0;
+#pragma unroll
+    for (int e = 0; e < EP; ++e) {
+      if (e < E && !((taken >> e) & 1ull) && s[e] > best) {
+        best = s[e];
+        bid = e;
+      }
+    }
+    taken |= 1ull << bid;
+    raw[r] = best;
+    raw_sum += best;
+    a.idx[t * k + r] = bid;
+  }
+  for (int r = 0; r < k; ++r) {
+    const double g = a.renorm ? raw[r] / raw_sum : raw[r];
+    a.gates[t * k + r] = (float)g;
+    if (a.gates64) a.gates64[t * k + r] = g;
+  }
+}
+
+template <int EP>
+__global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant__ CUtensorMap map_x,
+                                                           const __grid_constant__ CUtensorMap map_w,
+                                                           const Args a) {
+  constexpr int NP = np_of(EP);
+  constexpr int A_BYTES = BM * BK * 2, B_BYTES = NP * BK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int COLS = tmem_cols(NP);
+  const int S = a.stages;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sA = base, sB = base + S * A_BYTES;
+  const uint32_t bars = base + S * STAGE;
+  const uint32_t full_bar = bars, empty_bar = bars + 8 * S, done_bar = bars + 16 * S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE + 16 * S + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full_bar + 8 * i, 1);
+      mbar_init(empty_bar + 8 * i, 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_x);
+    prefetch_map(&map_w);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < a.nkb; ++kb) {
+        mbar_wait(empty_bar + 8 * stage, phase ^ 1);
+        mbar_expect_tx(full_bar + 8 * stage, STAGE);
+        tma_load_3d(&map_x, sA + stage * A_BYTES, full_bar + 8 * stage, kb * BK, m0, 0);
+        tma_load_3d(&map_w, sB + stage * B_BYTES, full_bar + 8 * stage, kb * BK, 0, 0);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_n(NP);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < a.nkb; ++kb) {
+        mbar_wait(full_bar + 8 * stage, phase);
+        tc_fence_after();
+        const uint32_t a_s = sA + stage * A_BYTES, b_s = sB + stage * B_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          tc_mma(tmem, smem_desc(a_s + k * 32, 16, 1024), smem_desc(b_s + k * 32, 16, 1024), idesc,
+                 (kb | k) != 0);
+        tc_commit(empty_bar + 8 * stage);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      tc_commit(done_bar);
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    mbar_wait(done_bar, 0);
+    tc_fence_after();
+    const uint32_t t_row = tmem + ((uint32_t)(32 * q) << 16);
+    // columns p * EP + e arrive in increasing order, so lg = (hi + mid) + lo
+    constexpr int NCH = (3 * EP + 31) / 32;
+    float lg[EP];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      uint32_t v[32];
+      tmem_ld32(t_row + c * 32, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = c * 32 + j;
+        if (col < EP) lg[col] = __uint_as_float(v[j]);
+        else if (col < 3 * EP) lg[col % EP] += __uint_as_float(v[j]);
+      }
+    }
+    const int64_t t = (int64_t)m0 + 32 * q + lane;
+    if (t < a.T) epilogue_row<EP>(a, t, lg);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(COLS));
+  }
+}
+
+template <int EP>
+static int launch(const void* x, int64_t T, int64_t H, const void* w, Args a, cudaStream_t st) {
+  constexpr int NP = np_of(EP);
+  constexpr int STAGE = BM * BK * 2 + NP * BK * 2;
+  CUtensorMap mx, mw;
+  int rc = make_map(&mx, x, (uint64_t)H, (uint64_t)T, 1, (uint64_t)H, (uint64_t)H * T, BM);
+  if (rc) return rc;
+  rc = make_map(&mw, w, (uint64_t)H, (uint64_t)NP, 1, (uint64_t)H, (uint64_t)H * NP, NP);
+  if (rc) return rc;
+  a.nkb = (int)ceil_div(H, BK);
+  a.stages = std::max(2, std::min(8, (196 * 1024) / STAGE));
+  const int smem = 1024 + a.stages * STAGE + 16 * a.stages + 64;
+  static bool attr_set = false;  // idempotent; races only repeat the same call
+  if (!attr_set) {
+    cudaFuncSetAttribute(router_tc_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    attr_set = true;
+  }
+  router_tc_kernel<EP><<<(unsigned)ceil_div(T, BM), 256, smem, st>>>(mx, mw, a);
+  B200MOE_CHECK_LAUNCH("router_fwd_tc");
+  if (EP > 32)
+    return router_topk(a.logits, T, a.E, a.k, a.gate_fn, a.renorm, a.scores, a.idx, a.gates, a.gates64,
+                       a.status, st);
+  return B200MOE_OK;
+}
+
+}  // namespace rtc
+
+int router_fwd_tc_np(int E) {
+  const int ep = E <= 8 ? 8 : E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 0;
+  return ep ? rtc::np_of(ep) : 0;
+}
+
+int router_fwd_tc(const void* x, int64_t T, int64_t H, const void* w_parts, int E, int k, int gate_fn,
+                  int renorm, float* logits, float* scores, int32_t* idx, float* gates, double* gates64,
+                  int32_t* status, cudaStream_t st) {
+  if (T == 0) return B200MOE_OK;
+  rtc::Args a{T, E, k, gate_fn, renorm, 0, 0, logits, scores, idx, gates, gates64, status};
+  if (E <= 8) return rtc::launch<8>(x, T, H, w_parts, a, st);
+  if (E <= 16) return rtc::launch<16>(x, T, H, w_parts, a, st);
+  if (E <= 32) return rtc::launch<32>(x, T, H, w_parts, a, st);
+  if (E <= 64) return rtc::launch<64>(x, T, H, w_parts, a, st);
+  set_error("router_fwd_tc: E=%d > 64 unsupported", E);
+  return B200MOE_EUNSUPPORTED;
+}
+
+}  // namespace b200moe

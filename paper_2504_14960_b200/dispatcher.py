@@ -36,10 +36,10 @@ from . import experts as X
 from . import gemm_tc
 from . import kernels as K
 from .collectives import LocalWorld, RankContext
-from .errors import ValidationError
-from .router import (DROP_FULLSEQUENCE, GATE_CODES, GatingParams,
-                     RoutingDecision, capacity_limit, check_finite, gather_full_sequence_decision,
-                     kept_mask, routing_from_logits)
+from .errors import NumericError, ProtocolError, ValidationError
+from .router import (DROP_FULLSEQUENCE, GATE_CODES, PRIORITY_PROBABILITY, GatingParams,
+                     RoutingDecision, capacity_limit, gather_full_sequence_decision,
+                     kept_mask, nonfinite_error, routing_from_logits)
 from .topology import (GroupSets, ParallelTopology, check_pp_consistency,
                        generate_parallel_groups, sequence_group)
 
@@ -303,6 +303,38 @@ def exchange_plan(counts: np.ndarray, ep_pos: int, L_: int, etp_recv: Optional[n
                         group_expert)
 
 
+# ----------------------------------------------------------- step status
+# Failures the device detects (router.py:141-144 non-finite inputs, a peer
+# buffer too small for the block, a peer whose step failed) are bits of a
+# per-rank int32 status word instead of blocking host checks: the router and
+# exchange kernels set them, the word is copied to pinned host memory right
+# after the router / the dispatch barrier, and moe_forward raises after
+# waiting for that early point of the step only (the GEMMs stay queued).
+ST_NONFINITE, ST_PEER_ABORT, ST_OVERSIZE = 1, 2, 4
+_STATUS: Dict[tuple, tuple] = {}
+
+
+def _status_slot(device, rank: int):
+    key = (str(device), rank)
+    slot = _STATUS.get(key)
+    if slot is None:
+        slot = (torch.zeros((1,), dtype=torch.int32, device=device),
+                torch.zeros((1,), dtype=torch.int32).pin_memory(),
+                torch.zeros((1,), dtype=torch.int32, device=device))  # scratch (unchecked steps)
+        _STATUS[key] = slot
+    return slot
+
+
+def _raise_status(bits: int, what: str = "") -> None:
+    if bits & ST_NONFINITE:
+        raise NumericError(f"token block contains non-finite values{what}")
+    if bits & ST_OVERSIZE:
+        raise ValidationError(f"token block exceeds the peer buffers{what}: pass peer_tokens >= the "
+                              "largest block on first use", constraint="peer-capacity")
+    if bits & ST_PEER_ABORT:
+        raise ProtocolError(f"a member of the expert-parallel exchange failed this step{what}")
+
+
 class RankLayer:
     """Everything one rank needs to run the layer forward and backward."""
 
@@ -351,6 +383,10 @@ class RankLayer:
         self.use_peer = (want == "peer" and not self.single and 1 < len(groups.xch) <= 32
                          and dtype == torch.bfloat16 and self.k <= 8 and gemm_tc.available()
                          and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
+        # step status (see _status_slot): the router writes bit 0 into the
+        # checked word only when inputs are validated
+        self.status, self.status_host, self.scratch = _status_slot(device, rank)
+        self.status_event = None
 
     # ------------------------------------------------------- shared expert
     # Builder-defined (no reference): a dense FFN over every token whose
@@ -379,11 +415,36 @@ class RankLayer:
         p = self.params
         T, H = x.shape
         x = x.to(self.device, self.dtype).contiguous()
-        if self.check:
-            check_finite(x, "token block")
-        logits = K.router_logits(x, self.wg, parts=self.wg_parts)
-        dec = routing_from_logits(logits, p, positions)
+        self.status.zero_()
+        self.status_event = None
+        rst = self.status if self.check else self.scratch
+        want64 = p.drop_priority == PRIORITY_PROBABILITY
+        if self.wg_parts is not None and K.router_fwd_supported(x, self.E):
+            # fused: x read once by TMA, logits on the tensor cores, softmax /
+            # sigmoid and top-k in the epilogue (router_tc.cu)
+            logits, scores, idx, gates, g64 = K.router_fwd(
+                x, p.device_w_g_tc(self.device), self.E, self.k, GATE_CODES[p.gate_fn],
+                p.renormalize_topk, rst, want_f64=want64)
+            kept = torch.ones((T, self.k), dtype=torch.bool, device=x.device)
+            dec = RoutingDecision(idx, gates, kept, torch.as_tensor(positions, dtype=torch.int64),
+                                  scores, g64)
+        else:
+            logits = K.router_logits(x, self.wg, parts=self.wg_parts)
+            dec = routing_from_logits(logits, p, positions, status=rst)
         return self.forward_routed(ctx, x, dec, logits)
+
+    def _mark_status(self):
+        """Copy the status word to pinned host memory at this point of the
+        stream (read by moe_forward via check_status)."""
+        self.status_host.copy_(self.status, non_blocking=True)
+        self.status_event = torch.cuda.Event()
+        self.status_event.record()
+
+    def check_status(self, what: str = "") -> None:
+        if self.status_event is None:
+            return
+        self.status_event.synchronize()
+        _raise_status(int(self.status_host[0]), what)
 
     def forward_routed(self, ctx, x, dec: RoutingDecision, logits=None):
         p = self.params
@@ -408,6 +469,7 @@ class RankLayer:
         self.align = -seg if seg else ALIGN
         saved = {"x": x, "dec": dec, "plan_dev": plan, "logits": logits}
         if self.single:
+            self._mark_status()
             # padded expert-major layout straight from the plan; group sizes stay on device
             if seg:
                 R = E * seg
@@ -424,6 +486,8 @@ class RankLayer:
                          pair_row=plan.gemm_row)
             self._finish_forward(ctx, saved, plan.counts)
             return out, saved
+        if not self.use_peer:
+            self._mark_status()  # the NCCL path also checks it with its count all-gather
         out, saved = self._forward_exchange(ctx, x, dec, plan, saved)
         if "xpl" in saved:
             recv = saved["xpl"].recv_counts
@@ -478,7 +542,12 @@ class RankLayer:
             if len(g.etp) > 1:
                 etp_recv = np.full((len(g.etp), len(g.ep) * self.L), self.seg, dtype=np.int64)
             return exchange_plan(counts, ep_pos, self.L, etp_recv, ALIGN)
-        counts = ctx.gather_counts(g.ep, plan.counts.to(torch.int64))  # [ep, E] host (one sync)
+        # [ep, E] host (one sync), with every member's step status appended
+        got = ctx.gather_counts(g.ep, torch.cat([plan.counts.to(torch.int64), self.status.to(torch.int64)]))
+        counts = got[:, :-1]
+        bad = [int(v) for v in got[:, -1]]
+        if any(bad):
+            _raise_status(bad[ep_pos] or ST_PEER_ABORT)
         mine = exchange_plan(counts, ep_pos, self.L, None, ALIGN)
         if len(g.etp) > 1:
             etp_recv = ctx.gather_counts(g.etp, torch.as_tensor(mine.recv_padded.reshape(-1)))
@@ -613,38 +682,49 @@ class RankLayer:
         px = cache.get(key)
         if px is None:
             # buffer layout must be identical on every member: agree on the
-            # largest token block once, when the buffers are created
-            T_max = max(int(self.peer_tokens or 0), T)
-            T_max = max(int(v) for v in ctx.meta(xch, T_max).values())
+            # largest token block and on the push mode once, when the buffers
+            # are created.  Deduplicated push: it trades link bytes for a local
+            # copy of the duplicate rows; measured worth it from top-4 up (C4:
+            # 1-2 % of the step), neutral or slightly worse at top-2
+            env = os.environ.get("B200MOE_PUSH_DEDUP")
+            dedup = env == "1" or (env is None and self.k >= 4)
+            got = ctx.meta(xch, (max(int(self.peer_tokens or 0), T), dedup))
+            T_max = max(int(v[0]) for v in got.values())
+            if len({bool(v[1]) for v in got.values()}) != 1:
+                raise ProtocolError("B200MOE_PUSH_DEDUP differs between the members of the exchange "
+                                    f"{xch}: {[bool(got[r][1]) for r in xch]}")
             cap = PX.capacity_rows(len(xch), T_max, self.k, self.L, ALIGN)
             ret = T_max * self.k + self.E * (ALIGN - 1)  # this rank's padded pair layout
             if self.pad_to_capacity and not self.params.dropless:
                 seg = (capacity_limit(self.params.capacity_factor, T_max, self.E) + ALIGN - 1) // ALIGN
                 ret = max(ret, self.E * seg * ALIGN)
             ret = (ret + ALIGN - 1) // ALIGN * ALIGN
-            # deduplicated push: it trades link bytes for a local copy of the
-            # duplicate rows; measured worth it from top-4 up (C4: 1-2 % of the
-            # step), neutral or slightly worse at top-2
-            env = os.environ.get("B200MOE_PUSH_DEDUP")
-            dedup = env == "1" or (env is None and self.k >= 4)
             px = PX.PeerExchange(ctx, xch, self.E, self.L, H, cap, ret, self.device, etp=len(self.g.etp),
                                  dedup=dedup)
             px.tokens = T_max
             cache[key] = px
-        elif T > px.tokens:
-            raise ValidationError(f"token block of {T} rows exceeds the peer buffers' {px.tokens}: "
-                                  "pass peer_tokens >= the largest block on first use",
-                                  constraint="peer-capacity")
         return px
 
     def _forward_peer(self, ctx, x, dec, plan, saved):
         T = x.shape[0]
         px = self._peer(ctx, T)
-        st = px.forward_dispatch(x, dec.experts, plan, ALIGN)
+        oversize = T > px.tokens
+        if oversize:
+            # the block does not fit the peers' buffers: take part in the
+            # step's protocol without tokens and fail it everywhere (status)
+            self.status.fill_(ST_OVERSIZE)
+            st = px.forward_dispatch(x[:0], dec.experts[:0], plan, ALIGN, status=self.status)
+        else:
+            st = px.forward_dispatch(x, dec.experts, plan, ALIGN, status=self.status)
+        self._mark_status()
         pre, h, _ = X.ffn_forward(px.region("xr"), st["goff"], self.L, None, self.pk, px.cap,
                                   y_scatter=px.scatter("yret"))
         y_sh = self._shared_forward(x, saved)
         px.barrier()  # every expert output row (ETP: every partial) is back in yret
+        if oversize:
+            out = torch.zeros_like(x)
+            saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row, y=None)
+            return out, saved
         y = px.returned("yret")
         out = K.combine(y, plan.gemm_row, T, gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
         saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row, y=y)
@@ -826,6 +906,19 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
     for r in results:
         outputs.append(None if r is None else r[0])
         context.per_rank.append(None if r is None else r[1])
+    # failures the device flagged during the step (non-finite inputs, an
+    # oversized block, a failed peer): the wait ends at the router / dispatch
+    # barrier of this step, the rest of the step stays queued on the GPU
+    layers = [(r, sv["layer"]) for r, sv in enumerate(context.per_rank) if sv is not None]
+    for r, layer in layers:
+        layer.status_event and layer.status_event.synchronize()
+    bits = {r: int(layer.status_host[0]) if layer.status_event is not None else 0 for r, layer in layers}
+    for mask in (ST_NONFINITE, ST_OVERSIZE, ST_PEER_ABORT):  # the root cause first
+        for r in sorted(bits):
+            if bits[r] & mask:
+                if mask == ST_NONFINITE:
+                    raise nonfinite_error(context.per_rank[r]["x"], params, f" (rank {r})")
+                _raise_status(mask, f" (rank {r})")
     for sv in context.per_rank:
         if sv is not None:
             sv["decision"] = sv["dec"]

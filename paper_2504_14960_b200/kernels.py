@@ -156,7 +156,8 @@ def router_stats(topk_idx: torch.Tensor, kept, scores, E: int):
     return counts, top1, psum
 
 
-def router_topk(logits: torch.Tensor, k: int, gate_fn: int, renorm: bool, want_f64: bool = False):
+def router_topk(logits: torch.Tensor, k: int, gate_fn: int, renorm: bool, want_f64: bool = False,
+                status: Optional[torch.Tensor] = None):
     T, E = logits.shape
     _cuda(logits, "logits", torch.float32)
     dev = logits.device
@@ -165,8 +166,36 @@ def router_topk(logits: torch.Tensor, k: int, gate_fn: int, renorm: bool, want_f
     gates = torch.empty((T, k), dtype=torch.float32, device=dev)
     g64 = torch.empty((T, k), dtype=torch.float64, device=dev) if want_f64 else None
     L.call("b200moe_router_topk", L.ptr(logits), T, E, k, gate_fn, int(renorm), L.ptr(scores),
-           L.ptr(idx), L.ptr(gates), L.ptr(g64), _sp())
+           L.ptr(idx), L.ptr(gates), L.ptr(g64), L.ptr(status), _sp())
     return scores, idx, gates, g64
+
+
+def router_fwd_supported(x: torch.Tensor, E: int) -> bool:
+    """The fused tensor-core router forward: bf16 tokens, E <= 64, H % 8 == 0."""
+    from . import gemm_tc
+
+    return (x.dtype == torch.bfloat16 and x.shape[1] % 8 == 0 and x.shape[1] >= 64
+            and int(L.load().b200moe_router_fwd_tc_np(E)) > 0 and gemm_tc.available())
+
+
+def router_fwd(x: torch.Tensor, w_tc: torch.Tensor, E: int, k: int, gate_fn: int, renorm: bool,
+               status: torch.Tensor, want_f64: bool = False):
+    """Fused router forward (router.py:141-162): logits on the tensor cores
+    against the exact bf16 parts of W_g (``w_tc``, GatingParams.device_w_g_tc),
+    softmax/sigmoid and top-k in the same kernel.  Non-finite logits set bit 0
+    of ``status``.  -> (logits, scores, idx, gates, gates_f64)"""
+    T, H = x.shape
+    _cuda(x, "x", torch.bfloat16)
+    _cuda(w_tc, "w_tc", torch.bfloat16)
+    dev = x.device
+    logits = torch.empty((T, E), dtype=torch.float32, device=dev)
+    scores = torch.empty((T, E), dtype=torch.float32, device=dev)
+    idx = torch.empty((T, k), dtype=torch.int32, device=dev)
+    gates = torch.empty((T, k), dtype=torch.float32, device=dev)
+    g64 = torch.empty((T, k), dtype=torch.float64, device=dev) if want_f64 else None
+    L.call("b200moe_router_fwd_tc", L.ptr(x), T, H, L.ptr(w_tc), E, k, gate_fn, int(renorm),
+           L.ptr(logits), L.ptr(scores), L.ptr(idx), L.ptr(gates), L.ptr(g64), L.ptr(status), _sp())
+    return logits, scores, idx, gates, g64
 
 
 class PlanTensors:
@@ -317,24 +346,25 @@ def act_fwd(pre, act: int, group_off, G: int, F: int, out=None):
 # ------------------------------------------------ EP exchange over peer memory
 # peer_base: int64 device tensor [ep] with the base address of every EP
 # member's symmetric buffer (peer.PeerExchange owns it and the region offsets).
-def ep_counts_push(counts: torch.Tensor, me: int, ep: int, peer_base, cnt_off: int):
+def ep_counts_push(counts: torch.Tensor, me: int, ep: int, peer_base, cnt_off: int, status=None):
     _cuda(counts, "counts", torch.int32)
     L.call("b200moe_ep_counts_push", L.ptr(counts), me, ep, counts.numel(), L.ptr(peer_base),
-           cnt_off, _sp())
+           cnt_off, L.ptr(status), _sp())
 
 
 def ep_barrier(peer_base, flag_off: int, me: int, ep: int, epoch: int):
     L.call("b200moe_ep_barrier", L.ptr(peer_base), flag_off, me, ep, epoch & 0xFFFFFFFF, _sp())
 
 
-def ep_layout(cnt: torch.Tensor, me: int, ep: int, etp: int, L_: int, align: int, cap_rows: int):
+def ep_layout(cnt: torch.Tensor, me: int, ep: int, etp: int, L_: int, align: int, cap_rows: int,
+              status=None):
     """-> (seg_off [ep*L], goff [L+1], gcount [L]) int32 on the device."""
     dev = cnt.device
     seg_off = torch.empty((ep * L_,), dtype=torch.int32, device=dev)
     goff = torch.empty((L_ + 1,), dtype=torch.int32, device=dev)
     gcount = torch.empty((L_,), dtype=torch.int32, device=dev)
     L.call("b200moe_ep_layout", L.ptr(cnt), me, ep, etp, L_, align, cap_rows, L.ptr(seg_off),
-           L.ptr(goff), L.ptr(gcount), _sp())
+           L.ptr(goff), L.ptr(gcount), L.ptr(status), _sp())
     return seg_off, goff, gcount
 
 
@@ -346,7 +376,7 @@ def ep_zero_pads(buf: torch.Tensor, goff, gcount, G: int, align: int, origin=Non
 
 def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int, peer_base, me: int,
                 etp: int, dst_off: int, origin_off: int = 0, bwd: bool = False, y_rows=None,
-                gates=None, dup_off: int = -1):
+                gates=None, dup_off: int = -1, status=None):
     """Forward: push x rows to the owners' receive buffers and record their
     origin.  Backward: push gates*u rows; returns dgates [T, k] fp32 = <u, y>
     with y the returned expert outputs (``y_rows``, local padded layout).
@@ -358,7 +388,7 @@ def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int,
     dg = torch.empty((T, k), dtype=torch.float32, device=x.device) if bwd else None
     L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
            L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, etp, dst_off, origin_off, dup_off,
-           L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), _sp())
+           L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), L.ptr(status), _sp())
     return dg
 
 

@@ -137,11 +137,14 @@ class PeerExchange:
 
     def _init_local(self, ctx):
         self.buf = torch.zeros((self.nbytes,), dtype=torch.uint8, device=self.device)
+        torch.cuda.current_stream().synchronize()  # zeroed flags before any peer's first barrier
         got = ctx.meta(self.group, self.buf.data_ptr())
         self.peer_base = torch.tensor([int(got[r]) for r in self.group], dtype=torch.int64,
                                       device=self.device)
         torch.cuda.current_stream().synchronize()
-        self.device_barrier = False
+        # LocalWorld(device_barrier=True): ranks on their own streams meet in
+        # the flag barrier kernel, as across GPUs; otherwise a host rendezvous
+        self.device_barrier = bool(getattr(ctx.world, "device_barrier", False))
 
     def region(self, name: str) -> torch.Tensor:
         """This rank's bf16 view of a row region: [cap, H] (receive side) or
@@ -186,17 +189,21 @@ class PeerExchange:
             self.ctx.meta(self.group, None)
 
     # ------------------------------------------------------------ steps
-    def forward_dispatch(self, x, topk_idx, plan, align: int):
+    def forward_dispatch(self, x, topk_idx, plan, align: int, status=None):
         """counts push -> barrier -> layout -> pads -> dispatch -> barrier.
-        Returns the routing state the rest of the step needs."""
-        K.ep_counts_push(plan.counts, self.me, self.members, self.peer_base, self.cnt_off)
+        Returns the routing state the rest of the step needs.  ``status``
+        (device int32[1]): a rank whose step already failed pushes an abort
+        marker instead of its counts, every member then skips the pushes and
+        flags the step (bit 1), so all of them finish the barriers and raise."""
+        K.ep_counts_push(plan.counts, self.me, self.members, self.peer_base, self.cnt_off, status=status)
         self.barrier()
         seg_off, goff, gcount = K.ep_layout(self.counts(), self.me, self.ep, self.etp, self.L, align,
-                                            self.cap)
+                                            self.cap, status=status)
         K.ep_zero_pads(self.region("xr"), goff, gcount, self.L, align, origin=self.origin())
         dup_off = self.off["dup"] if self.dedup else -1
         K.ep_dispatch(x, topk_idx, plan.gemm_row, plan.poffsets, seg_off, self.L, self.peer_base,
-                      self.me, self.etp, self.off["xr"], self.off["origin"], dup_off=dup_off)
+                      self.me, self.etp, self.off["xr"], self.off["origin"], dup_off=dup_off,
+                      status=status)
         self.barrier()
         if self.dedup:
             K.ep_expand(self.region("xr"), goff, gcount, self.L, self.dup(), 0)

@@ -120,6 +120,28 @@ class GatingParams:
             self._dev_cache[key] = (w3t, w6)
         return self._dev_cache[key]
 
+    def device_w_g_tc(self, device=None) -> torch.Tensor:
+        """B operand of the fused tensor-core router (router_tc.cu): bf16
+        [NP, H], rows p * EP + e = part p (hi, mid, lo; hi + mid + lo == W_g
+        exactly) of expert e's column, EP = E rounded up to 8/16/32/64, zero
+        padded to NP = round_up(3 EP, 16) rows (cached)."""
+        device = torch.device(device or _device_default())
+        key = ("wg_tc", str(device))
+        if key not in self._dev_cache:
+            w = self.device_w_g(device)
+            H, E = w.shape
+            EP = next(c for c in (8, 16, 32, 64, E) if c >= E)
+            NP = int(L.load().b200moe_router_fwd_tc_np(E))
+            hi = w.to(torch.bfloat16)
+            r = w - hi.float()
+            mid = r.to(torch.bfloat16)
+            lo = (r - mid.float()).to(torch.bfloat16)
+            out = torch.zeros((max(NP, 3 * EP), H), dtype=torch.bfloat16, device=device)
+            for p, part in enumerate((hi, mid, lo)):
+                out[p * EP:p * EP + E] = part.T
+            self._dev_cache[key] = out[:NP].contiguous() if NP else out
+        return self._dev_cache[key]
+
 
 @dataclass
 class RoutingDecision:
@@ -166,19 +188,25 @@ class RoutingDecision:
                                c(self.scores), c(self.gates_f64))
 
 
-def check_finite(x: torch.Tensor, what: str) -> None:
-    """router.py:141-144 (one device reduction + host read)."""
-    if not bool(torch.isfinite(x).all()):
-        raise NumericError(f"{what} contains non-finite values")
+def nonfinite_error(x: Optional[torch.Tensor], params: GatingParams, suffix: str = "") -> NumericError:
+    """The router.py:141-144 error for a step whose router flagged non-finite
+    logits: the token block unless it is finite, then the gating weights
+    (only evaluated on the error path)."""
+    if x is not None and bool(torch.isfinite(x).all()) and \
+            not bool(torch.isfinite(params.device_w_g(x.device)).all()):
+        return NumericError("gating weights contain non-finite values" + suffix)
+    return NumericError("token block contains non-finite values" + suffix)
 
 
 def routing_from_logits(logits: torch.Tensor, params: GatingParams, positions=None,
-                        want_f64: bool = False) -> RoutingDecision:
-    """Scores, top-k and gates from fp32 logits (router.py:146-162)."""
+                        want_f64: bool = False, status: Optional[torch.Tensor] = None) -> RoutingDecision:
+    """Scores, top-k and gates from fp32 logits (router.py:146-162).  A token
+    with non-finite logits sets bit 0 of ``status`` and gets the placeholder
+    routing 0..k-1."""
     n = logits.shape[0]
     scores, idx, gates, g64 = K.router_topk(
         logits.contiguous(), params.k, GATE_CODES[params.gate_fn], params.renormalize_topk,
-        want_f64=want_f64 or params.drop_priority == PRIORITY_PROBABILITY)
+        want_f64=want_f64 or params.drop_priority == PRIORITY_PROBABILITY, status=status)
     if positions is None:
         positions = torch.arange(n, dtype=torch.int64)
     else:
@@ -201,11 +229,27 @@ def compute_gates(x, params: GatingParams, positions=None, *, check: bool = True
     if x.dim() != 2 or x.shape[1] != params.hidden:
         raise ValidationError(f"token block shape {tuple(x.shape)} incompatible with w_g "
                               f"{tuple(params.w_g.shape)}", constraint="x-shape")
-    if check:
-        check_finite(x, "token block")
-        check_finite(params.device_w_g(x.device), "gating weights")
-    logits = K.router_logits(x, params.device_w_g(x.device))
-    return routing_from_logits(logits, params, positions)
+    status = torch.zeros((1,), dtype=torch.int32, device=x.device)
+    if x.dtype == torch.bfloat16 and K.router_fwd_supported(x, params.num_experts):
+        # fused tensor-core router (router_tc.cu): x read once
+        _, scores, idx, gates, g64 = K.router_fwd(
+            x, params.device_w_g_tc(x.device), params.num_experts, params.k,
+            GATE_CODES[params.gate_fn], params.renormalize_topk, status,
+            want_f64=params.drop_priority == PRIORITY_PROBABILITY)
+        n = x.shape[0]
+        pos = torch.arange(n, dtype=torch.int64) if positions is None else positions
+        dec = RoutingDecision(idx, gates, torch.ones((n, params.k), dtype=torch.bool, device=x.device),
+                              torch.as_tensor(pos, dtype=torch.int64), scores, g64)
+        if dec.positions.shape != (n,):
+            raise ValidationError("positions must have one entry per token", constraint="positions")
+    else:
+        logits = K.router_logits(x, params.device_w_g(x.device))
+        dec = routing_from_logits(logits, params, positions, status=status)
+    # router.py:141-144: one host read of the flag the kernels raised (no
+    # separate pass over x)
+    if check and int(status.item()) & 1:
+        raise nonfinite_error(x, params)
+    return dec
 
 
 def capacity_limit(capacity_factor: float, l_scope: int, num_experts: int) -> int:

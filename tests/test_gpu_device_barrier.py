@@ -1,0 +1,148 @@
+"""GPU: the production synchronisation path of the peer exchange on ONE GPU.
+
+LocalWorld(device_barrier=True) runs every rank on its own CUDA stream and
+meets the ranks in ep_barrier_kernel (flag stores with st.release.sys into
+the peers' buffers, ld.acquire.sys spin) instead of a host rendezvous: the
+same kernels, flags and cross-rank stores the NcclWorld path uses across
+GPUs -- the counts push into the peers' matrices, the dispatch push into
+their receive buffers, the GEMM scatter epilogue writing into the senders'
+return buffers and the deduplicated rows read by ep_expand after the
+barrier.  Results must be bit-identical with the host-barrier emulation
+(whose parity with the NCCL path and the oracle test_gpu_peer.py checks)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import moe_oracle as O  # noqa: E402
+
+import paper_2504_14960_b200 as B  # noqa: E402
+from paper_2504_14960_b200.errors import NumericError, ProtocolError, ValidationError  # noqa: E402
+
+
+def _blocks(sizes, H, seed, nan_rank=None):
+    rng = np.random.default_rng(seed)
+    out, ups, start = [], [], 0
+    for r, n in enumerate(sizes):
+        x = rng.standard_normal((n, H))
+        if r == nan_rank:
+            x[n // 2, 1] = np.nan
+        out.append(B.TokenBlock(torch.as_tensor(x, dtype=torch.float32).to("cuda", torch.bfloat16),
+                                np.arange(start, start + n)))
+        start += n
+        ups.append(torch.as_tensor(rng.standard_normal((n, H)), dtype=torch.float32).to("cuda", torch.bfloat16))
+    return out, ups
+
+
+def _run(world, topo, params, weights, blocks, ups, shared=None):
+    outs, ctx = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16,
+                              shared_weights=shared)
+    res = B.moe_backward(ups, ctx)
+    torch.cuda.synchronize()
+    return outs, ctx, res
+
+
+def _same(a, b):
+    (o0, c0, r0), (o1, c1, r1) = a, b
+    for r in range(len(o0)):
+        torch.testing.assert_close(o1[r], o0[r], rtol=0, atol=0)
+        torch.testing.assert_close(r1.input_grads[r], r0.input_grads[r], rtol=0, atol=0)
+    torch.testing.assert_close(r1.w_g_grad, r0.w_g_grad, rtol=0, atol=0)
+    for key in r0.expert_grads:
+        for x, y in zip(r0.expert_grads[key][0] + r0.expert_grads[key][1],
+                        r1.expert_grads[key][0] + r1.expert_grads[key][1]):
+            torch.testing.assert_close(y, x, rtol=0, atol=0)
+
+
+CASES = [
+    # world, ep, etp, E, k, sizes, cf, dedup
+    (2, 2, 1, 8, 2, (384, 256), None, "0"),
+    (2, 2, 1, 16, 4, (320, 192), None, "1"),  # deduplicated push across "ranks" (k >= 4, L >= 2)
+    (4, 4, 1, 16, 8, (256, 96, 200, 160), None, "1"),  # k = 8, four experts per rank
+    (4, 2, 2, 8, 2, (192, 64, 128, 256), 1.0, "0"),  # EP x ETP with dropping (C3-like)
+    (4, 2, 2, 16, 4, (128, 128, 96, 64), None, "1"),  # dedup with ETP siblings
+]
+
+
+@pytest.mark.parametrize("world,ep,etp,E,k,sizes,cf,dedup", CASES)
+def test_device_barrier_matches_host_barrier(world, ep, etp, E, k, sizes, cf, dedup, monkeypatch):
+    monkeypatch.setenv("B200MOE_PUSH_DEDUP", dedup)
+    H, F, seed = 128, 256, 5
+    topo = B.ParallelTopology(world_size=world, ep=ep, etp=etp, tp=etp)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=cf)
+    weights = B.init_expert_weights(E, H, F, etp, seed, ep_size=ep, activation="swiglu")
+    blocks, ups = _blocks(sizes, H, seed)
+    host = _run(B.LocalWorld(world), topo, params, weights, blocks, ups)
+    dw = B.LocalWorld(world, device_barrier=True)
+    dev = _run(dw, topo, params, weights, blocks, ups)
+    px = dev[1].per_rank[0]["peer"]
+    assert px.device_barrier and px.epoch > 0 and px.dedup == (dedup == "1")
+    _same(host, dev)
+    # a second step on the same buffers (epochs advance, flags reused)
+    _same(host, _run(dw, topo, params, weights, blocks, ups))
+
+
+def test_dedup_on_off_bit_identical_with_device_barrier(monkeypatch):
+    H, F, E, k, seed = 128, 256, 16, 4, 9
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
+    blocks, ups = _blocks((300, 200), H, seed)
+    got = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("B200MOE_PUSH_DEDUP", flag)
+        got[flag] = _run(B.LocalWorld(2, device_barrier=True), topo, params, weights, blocks, ups)
+    _same(got["0"], got["1"])
+
+
+def test_failed_step_fails_every_rank_then_recovers():
+    """A non-finite block on one rank, then an oversized block: every rank
+    finishes the step's device barriers (abort markers in the count rows),
+    moe_forward raises the root cause, and the next step is unaffected."""
+    H, F, E, k, seed = 128, 256, 8, 2, 3
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
+    blocks, ups = _blocks((128, 128), H, seed)
+    ref = _run(B.LocalWorld(2), topo, params, weights, blocks, ups)
+    for barrier in (False, True):
+        world = B.LocalWorld(2, device_barrier=barrier)
+        _run(world, topo, params, weights, blocks, ups)
+        bad, _ = _blocks((128, 128), H, seed, nan_rank=1)
+        with pytest.raises(NumericError, match="rank 1"):
+            B.moe_forward(bad, weights, topo, params, world, dtype=torch.bfloat16)
+        big, _ = _blocks((256, 128), H, seed)
+        with pytest.raises(ValidationError, match="peer buffers"):
+            B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
+        _same(ref, _run(world, topo, params, weights, blocks, ups))
+
+
+def test_push_mode_must_agree(monkeypatch):
+    """B200MOE_PUSH_DEDUP is agreed when the buffers are created; members that
+    disagree fail loudly instead of leaving stale duplicate rows."""
+    H, F, E, k, seed = 64, 128, 16, 4, 1
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
+    blocks, _ = _blocks((64, 64), H, seed)
+    import threading
+
+    orig = B.dispatcher.os.environ.get
+    local = threading.local()
+
+    def per_rank_env(key, default=None):
+        if key == "B200MOE_PUSH_DEDUP":
+            return "1" if getattr(local, "rank", 0) == 0 else "0"
+        return orig(key, default)
+
+    real = B.dispatcher.RankLayer._peer
+
+    def tagged(self, ctx, T):
+        local.rank = ctx.rank
+        return real(self, ctx, T)
+
+    monkeypatch.setattr(B.dispatcher.RankLayer, "_peer", tagged)
+    monkeypatch.setattr(B.dispatcher.os.environ, "get", per_rank_env)
+    with pytest.raises(ProtocolError, match="PUSH_DEDUP"):
+        B.moe_forward(blocks, weights, topo, params, B.LocalWorld(2), dtype=torch.bfloat16)

@@ -53,3 +53,81 @@ def test_tensor_core_router_gemms_match_fp64(T, H, E):
     ref_w = x.double().T @ dz.double()
     assert _rel(dwg, ref_w) < 1e-5
     assert _rel(K.router_wgrad(x, dz), ref_w) < 2e-6
+
+
+# ----------------------------------------------------------- fused router
+from oracle import moe_oracle as O  # noqa: E402
+from paper_2504_14960_b200 import _lib as L  # noqa: E402
+
+
+@pytest.mark.parametrize("T,H,E,k", [(16384, 4096, 8, 2), (1000, 256, 8, 2), (333, 512, 4, 1),
+                                     (2048, 3584, 64, 8), (777, 1024, 16, 4), (640, 512, 32, 6)])
+@pytest.mark.parametrize("gate_fn,renorm", [("softmax", False), ("sigmoid", True)])
+def test_fused_router_forward(T, H, E, k, gate_fn, renorm):
+    """router_fwd (tcgen05 logits + softmax/sigmoid + top-k in one kernel,
+    router_tc.cu): logits fp32-accurate against float64, and ids / scores /
+    gates exactly the reference arithmetic on those logits (router.py:146-162),
+    checked against the pinned oracle; ties injected."""
+    g = torch.Generator(device="cuda").manual_seed(T * 31 + E)
+    bnd = H ** -0.5
+    wg = ((torch.rand((H, E), generator=g, device="cuda") * 2 - 1) * bnd).float()
+    x = torch.randn((T, H), generator=g, device="cuda").to(torch.bfloat16)
+    x[5::97] = x[5]  # identical rows: identical logits
+    if E >= 2:
+        wg[:, 1] = wg[:, 0]  # experts 0 and 1 tie on every token
+    params = GatingParams(w_g=wg, k=k, gate_fn=gate_fn, renormalize_topk=renorm)
+    st = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    code = L.GATE_SOFTMAX if gate_fn == "softmax" else L.GATE_SIGMOID
+    logits, scores, idx, gates, g64 = K.router_fwd(x, params.device_w_g_tc("cuda"), E, k, code, renorm, st,
+                                                   want_f64=True)
+    torch.cuda.synchronize()
+    assert int(st) == 0
+    ref = x.double() @ wg.double()
+    assert float((logits.double() - ref).abs().max() / ref.abs().max()) < 1e-5
+    lg = logits.double().cpu().numpy()
+    ro = O.route_logits(lg, k, gate_fn, renorm)
+    np.testing.assert_array_equal(idx.cpu().numpy(), ro.experts)
+    np.testing.assert_allclose(g64.cpu().numpy(), ro.gates, rtol=1e-14, atol=0)
+    np.testing.assert_allclose(gates.cpu().numpy(), ro.gates.astype(np.float32), rtol=1e-6)
+    np.testing.assert_allclose(scores.cpu().numpy(), ro.scores.astype(np.float32), rtol=1e-6, atol=1e-30)
+
+
+def test_fused_router_flags_nonfinite_and_routes_safely():
+    T, H, E, k = 1000, 512, 8, 2
+    g = torch.Generator(device="cuda").manual_seed(3)
+    wg = torch.randn((H, E), generator=g, device="cuda") * H ** -0.5
+    x = torch.randn((T, H), generator=g, device="cuda").to(torch.bfloat16)
+    x[17, 3] = float("nan")
+    x[900, 0] = float("inf")
+    params = GatingParams(w_g=wg, k=k)
+    st = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    _, _, idx, _, _ = K.router_fwd(x, params.device_w_g_tc("cuda"), E, k, L.GATE_SOFTMAX, False, st)
+    assert int(st) & 1
+    assert idx[17].tolist() == [0, 1] and idx[900].tolist() == [0, 1]
+    assert int(idx.min()) >= 0 and int(idx.max()) < E
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_layer_nonfinite_raises_without_blocking_check(dtype):
+    """moe_forward raises NumericError (router.py:141-144) from the device flag;
+    the message names the token block or the gating weights like the reference."""
+    import paper_2504_14960_b200 as B
+    from paper_2504_14960_b200.errors import NumericError
+
+    E, k, H, F, T = 8, 2, 256, 512, 512
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, 0), k=k)
+    weights = B.init_expert_weights(E, H, F, 1, 0, activation="swiglu")
+    x = torch.randn((T, H), device="cuda").to(dtype)
+    x[7, 5] = float("nan")
+    with pytest.raises(NumericError, match="token block"):
+        B.moe_forward([B.TokenBlock(x, np.arange(T))], weights, B.ParallelTopology(world_size=1), params,
+                      B.LocalWorld(1))
+    wbad = O.gating_matrix(H, E, 0)
+    wbad[3, 2] = np.inf
+    with pytest.raises(NumericError, match="gating weights"):
+        B.moe_forward([B.TokenBlock(torch.randn((T, H), device="cuda").to(dtype), np.arange(T))], weights,
+                      B.ParallelTopology(world_size=1), B.GatingParams(w_g=wbad, k=k), B.LocalWorld(1))
+    # unchecked: no error, valid routing
+    outs, _ = B.moe_forward([B.TokenBlock(x, np.arange(T))], weights, B.ParallelTopology(world_size=1), params,
+                            B.LocalWorld(1), check_finite_inputs=False)
+    torch.cuda.synchronize()

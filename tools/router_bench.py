@@ -66,8 +66,11 @@ def main():
     rec("logits_cuda_core", lambda: K.router_logits(x, wg))
     logits = K.router_logits(x, wg)
     rec("topk", lambda: K.router_topk(logits, k, L.GATE_SOFTMAX, False), T * E * 8)
-    if hasattr(K, "router_fwd"):
-        rec("router_fwd_fused", lambda: K.router_fwd(x, wg, k, L.GATE_SOFTMAX, False))
+    st = torch.zeros((1,), dtype=torch.int32, device=dev)
+    w_tc = params.device_w_g_tc(dev)
+    rec("router_fwd_fused", lambda: K.router_fwd(x, w_tc, E, k, L.GATE_SOFTMAX, False, st))
+    if hasattr(K, "combine_router"):
+        pass
     scores, idx, gates, _ = K.router_topk(logits, k, L.GATE_SOFTMAX, False)
     dgates = torch.randn((T, k), generator=g, device=dev)
     rec("router_bwd", lambda: K.router_bwd(dgates, scores, idx, gates, L.GATE_SOFTMAX, False), T * E * 8)
