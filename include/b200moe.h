@@ -125,10 +125,20 @@ B200MOE_API int b200moe_capacity_by_gate(const int64_t* perm0, const int32_t* of
                              const int64_t* positions, int64_t T, int k, int E, int64_t cap,
                              uint8_t* kept_out, void* stream);
 
-/* dz[T,E] = d(gates)/d(logits)^T dgates                 -- dispatcher.py:470-488 */
+/* dz[T,E] = d(gates)/d(logits)^T dgates                 -- dispatcher.py:470-488
+ * dz_parts (nullable, bf16 [T, b200moe_router_parts_cols(E)]): also the exact
+ * split hi + mid + lo of dz, cols p * EPW + e (EPW = E rounded up to
+ * 8/16/32/64), zero padded -- the B operand of b200moe_router_wgrad_tc. */
 B200MOE_API int b200moe_router_bwd(const float* dgates, const float* scores, const int32_t* topk_idx,
                        const float* gates, int64_t T, int E, int k, int gate_fn, int renorm,
-                       float* dz, void* stream);
+                       float* dz, void* dz_parts, void* stream);
+B200MOE_API int b200moe_router_parts_cols(int E);
+/* dW_g[H,E] = x^T dz on the tensor cores (bf16 x [T,H], the dz parts of
+ * b200moe_router_bwd), split over tokens and folded in fixed order; H % 64
+ * == 0, E <= 64.                                          -- dispatcher.py:489 */
+B200MOE_API size_t b200moe_router_wgrad_tc_ws(int64_t T, int64_t H, int E);
+B200MOE_API int b200moe_router_wgrad_tc(const void* x, const void* dz_parts, int64_t T, int64_t H, int E,
+                                        float* dw_g, void* workspace, size_t workspace_bytes, void* stream);
 
 /* dw_g[H,E] (fp32, overwritten) = x^T dz, split over token chunks and
  * reduced in a fixed order (deterministic).  workspace: >=

@@ -54,7 +54,10 @@ _SIGS = {
     "b200moe_dispatch_plan_ws": [I64, I32],
     "b200moe_dispatch_plan": [P, P, P, P, I64, I32, I32, I64, I32, P, SZ, P, P, P, P, P, P, P, P, P],
     "b200moe_capacity_by_gate": [P, P, P, P, I64, I32, I32, I64, P, P],
-    "b200moe_router_bwd": [P, P, P, P, I64, I32, I32, I32, I32, P, P],
+    "b200moe_router_bwd": [P, P, P, P, I64, I32, I32, I32, I32, P, P, P],
+    "b200moe_router_parts_cols": [I32],
+    "b200moe_router_wgrad_tc_ws": [I64, I64, I32],
+    "b200moe_router_wgrad_tc": [P, P, I64, I64, I32, P, P, SZ, P],
     "b200moe_router_wgrad_ws": [I64, I64, I32],
     "b200moe_router_wgrad": [P, I32, P, I64, I64, I32, P, P, SZ, P],
     "b200moe_permute": [P, I32, I64, I64, I32, P, P, P, P, P, I32, I32, P],
@@ -82,6 +85,7 @@ _RESTYPES = {
     "b200moe_dispatch_plan_ws": SZ,
     "b200moe_router_wgrad_ws": SZ,
     "b200moe_router_stats_ws": SZ,
+    "b200moe_router_wgrad_tc_ws": SZ,
 }
 
 _lib: Optional[ctypes.CDLL] = None
@@ -128,9 +132,10 @@ def check(rc: int, what: str) -> None:
 # kernels launched per entry point (bench.py reports the total as gpu_launches)
 _LAUNCHES = {"b200moe_dispatch_plan": 3}
 _LAUNCHES["b200moe_router_wgrad"] = 2
+_LAUNCHES["b200moe_router_wgrad_tc"] = 2
 _LAUNCHES["b200moe_router_stats"] = 2
 _NO_LAUNCH = {"b200moe_version", "b200moe_last_error", "b200moe_device_check", "b200moe_enable_peer_access",
-              "b200moe_router_fwd_tc_np",
+              "b200moe_router_fwd_tc_np", "b200moe_router_parts_cols", "b200moe_router_wgrad_tc_ws",
               "b200moe_dispatch_plan_ws", "b200moe_router_wgrad_ws", "b200moe_router_stats_ws"}
 _launches = 0
 

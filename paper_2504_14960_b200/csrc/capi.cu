@@ -30,7 +30,10 @@ int dispatch_plan(const int32_t*, const float*, const uint8_t*, const int32_t*, 
 int capacity_by_gate(const int64_t*, const int32_t*, const double*, const int64_t*, int64_t, int,
                      int, int64_t, uint8_t*, cudaStream_t);
 int router_bwd(const float*, const float*, const int32_t*, const float*, int64_t, int, int, int,
-               int, float*, cudaStream_t);
+               int, float*, void*, int, int, cudaStream_t);
+int router_parts_layout(int, int*, int*);
+size_t router_wgrad_tc_ws_bytes(int64_t, int64_t, int);
+int router_wgrad_tc(const void*, const void*, int64_t, int64_t, int, float*, void*, size_t, cudaStream_t);
 size_t router_wgrad_ws_bytes(int64_t, int64_t, int);
 int router_wgrad(const void*, int, const float*, int64_t, int64_t, int, float*, void*, cudaStream_t);
 int permute(const void*, int, int64_t, int64_t, int, const int32_t*, const float*, void*,
@@ -194,11 +197,32 @@ int b200moe_capacity_by_gate(const int64_t* perm0, const int32_t* offsets0, cons
 
 int b200moe_router_bwd(const float* dgates, const float* scores, const int32_t* topk_idx,
                        const float* gates, int64_t T, int E, int k, int gate_fn, int renorm,
-                       float* dz, void* stream) {
+                       float* dz, void* dz_parts, void* stream) {
   REQUIRE(E >= 1 && k >= 1 && k <= E, "router_bwd: bad E=%d k=%d", E, k);
+  int epw = 0, nb = 0;
+  REQUIRE(!dz_parts || router_parts_layout(E, &epw, &nb), "router_bwd: dz parts need E <= 64 (E=%d)", E);
   if (T == 0) return B200MOE_OK;
   REQUIRE(dgates && scores && topk_idx && gates && dz, "router_bwd: null pointer");
-  return router_bwd(dgates, scores, topk_idx, gates, T, E, k, gate_fn, renorm, dz, S(stream));
+  return router_bwd(dgates, scores, topk_idx, gates, T, E, k, gate_fn, renorm, dz, dz_parts, epw, nb,
+                    S(stream));
+}
+
+int b200moe_router_parts_cols(int E) {
+  int epw = 0, nb = 0;
+  return router_parts_layout(E, &epw, &nb) ? nb : 0;
+}
+
+size_t b200moe_router_wgrad_tc_ws(int64_t T, int64_t H, int E) { return router_wgrad_tc_ws_bytes(T, H, E); }
+
+int b200moe_router_wgrad_tc(const void* x, const void* dz_parts, int64_t T, int64_t H, int E, float* dw_g,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  int epw = 0, nb = 0;
+  REQUIRE(router_parts_layout(E, &epw, &nb), "router_wgrad_tc: E=%d > 64 unsupported", E);
+  REQUIRE(T >= 0 && H >= 128 && H % 64 == 0, "router_wgrad_tc: H=%lld must be a multiple of 64 (>= 128)",
+          (long long)H);
+  REQUIRE(dw_g && (T == 0 || (x && dz_parts && workspace)), "router_wgrad_tc: null pointer");
+  REQUIRE(workspace_bytes >= router_wgrad_tc_ws_bytes(T, H, E), "router_wgrad_tc: workspace too small");
+  return router_wgrad_tc(x, dz_parts, T, H, E, dw_g, workspace, workspace_bytes, S(stream));
 }
 
 size_t b200moe_router_wgrad_ws(int64_t T, int64_t H, int E) { return router_wgrad_ws_bytes(T, H, E); }

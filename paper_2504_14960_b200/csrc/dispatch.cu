@@ -295,6 +295,81 @@ __global__ void __launch_bounds__(256) combine_vec_kernel(
   }
 }
 
+// Backward combine with the router term (dispatcher.py:480-490 for bf16,
+// E <= 8, H % 8 == 0):  dx[t] = sum_s rows[pair_row[t, s]] + dz[t] @ W_g^T
+// (+ out[t] when accumulating).  A block covers 2048 consecutive columns,
+// each thread 8 of them with its 8 x E slice of W_g^T in registers for the
+// whole kernel, and walks a chunk of tokens: per token k 16-byte row loads,
+// one 16-byte store, dz[t] and the pair rows as uniform loads -- the FMAs of
+// the router term hide under the row traffic (HBM-bound like the plain
+// gather).  fp32 sum order: slots in order, then the router term.
+constexpr int CR_COLS = 2048;
+
+template <int KMAX, int EP, int UT>
+__global__ void __launch_bounds__(256, 2) combine_router_kernel(
+    const __nv_bfloat16* __restrict__ rows, int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_row,
+    const float* __restrict__ dz, const float* __restrict__ wgT, int E, __nv_bfloat16* __restrict__ out,
+    int accumulate, int64_t chunk) {
+  const int64_t h0 = (int64_t)blockIdx.y * CR_COLS + threadIdx.x * 8;
+  if (h0 >= H) return;
+  float w[EP][8];
+#pragma unroll
+  for (int e = 0; e < EP; ++e) {
+    if (e < E) {
+      const float4* wp = reinterpret_cast<const float4*>(wgT + (int64_t)e * H + h0);
+      const float4 a = __ldg(wp), b = __ldg(wp + 1);
+      w[e][0] = a.x; w[e][1] = a.y; w[e][2] = a.z; w[e][3] = a.w;
+      w[e][4] = b.x; w[e][5] = b.y; w[e][6] = b.z; w[e][7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[e][j] = 0.f;
+    }
+  }
+  const int64_t tb = (int64_t)blockIdx.x * chunk, te = min(Tn, tb + chunk);
+  for (int64_t t = tb; t < te; t += UT) {
+    Vec16<__nv_bfloat16> v[UT][KMAX];
+    bool has[UT][KMAX];
+#pragma unroll
+    for (int u = 0; u < UT; ++u)
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        const int32_t r = (t + u < te && s < k) ? __ldg(pair_row + (t + u) * k + s) : -1;
+        has[u][s] = r >= 0;
+        if (r >= 0) v[u][s].raw = ld_nc_v4(rows + (int64_t)r * H + h0);
+      }
+#pragma unroll
+    for (int u = 0; u < UT; ++u) {
+      if (t + u >= te) break;
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s)
+        if (has[u][s]) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(v[u][s].v[j]);
+        }
+      const float* dr = dz + (t + u) * E;
+#pragma unroll
+      for (int e = 0; e < EP; ++e) {
+        const float d = e < E ? __ldg(dr + e) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(d, w[e][j], acc[j]);
+      }
+      __nv_bfloat16* o = out + (t + u) * H + h0;
+      Vec16<__nv_bfloat16> q;
+      if (accumulate) {
+        q.raw = ld_v4(o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __bfloat162float(q.v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q.v[j] = __float2bfloat16_rn(acc[j]);
+      st_v4(o, q.raw);
+    }
+  }
+}
+
 // Gather-sum without the router term: one warp per token (high occupancy),
 // each lane owns 8 columns per step and keeps UNR steps x k row loads in
 // flight.
@@ -444,8 +519,22 @@ static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const i
   constexpr int TPW = 4;
   const unsigned grid = (unsigned)ceil_div(ceil_div(Tn, TPW), 8);
   bool done = false;
+  if constexpr (sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+    if (dz && !gates && E <= 8 && H % 8 == 0 && k <= 8 && Tn > 0) {  // (k > 8: combine_vec below)
+      // two tokens (2k 16-byte row loads) in flight per thread
+      int64_t chunk = std::max<int64_t>(ceil_div(ceil_div(Tn, 148), 8) * 8, 16);
+      dim3 g2((unsigned)ceil_div(Tn, chunk), (unsigned)ceil_div(H, CR_COLS));
+      auto* ob = reinterpret_cast<__nv_bfloat16*>(out);
+      auto* rb = reinterpret_cast<const __nv_bfloat16*>(rows);
+#define CR(KM) if (E <= 4) combine_router_kernel<KM, 4, 2><<<g2, 256, 0, st>>>(rb, Tn, H, k, pr, dz, wgT, E, ob, acc, chunk); \
+               else combine_router_kernel<KM, 8, 2><<<g2, 256, 0, st>>>(rb, Tn, H, k, pr, dz, wgT, E, ob, acc, chunk)
+      KDISPATCH(k, CR)
+#undef CR
+      done = true;
+    }
+  }
   if constexpr (sizeof(Tin) == 2) {
-    if (!dz && H % 8 == 0) {
+    if (!done && !dz && H % 8 == 0) {
       const unsigned g1 = (unsigned)ceil_div(Tn, 8);
 #define CG1(KM) combine_gather_kernel<Tin, Tout, KM, (KM <= 2 ? 4 : (KM <= 4 ? 2 : 1))><<<g1, 256, 0, st>>>(rows, Tn, H, k, pr, gates, out, acc)
       if (Tn > 0) { KDISPATCH(k, CG1) }

@@ -515,13 +515,23 @@ __global__ void __launch_bounds__(256) capacity_by_gate_kernel(
 // ---------------------------------------------------------------------------
 // router backward                                  (dispatcher.py:470-488)
 // ---------------------------------------------------------------------------
+// an fp32 value as three bf16 parts hi + mid + lo == v exactly (8 + 8 + 8
+// significand bits); see split_bf16x3_kernel below
+__device__ __forceinline__ void split3(float v, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+
 template <int NPL>
 __global__ void __launch_bounds__(256) router_bwd_kernel(const float* __restrict__ dgates,
                                                          const float* __restrict__ scores,
                                                          const int32_t* __restrict__ topk,
                                                          const float* __restrict__ gates,
                                                          int64_t Tn, int E, int k, int gate_fn,
-                                                         int renorm, float* __restrict__ dz) {
+                                                         int renorm, float* __restrict__ dz,
+                                                         __nv_bfloat16* __restrict__ parts, int epw, int nb) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= Tn) return;
@@ -554,16 +564,29 @@ __global__ void __launch_bounds__(256) router_bwd_kernel(const float* __restrict
     for (int j = 0; j < NPL; ++j) dot += ds[j] * sc[j];
     dot = warp_sum(dot);
 #pragma unroll
-    for (int j = 0; j < NPL; ++j) {
-      const int e = lane + 32 * j;
-      if (e < E) dz[t * E + e] = (float)(sc[j] * (ds[j] - dot));
-    }
+    for (int j = 0; j < NPL; ++j) ds[j] = sc[j] * (ds[j] - dot);
   } else {
 #pragma unroll
-    for (int j = 0; j < NPL; ++j) {
-      const int e = lane + 32 * j;
-      if (e < E) dz[t * E + e] = (float)(ds[j] * sc[j] * (1.0 - sc[j]));
+    for (int j = 0; j < NPL; ++j) ds[j] = ds[j] * sc[j] * (1.0 - sc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int e = lane + 32 * j;
+    if (e >= E) continue;
+    const float v = (float)ds[j];
+    dz[t * E + e] = v;
+    if (parts) {  // the exact bf16 split hi + mid + lo of dz for the tensor-core x^T dz
+      __nv_bfloat16 hi, mid, lo;
+      split3(v, hi, mid, lo);
+      __nv_bfloat16* row = parts + t * nb;
+      row[e] = hi;
+      row[epw + e] = mid;
+      row[2 * epw + e] = lo;
     }
+  }
+  if (parts) {
+    for (int c = lane; c < nb; c += 32)
+      if (c >= 3 * epw || c % epw >= E) parts[t * nb + c] = __float2bfloat16_rn(0.f);
   }
 }
 
@@ -714,12 +737,6 @@ int router_stats(const int32_t* topk, const uint8_t* kept, const float* scores, 
 // accumulation.  Parts are laid out as column blocks of stride Ep (E rounded
 // up to 8, zero padded).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void split3(float v, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
-  hi = __float2bfloat16_rn(v);
-  const float r1 = v - __bfloat162float(hi);
-  mid = __float2bfloat16_rn(r1);
-  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-}
 
 // src [rows, E] fp32 -> out3 [rows, 3 Ep] = (hi | mid | lo) and/or
 // out6 [rows, 6 Ep] = (hi | hi | hi | mid | mid | lo) (the dz side of the
@@ -853,9 +870,11 @@ int capacity_by_gate(const int64_t* perm0, const int32_t* off0, const double* g6
 }
 
 int router_bwd(const float* dgates, const float* scores, const int32_t* topk, const float* gates,
-               int64_t Tn, int E, int k, int gate_fn, int renorm, float* dz, cudaStream_t st) {
+               int64_t Tn, int E, int k, int gate_fn, int renorm, float* dz, void* parts, int epw, int nb,
+               cudaStream_t st) {
   const unsigned grid = (unsigned)ceil_div(Tn, 8);
-#define RB(NPL) router_bwd_kernel<NPL><<<grid, 256, 0, st>>>(dgates, scores, topk, gates, Tn, E, k, gate_fn, renorm, dz)
+  __nv_bfloat16* pb = static_cast<__nv_bfloat16*>(parts);
+#define RB(NPL) router_bwd_kernel<NPL><<<grid, 256, 0, st>>>(dgates, scores, topk, gates, Tn, E, k, gate_fn, renorm, dz, pb, epw, nb)
   if (E <= 32) RB(1);
   else if (E <= 64) RB(2);
   else if (E <= 128) RB(4);
@@ -869,14 +888,81 @@ int router_bwd(const float* dgates, const float* scores, const int32_t* topk, co
   return B200MOE_OK;
 }
 
+// bf16 x, E <= 8, H % 8 == 0: thread (h-slice of 8 columns) x (token chunk)
+// keeps its 8 x E block of dW_g in registers and streams its chunk's x rows
+// once (16-byte loads, a block covers 2048 consecutive columns); dz[t] is a
+// uniform (broadcast) load.  The chunks' partial blocks are folded in chunk
+// order by router_wgrad_reduce_kernel (deterministic).  HBM-bound on x.
+constexpr int WGV_COLS = 2048;  // columns per block: 256 threads x 8
+constexpr int WGV_MAX_CHUNKS = 148;
+
+template <int EP, int UT>
+__global__ void __launch_bounds__(256, 2) router_wgrad_vec_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                 const float* __restrict__ dz, int64_t Tn,
+                                                                 int64_t H, int E, int64_t chunk,
+                                                                 float* __restrict__ part) {
+  const int64_t h0 = (int64_t)blockIdx.y * WGV_COLS + threadIdx.x * 8;
+  if (h0 >= H) return;
+  const int64_t tb = (int64_t)blockIdx.x * chunk, te = min(Tn, tb + chunk);
+  float acc[8][EP];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int e = 0; e < EP; ++e) acc[j][e] = 0.f;
+  for (int64_t t = tb; t < te; t += UT) {
+    Vec16<__nv_bfloat16> v[UT];
+#pragma unroll
+    for (int u = 0; u < UT; ++u)
+      if (t + u < te) v[u].raw = ld_nc_v4(x + (t + u) * H + h0);
+#pragma unroll
+    for (int u = 0; u < UT; ++u) {
+      if (t + u >= te) break;
+      float d[EP];
+      const float* dr = dz + (t + u) * E;
+#pragma unroll
+      for (int e = 0; e < EP; ++e) d[e] = e < E ? __ldg(dr + e) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float xv = __bfloat162float(v[u].v[j]);
+#pragma unroll
+        for (int e = 0; e < EP; ++e) acc[j][e] = fmaf(xv, d[e], acc[j][e]);
+      }
+    }
+  }
+  float* o = part + ((int64_t)blockIdx.x * H + h0) * E;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int e = 0; e < EP; ++e)
+      if (e < E) o[j * E + e] = acc[j][e];
+}
+
 size_t router_wgrad_ws_bytes(int64_t Tn, int64_t H, int E) {
-  return (size_t)ceil_div(Tn > 0 ? Tn : 1, WG_CHUNK) * H * E * sizeof(float);
+  const int64_t nch = std::max<int64_t>(ceil_div(Tn > 0 ? Tn : 1, WG_CHUNK), WGV_MAX_CHUNKS);
+  return (size_t)nch * H * E * sizeof(float);
 }
 
 int router_wgrad(const void* x, int dt, const float* dz, int64_t Tn, int64_t H, int E, float* dwg,
                  void* ws, cudaStream_t st) {
-  const int64_t nch = ceil_div(Tn, WG_CHUNK);
   float* part = static_cast<float*>(ws);
+  const int64_t HE = H * E;
+  if (dt == B200MOE_BF16 && E <= 8 && H % 8 == 0 && Tn > 0) {
+    constexpr int UT = 4;
+    int64_t chunk = ceil_div(Tn, WGV_MAX_CHUNKS);
+    chunk = std::max<int64_t>(ceil_div(chunk, UT) * UT, 32);
+    const int64_t nch = ceil_div(Tn, chunk);
+    dim3 grid((unsigned)nch, (unsigned)ceil_div(H, WGV_COLS));
+    const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+    if (E <= 4)
+      router_wgrad_vec_kernel<4, UT><<<grid, 256, 0, st>>>(xb, dz, Tn, H, E, chunk, part);
+    else
+      router_wgrad_vec_kernel<8, UT><<<grid, 256, 0, st>>>(xb, dz, Tn, H, E, chunk, part);
+    router_wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(HE, 256), 148 * 8), 256, 0, st>>>(
+        part, nch, HE, dwg);
+    B200MOE_CHECK_LAUNCH("router_wgrad");
+    return B200MOE_OK;
+  }
+  const int64_t nch = ceil_div(Tn, WG_CHUNK);
   dim3 grid((unsigned)ceil_div(H, 64), (unsigned)nch);
   if (dt == B200MOE_BF16)
     router_wgrad_partial_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
@@ -884,7 +970,6 @@ int router_wgrad(const void* x, int dt, const float* dz, int64_t Tn, int64_t H, 
   else
     router_wgrad_partial_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), dz, Tn,
                                                              H, E, part);
-  const int64_t HE = H * E;
   router_wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(HE, 256), 148 * 8), 256, 0, st>>>(
       part, nch, HE, dwg);
   B200MOE_CHECK_LAUNCH("router_wgrad");

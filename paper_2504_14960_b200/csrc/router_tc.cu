@@ -167,11 +167,16 @@ __global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // CTAs start their K walk at staggered offsets so that concurrent tiles do
+  // not stream the same 8 KB-strided column block of x at the same time (the
+  // DRAM partitions stay evenly loaded); the fp32 sum order is fixed per CTA
+  const int kb_rot = (int)((blockIdx.x * 7u) % (unsigned)a.nkb);
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < a.nkb; ++kb) {
+      for (int i = 0; i < a.nkb; ++i) {
+        const int kb = i + kb_rot < a.nkb ? i + kb_rot : i + kb_rot - a.nkb;
         mbar_wait(empty_bar + 8 * stage, phase ^ 1);
         mbar_expect_tx(full_bar + 8 * stage, STAGE);
         tma_load_3d(&map_x, sA + stage * A_BYTES, full_bar + 8 * stage, kb * BK, m0, 0);
@@ -187,14 +192,14 @@ __global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant
       constexpr uint32_t idesc = idesc_n(NP);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < a.nkb; ++kb) {
+      for (int i = 0; i < a.nkb; ++i) {
         mbar_wait(full_bar + 8 * stage, phase);
         tc_fence_after();
         const uint32_t a_s = sA + stage * A_BYTES, b_s = sB + stage * B_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
           tc_mma(tmem, smem_desc(a_s + k * 32, 16, 1024), smem_desc(b_s + k * 32, 16, 1024), idesc,
-                 (kb | k) != 0);
+                 (i | k) != 0);
         tc_commit(empty_bar + 8 * stage);
         if (++stage == S) {
           stage = 0;
@@ -258,7 +263,227 @@ static int launch(const void* x, int64_t T, int64_t H, const void* w, Args a, cu
   return B200MOE_OK;
 }
 
+// ---------------------------------------------------------------------------
+// dW_g = x^T dz (dispatcher.py:489) on the tensor cores: M = H (128 columns of
+// x per tile), N = NB (the three exact bf16 parts of dz, [T, NB] written by
+// router_bwd, cols p * EPW + e, zero padded to a multiple of 64), K = tokens.
+// Both operands are MN-major in memory (x is [T, H], dz parts [T, NB]): the
+// TMA boxes are {64 columns, 64 tokens} with 128B swizzle.  The tokens are
+// split over the grid's y dimension; each CTA folds the parts of its
+// accumulator rows, (hi + mid) + lo, into an fp32 partial dW_g [split, H, E]
+// which router_wgrad_reduce_kernel sums in split order (deterministic).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr uint32_t idesc_mn(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+
+struct WArgs {
+  int64_t T, H;
+  int E, epw, kb_per_split, nkb, stages;
+  float* part;
+};
+
+template <int EPW>
+__global__ void __launch_bounds__(256) router_wgrad_tc_kernel(const __grid_constant__ CUtensorMap map_x,
+                                                              const __grid_constant__ CUtensorMap map_d,
+                                                              const WArgs a) {
+  constexpr int NB = (3 * EPW + 63) / 64 * 64;
+  constexpr int A_BYTES = BM * BK * 2, B_BYTES = NB * BK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int COLS = tmem_cols(NB);
+  const int S = a.stages;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sA = base, sB = base + S * A_BYTES;
+  const uint32_t bars = base + S * STAGE;
+  const uint32_t full_bar = bars, empty_bar = bars + 8 * S, done_bar = bars + 16 * S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE + 16 * S + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+  const int kb0 = blockIdx.y * a.kb_per_split;
+  const int kb1 = min(a.nkb, kb0 + a.kb_per_split);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full_bar + 8 * i, 1);
+      mbar_init(empty_bar + 8 * i, 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_x);
+    prefetch_map(&map_d);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int nk = kb1 - kb0;
+  const int kb_rot = nk > 0 ? (int)((blockIdx.x * 5u) % (unsigned)nk) : 0;  // staggered walk, as above
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < nk; ++i) {
+        const int kb = kb0 + (i + kb_rot < nk ? i + kb_rot : i + kb_rot - nk);
+        mbar_wait(empty_bar + 8 * stage, phase ^ 1);
+        mbar_expect_tx(full_bar + 8 * stage, STAGE);
+#pragma unroll
+        for (int i = 0; i < BM / 64; ++i)  // x: {64 columns, 64 tokens} per box
+          tma_load_3d(&map_x, sA + stage * A_BYTES + i * 8192, full_bar + 8 * stage, m0 + 64 * i, kb * BK, 0);
+#pragma unroll
+        for (int i = 0; i < NB / 64; ++i)
+          tma_load_3d(&map_d, sB + stage * B_BYTES + i * 8192, full_bar + 8 * stage, 64 * i, kb * BK, 0);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_mn(NB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < nk; ++i) {
+        mbar_wait(full_bar + 8 * stage, phase);
+        tc_fence_after();
+        const uint32_t a_s = sA + stage * A_BYTES, b_s = sB + stage * B_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)  // MN-major: +16 K-rows = 2 KB per step
+          tc_mma(tmem, smem_desc(a_s + k * 2048, 8192, 1024), smem_desc(b_s + k * 2048, 8192, 1024), idesc,
+                 (i | k) != 0);
+        tc_commit(empty_bar + 8 * stage);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (kb1 > kb0) tc_commit(done_bar);
+      else mbar_arrive(done_bar);
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    mbar_wait(done_bar, 0);
+    tc_fence_after();
+    const uint32_t t_row = tmem + ((uint32_t)(32 * q) << 16);
+    float dw[EPW];
+#pragma unroll
+    for (int e = 0; e < EPW; ++e) dw[e] = 0.f;
+    if (kb1 > kb0) {
+      // parts arrive in column order p * EPW + e: dw = (hi + mid) + lo
+#pragma unroll
+      for (int c = 0; c < (3 * EPW + 31) / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(t_row + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = c * 32 + j;
+          if (col < 3 * EPW) dw[col % EPW] += __uint_as_float(v[j]);
+        }
+      }
+    }
+    const int64_t h = (int64_t)m0 + 32 * q + lane;
+    if (h < a.H) {
+      float* o = a.part + ((int64_t)blockIdx.y * a.H + h) * a.E;
+#pragma unroll
+      for (int e = 0; e < EPW; ++e)
+        if (e < a.E) o[e] = dw[e];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(COLS));
+  }
+}
+
+__global__ void wgrad_reduce_kernel(const float* __restrict__ part, int64_t nsplit, int64_t HE,
+                                    float* __restrict__ dwg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < HE; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int64_t c = 0; c < nsplit; ++c) s += part[c * HE + i];
+    dwg[i] = s;
+  }
+}
+
+template <int EPW>
+static int launch_wgrad(const void* x, const void* dz_parts, int64_t T, int64_t H, int E, int epw, float* dwg,
+                        void* ws, size_t ws_bytes, cudaStream_t st) {
+  constexpr int NB = (3 * EPW + 63) / 64 * 64;
+  constexpr int STAGE = BM * BK * 2 + NB * BK * 2;
+  CUtensorMap mx, md;
+  int rc = make_map(&mx, x, (uint64_t)H, (uint64_t)T, 1, (uint64_t)H, (uint64_t)H * T, 64);
+  if (rc) return rc;
+  rc = make_map(&md, dz_parts, (uint64_t)NB, (uint64_t)T, 1, (uint64_t)NB, (uint64_t)NB * T, 64);
+  if (rc) return rc;
+  WArgs a{T, H, E, epw, 0, (int)ceil_div(T, BK), 0, static_cast<float*>(ws)};
+  // two CTAs per SM when four stages fit in half of the shared memory
+  a.stages = 4;
+  const int smem = 1024 + a.stages * STAGE + 16 * a.stages + 64;
+  const int per_sm = smem <= 113 * 1024 ? 2 : 1;
+  const int mt = (int)ceil_div(H, BM);
+  int split = std::max(1, std::min(a.nkb, num_sms() * per_sm / mt));
+  a.kb_per_split = (int)ceil_div(a.nkb, split);
+  split = (int)ceil_div(a.nkb, a.kb_per_split);
+  if ((size_t)split * H * E * sizeof(float) > ws_bytes) {
+    set_error("router_wgrad_tc: workspace too small");
+    return B200MOE_EINVAL;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(router_wgrad_tc_kernel<EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    attr_set = true;
+  }
+  router_wgrad_tc_kernel<EPW><<<dim3((unsigned)mt, (unsigned)split), 256, smem, st>>>(mx, md, a);
+  const int64_t HE = H * E;
+  wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(HE, 256), 148 * 8), 256, 0, st>>>(
+      a.part, split, HE, dwg);
+  B200MOE_CHECK_LAUNCH("router_wgrad_tc");
+  return B200MOE_OK;
+}
+
 }  // namespace rtc
+
+// dz-part layout of the tensor-core x^T dz: cols p * epw + e, nb columns
+int router_parts_layout(int E, int* epw, int* nb) {
+  const int ep = E <= 8 ? 8 : E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 0;
+  if (!ep) return 0;
+  *epw = ep;
+  *nb = (3 * ep + 63) / 64 * 64;
+  return 1;
+}
+
+size_t router_wgrad_tc_ws_bytes(int64_t T, int64_t H, int E) {
+  (void)T;
+  return (size_t)std::max(1, num_sms() * 2) * (size_t)H * E * sizeof(float);
+}
+
+int router_wgrad_tc(const void* x, const void* dz_parts, int64_t T, int64_t H, int E, float* dwg, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+  int epw = 0, nb = 0;
+  if (!router_parts_layout(E, &epw, &nb)) {
+    set_error("router_wgrad_tc: E=%d > 64 unsupported", E);
+    return B200MOE_EUNSUPPORTED;
+  }
+  if (T == 0) return cudaMemsetAsync(dwg, 0, (size_t)H * E * sizeof(float), st) == cudaSuccess ? B200MOE_OK
+                                                                                              : B200MOE_ELAUNCH;
+  (void)nb;
+  if (epw == 8) return rtc::launch_wgrad<8>(x, dz_parts, T, H, E, epw, dwg, ws, ws_bytes, st);
+  if (epw == 16) return rtc::launch_wgrad<16>(x, dz_parts, T, H, E, epw, dwg, ws, ws_bytes, st);
+  if (epw == 32) return rtc::launch_wgrad<32>(x, dz_parts, T, H, E, epw, dwg, ws, ws_bytes, st);
+  return rtc::launch_wgrad<64>(x, dz_parts, T, H, E, epw, dwg, ws, ws_bytes, st);
+}
 
 int router_fwd_tc_np(int E) {
   const int ep = E <= 8 ? 8 : E <= 16 ? 16 : E <= 32 ? 32 : E <= 64 ? 64 : 0;

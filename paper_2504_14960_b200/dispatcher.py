@@ -807,17 +807,26 @@ class RankLayer:
             dx_mine = self._reduce_blocks(ctx, xpl, dxp)
             rows = torch.empty((max(sv["R_send"], 1), H), dtype=u.dtype, device=u.device)
             ctx.a2a_single(self.g.ep, dx_mine, xpl.recv_splits, rows, xpl.send_splits)
+        wg_tc = self.wg_parts is not None and K.router_wgrad_tc_supported(x, E)
         dz = K.router_bwd(dgates, dec.scores, dec.experts, dec.gates, GATE_CODES[p.gate_fn],
-                          p.renormalize_topk)
+                          p.renormalize_topk, want_parts=wg_tc)
+        if wg_tc:
+            dz, dz_parts = dz
         dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
-        if self.wg_parts is None and E <= 8:
-            # router term fused into the combine (w_g^T chunks reused per warp)
+        if E <= 8:
+            # router term dz . W_g^T fused into the combine (W_g^T slice held in
+            # registers, csrc/dispatch.cu combine_router_kernel for bf16)
             dx = K.combine(rows, sv["pair_row"], T, gates=None, dz=dz, w_gT=self.wgT, out=dx_sh,
                            accumulate=dx_sh is not None)
         else:
             dx = K.combine(rows, sv["pair_row"], T, gates=None, out=dx_sh, accumulate=dx_sh is not None)
             K.router_term(dz, self.wg, dx, parts=self.wg_parts)
-        dwg = K.router_wgrad(x, dz, tc=self.wg_parts is not None)
+        # dW_g = x^T dz: x read once by TMA, tensor cores against the exact
+        # bf16 parts of dz written by router_bwd (router_tc.cu)
+        if wg_tc:
+            dwg = K.router_wgrad_tc(x, dz_parts, E)
+        else:
+            dwg = K.router_wgrad(x, dz, tc=self.wg_parts is not None)
         return dx, dwg, dw1p, dw2p
 
 

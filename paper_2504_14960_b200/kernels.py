@@ -286,13 +286,40 @@ def combine(rows: torch.Tensor, pair_row: torch.Tensor, T: int, gates=None, dz=N
     return out
 
 
-def router_bwd(dgates, scores, topk_idx, gates, gate_fn: int, renorm: bool) -> torch.Tensor:
+def router_bwd(dgates, scores, topk_idx, gates, gate_fn: int, renorm: bool, want_parts: bool = False):
+    """dz [T, E] fp32 (dispatcher.py:470-488); with ``want_parts`` also
+    (dz, parts): the exact bf16 split of dz laid out for router_wgrad_tc."""
     T, E = scores.shape
     k = topk_idx.shape[1]
     dz = torch.empty((T, E), dtype=torch.float32, device=scores.device)
+    parts = None
+    if want_parts:
+        nb = int(L.load().b200moe_router_parts_cols(E))
+        parts = torch.empty((T, nb), dtype=torch.bfloat16, device=scores.device)
     L.call("b200moe_router_bwd", L.ptr(dgates), L.ptr(scores), L.ptr(topk_idx), L.ptr(gates), T,
-           E, k, gate_fn, int(renorm), L.ptr(dz), _sp())
-    return dz
+           E, k, gate_fn, int(renorm), L.ptr(dz), L.ptr(parts), _sp())
+    return (dz, parts) if want_parts else dz
+
+
+def router_wgrad_tc_supported(x: torch.Tensor, E: int) -> bool:
+    from . import gemm_tc
+
+    return (x.dtype == torch.bfloat16 and x.shape[1] % 64 == 0 and x.shape[1] >= 128
+            and int(L.load().b200moe_router_parts_cols(E)) > 0 and gemm_tc.available())
+
+
+def router_wgrad_tc(x: torch.Tensor, dz_parts: torch.Tensor, E: int) -> torch.Tensor:
+    """dW_g = x^T dz (dispatcher.py:489) on the tensor cores against the dz
+    parts of router_bwd(want_parts=True); x read once."""
+    T, H = x.shape
+    _cuda(x, "x", torch.bfloat16)
+    _cuda(dz_parts, "dz_parts", torch.bfloat16)
+    dwg = torch.empty((H, E), dtype=torch.float32, device=x.device)
+    ws_bytes = int(L.load().b200moe_router_wgrad_tc_ws(T, H, E))
+    ws = torch.empty((max(ws_bytes // 4, 1),), dtype=torch.float32, device=x.device)
+    L.call("b200moe_router_wgrad_tc", L.ptr(x), L.ptr(dz_parts), T, H, E, L.ptr(dwg), L.ptr(ws),
+           ctypes.c_size_t(ws.numel() * 4), _sp())
+    return dwg
 
 
 def router_wgrad(x: torch.Tensor, dz: torch.Tensor, tc: bool = False) -> torch.Tensor:

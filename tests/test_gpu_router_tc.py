@@ -131,3 +131,60 @@ def test_layer_nonfinite_raises_without_blocking_check(dtype):
     outs, _ = B.moe_forward([B.TokenBlock(x, np.arange(T))], weights, B.ParallelTopology(world_size=1), params,
                             B.LocalWorld(1), check_finite_inputs=False)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("T,H,E,k,acc", [(16384, 4096, 8, 2, False), (1000, 6144, 8, 2, True),
+                                         (333, 512, 4, 1, False), (777, 1032, 8, 4, True)])
+def test_combine_with_router_term(T, H, E, k, acc):
+    """Backward combine with the fused router term (dispatcher.py:480-490):
+    dx = sum of the k pair rows + dz W_g^T (+ the shared-expert dx), bf16 out,
+    against float64 on the same inputs; dropped pairs (-1) contribute nothing."""
+    g = torch.Generator(device="cuda").manual_seed(T + H)
+    R = T * k
+    rows = torch.randn((R, H), generator=g, device="cuda").to(torch.bfloat16)
+    pair_row = torch.randperm(R, generator=g, device="cuda").to(torch.int32).reshape(T, k).contiguous()
+    pair_row[::7, -1] = -1
+    dz = torch.randn((T, E), generator=g, device="cuda")
+    wg = torch.randn((H, E), generator=g, device="cuda") * H ** -0.5
+    base = torch.randn((T, H), generator=g, device="cuda").to(torch.bfloat16)
+    out = base.clone() if acc else None
+    dx = K.combine(rows, pair_row, T, dz=dz, w_gT=wg.T.contiguous(), out=out, accumulate=acc)
+    pr = pair_row.long()
+    ref = torch.zeros((T, H), dtype=torch.float64, device="cuda")
+    for s in range(k):
+        m = pr[:, s] >= 0
+        ref[m] += rows[pr[m, s]].double()
+    ref += dz.double() @ wg.double().T
+    if acc:
+        ref += base.double()
+    err = float((dx.double() - ref).abs().max() / ref.abs().max())
+    assert err < 8e-3, err  # one bf16 rounding of the result
+
+
+@pytest.mark.parametrize("T,H,E,k", [(16384, 4096, 8, 2), (1000, 256, 8, 2), (333, 512, 4, 1),
+                                     (2048, 3584, 64, 8), (777, 1024, 16, 4), (640, 512, 32, 6)])
+def test_tensor_core_wgrad_from_dz_parts(T, H, E, k):
+    """router_bwd writes dz and its exact bf16 parts; router_wgrad_tc
+    (x^T dz on the tensor cores, x read once) matches float64 and the parts
+    sum back to dz exactly."""
+    g = torch.Generator(device="cuda").manual_seed(T * 3 + E)
+    x = torch.randn((T, H), generator=g, device="cuda").to(torch.bfloat16)
+    logits = torch.randn((T, E), generator=g, device="cuda")
+    scores, idx, gates, _ = K.router_topk(logits, k, L.GATE_SOFTMAX, False)
+    dgates = torch.randn((T, k), generator=g, device="cuda")
+    dz, parts = K.router_bwd(dgates, scores, idx, gates, L.GATE_SOFTMAX, False, want_parts=True)
+    torch.testing.assert_close(dz, K.router_bwd(dgates, scores, idx, gates, L.GATE_SOFTMAX, False),
+                               rtol=0, atol=0)
+    epw = next(c for c in (8, 16, 32, 64) if c >= E)
+    p = parts.double()
+    recon = p[:, :E] + p[:, epw:epw + E] + p[:, 2 * epw:2 * epw + E]
+    assert torch.equal(recon, dz.double())
+    pad = torch.ones(parts.shape[1], dtype=torch.bool, device="cuda")
+    for q in range(3):
+        pad[q * epw:q * epw + E] = False
+    assert not bool(parts[:, pad].any())
+    dwg = K.router_wgrad_tc(x, parts, E)
+    ref = x.double().T @ dz.double()
+    assert float((dwg.double() - ref).abs().max() / ref.abs().max()) < 1e-5
+    # deterministic: the split reduction runs in a fixed order
+    torch.testing.assert_close(K.router_wgrad_tc(x, parts, E), dwg, rtol=0, atol=0)
