@@ -500,22 +500,29 @@ def main():
         px_last = sv_last.get("peer")
         dedup = bool(px_last is not None and px_last.dedup)
         if dedup:
-            # one row per (token, destination EP index) crosses the link
+            # one row per (token, remote EP index) crosses the link; rows for
+            # this rank's own EP index stay per pair (also to its ETP
+            # siblings, ep_peer.cu dispatch)
             dec = sv_last["dec"]
             dst = (dec.experts.to(torch.int64) // (E // ep)).masked_fill(~dec.kept.bool(), -1)
             per_dst = torch.stack([(dst == j).any(1).sum() for j in range(ep)]).cpu().tolist()
-            pushed_rows = sum(c * (etp - (1 if j == e_idx else 0)) for j, c in enumerate(per_dst))
+            pushed_rows = sum(c * etp for j, c in enumerate(per_dst) if j != e_idx) + \
+                per_ep[e_idx] * (etp - 1)
         remote = 2 * pushed_rows * H * 2
         allc = [torch.empty_like(cnt) for _ in range(world)]
         dist.all_gather(allc, cnt)
         job_wire = wire_rows([c.reshape(ep, -1).cpu().numpy() for c in allc], topo) * H * 2
         t_x = sum(m for _, m in peer_events) / 1e3
+        t_expand = sum(m for n_, m in all_launches if n_ == "ep_expand") / 1e3
         # launch order within a step: forward push (x), then backward push
         # (g*u, with the dgate dots against the returned rows)
         per_dir = {f"{d}_gbs": remote / 2 / (m / 1e3) / 1e9
                    for d, (_, m) in zip(("forward", "backward"), peer_events)} if len(peer_events) == 2 else None
         a2a = {"busbw_gbs": remote / t_x / 1e9, "nominal_gbs": 900.0,
-               "frac_nominal": remote / t_x / 1e9 / 900.0, "ms_per_step": t_x * 1e3,
+               "frac_nominal": remote / t_x / 1e9 / 900.0,
+               # measured peer-copy reference of this pool (B200_PROFILING.md): 770 GB/s per direction
+               "measured_peer_gbs": 770.0, "frac_measured": remote / t_x / 1e9 / 770.0,
+               "ms_per_step": t_x * 1e3, "expand_ms_per_step": t_expand * 1e3,
                "per_push": per_dir, "dedup": dedup,
                "remote_bytes_per_step": remote, "job_wire_bytes_per_step": job_wire,
                "impl": "NVLink peer memory: ep_dispatch push kernels + GEMM scatter epilogues (peer.py)"}
@@ -588,9 +595,10 @@ def main():
             stager.consume(state["x_ev"])
             blocks = [None] * world
             blocks[rank] = B.TokenBlock(xd[i % 2], positions)
+            # the API's default path: inputs validated (router.py:141-144) through
+            # the device status word, read after the router/dispatch barrier
             outs, fctx = B.moe_forward(blocks, wmap, topo, params, api_world, dtype=torch.bfloat16,
-                                       check_finite_inputs=False, shared_weights=shared,
-                                       pad_to_capacity=c["pad"])
+                                       shared_weights=shared, pad_to_capacity=c["pad"])
             stager.download(outs[rank], yh)  # overlaps the backward
             state["x_ev"] = None if last else stager.upload(xh, xd[(i + 1) % 2])
             stager.consume(u_ev)
@@ -617,8 +625,8 @@ def main():
                "h2d_bytes_per_step": 2 * xh.numel() * xh.element_size(),
                "d2h_bytes_per_step": 2 * yh.numel() * yh.element_size(),
                "ms_per_step": e2e_ms,
-               "path": "moe_forward/moe_backward API; pinned host x/u in, y/dx out every step "
-                       "via HostStager copy streams overlapping compute"}
+               "path": "moe_forward/moe_backward API (default: check_finite_inputs=True); pinned "
+                       "host x/u in, y/dx out every step via HostStager copy streams overlapping compute"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu and not a.profile_only:

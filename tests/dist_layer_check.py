@@ -29,12 +29,17 @@ def rel(a, b):
 
 
 def cases(world):
-    # tp, cp, ep, etp, cf, drop_mode, act
+    # tp, cp, ep, etp, cf, drop_mode, act, E, k -- the last case of each list
+    # has top-4 with several experts per EP index: the deduplicated push runs
+    # across GPUs (flag barrier, leader rows written over NVLink, ep_expand)
     if world == 2:
-        return [(1, 1, 2, 1, None, "subsequence", "swiglu"), (2, 1, 1, 2, None, "subsequence", "relu"),
-                (1, 2, 2, 1, 1.0, "fullsequence", "gelu"), (2, 1, 2, 1, 1.0, "subsequence", "swiglu")]
-    return [(1, 1, world, 1, None, "subsequence", "swiglu"), (2, 1, 2, 2, 1.0, "subsequence", "relu"),
-            (2, 2, 2, 2, 1.0, "fullsequence", "gelu"), (1, 2, world // 2, 2, None, "subsequence", "swiglu")]
+        return [(1, 1, 2, 1, None, "subsequence", "swiglu", 8, 2), (2, 1, 1, 2, None, "subsequence", "relu", 8, 2),
+                (1, 2, 2, 1, 1.0, "fullsequence", "gelu", 8, 2), (2, 1, 2, 1, 1.0, "subsequence", "swiglu", 8, 2),
+                (1, 1, 2, 1, None, "subsequence", "swiglu", 16, 4)]
+    return [(1, 1, world, 1, None, "subsequence", "swiglu", 8, 2), (2, 1, 2, 2, 1.0, "subsequence", "relu", 8, 2),
+            (2, 2, 2, 2, 1.0, "fullsequence", "gelu", 8, 2),
+            (1, 2, world // 2, 2, None, "subsequence", "swiglu", 8, 2),
+            (1, 1, world, 1, None, "subsequence", "swiglu", 16, 4)]
 
 
 def main():
@@ -44,9 +49,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    E, k, H, F, seq = 8, 2, 128, 256, 256
+    H, F, seq = 128, 256, 256
     failures = []
-    for ci, (tp, cp, ep, etp, cf, mode, act) in enumerate(cases(world)):
+    for ci, (tp, cp, ep, etp, cf, mode, act, E, k) in enumerate(cases(world)):
         for dtype, tol, xch in ((torch.float32, 1e-5, "nccl"), (torch.bfloat16, 2e-2, "peer"),
                                 (torch.bfloat16, 2e-2, "nccl")):
             seed = 40 + ci
@@ -91,6 +96,23 @@ def main():
                   flush=True)
             if worst >= tol:
                 failures.append(tag)
+            if peer and k >= 4:
+                # the deduplicated push is bit-identical to the per-pair push
+                # across GPUs (both settings agreed by every rank)
+                assert fctx.per_rank[rank]["peer"].dedup
+                os.environ["B200MOE_PUSH_DEDUP"] = "0"
+                try:
+                    outs0, fctx0 = B.moe_forward(blocks, weights, topo, params, nw, seq_len=seq, exchange=xch,
+                                                 peer_tag="nodedup")
+                    res0 = B.moe_backward(ups, fctx0)
+                finally:
+                    del os.environ["B200MOE_PUSH_DEDUP"]
+                torch.cuda.synchronize()
+                same = (torch.equal(outs0[rank], outs[rank]) and torch.equal(res0.input_grads[rank], res.input_grads[rank])
+                        and torch.equal(res0.w_g_grad, res.w_g_grad) and not fctx0.per_rank[rank]["peer"].dedup)
+                print(f"[rank {rank}] {'OK' if same else 'FAIL'} {tag} dedup push == per-pair push", flush=True)
+                if not same:
+                    failures.append(tag + " dedup")
     dist.barrier()
     dist.destroy_process_group()
     if failures:

@@ -140,8 +140,32 @@ def reference_layer(L: Layer, dec, u):
 
 
 def _rel(a, b):
+    """max|a - b| / max|b| -- the north star's rel-err
+    (reference tests/test_acceptance.py:85-87)."""
     a, b = a.double(), b.double()
-    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+def _record(name, errs):
+    """Per-tensor errors, also appended to $B200MOE_PARITY_LOG (JSON lines)
+    when set, for profiles/."""
+    import json
+    import os
+
+    print(name, {k: f"{v:.2e}" for k, v in errs.items()})
+    path = os.environ.get("B200MOE_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"config": name, "metric": "max|d|/max|want|", **errs}) + "\n")
+
+
+def _layer_errors(L, out, sv, grads):
+    dx, dwg, dw1p, dw2p = grads
+    ro, rdx, rdwg, rdw1, rdw2 = reference_layer(L, sv["dec"], L.u)
+    E = L.c["E"]
+    return {"out": _rel(out.float(), ro), "dx": _rel(dx.float(), rdx), "dw_g": _rel(dwg.float(), rdwg),
+            "dw1": max(_rel(dw1p[e].T.float(), rdw1[e]) for e in range(E)),
+            "dw2": max(_rel(dw2p[e].T.float(), rdw2[e]) for e in range(E))}
 
 
 @pytest.mark.parametrize("name", ["c2", "c4", "c5"])
@@ -159,11 +183,8 @@ def test_full_size_layer_vs_fp32_reference(name):
     np.testing.assert_array_equal(sv["plan_dev"].perm[:P].cpu().numpy(), plan.permutation)
     np.testing.assert_array_equal(sv["plan_dev"].counts.cpu().numpy(), plan.send_counts.reshape(-1))
     # floats against the fp32 restatement
-    ro, rdx, rdwg, rdw1, rdw2 = reference_layer(L, dec, L.u)
-    errs = {"out": _rel(out.float(), ro), "dx": _rel(dx.float(), rdx), "dw_g": _rel(dwg.float(), rdwg),
-            "dw1": max(_rel(dw1p[e].T.float(), rdw1[e]) for e in range(L.c["E"])),
-            "dw2": max(_rel(dw2p[e].T.float(), rdw2[e]) for e in range(L.c["E"]))}
-    print(name, {k: f"{v:.2e}" for k, v in errs.items()})
+    errs = _layer_errors(L, out, sv, (dx, dwg, dw1p, dw2p))
+    _record(name, errs)
     for key, v in errs.items():
         assert v < BF16_TOL, (key, v)
 
@@ -212,9 +233,22 @@ def test_full_size_capacity_and_padding():
     want = O.capacity_rank_vectorized(experts, cap, E)
     np.testing.assert_array_equal(dec.kept.cpu().numpy(), want)
     assert np.bincount(experts[want], minlength=E).max() <= cap
+    # floats against the fp32 restatement on the kept pairs (dropped pairs
+    # contribute nothing; fully dropped tokens output exact zeros)
+    errs = _layer_errors(L, out, sv, grads)
+    _record("c3", errs)
+    for key, v in errs.items():
+        assert v < BF16_TOL, (key, v)
+    dropped = ~dec.kept.any(1)
+    if bool(dropped.any()):
+        assert not bool(out[dropped].any())
     P = Layer("c3", pad=True)
-    out_p, _, grads_p = P.run()
+    out_p, sv_p, grads_p = P.run()
     torch.testing.assert_close(out_p, out, rtol=0, atol=0)
+    errs_p = _layer_errors(P, out_p, sv_p, grads_p)
+    _record("c3-pad-to-capacity", errs_p)
+    for key, v in errs_p.items():
+        assert v < BF16_TOL, (key, v)
     # gradients: same sums over the same rows (padding rows are zero)
     for a, b in zip(grads_p, grads):
         assert _rel(a.float(), b.float()) < 1e-6

@@ -208,6 +208,9 @@ def test_layer_cases_bf16_vs_oracle_with_gpu_logits(golden, ledgers):
         rnd = lambda a: t(a, torch.bfloat16).float().cpu().numpy().astype(np.float64)  # noqa: E731
         x, u = d[c + "_x"], d[c + "_u"]
         y = np.zeros_like(x); yw = np.zeros_like(x); dx = np.zeros_like(x); dxw = np.zeros_like(x)
+        dwg_w = np.zeros_like(d[c + "_wg"])
+        dw1_w = [np.zeros_like(d[c + "_w1"][e]) for e in range(E)]
+        dw2_w = [np.zeros_like(d[c + "_w2"][e]) for e in range(E)]
         for r, p in enumerate(positions):
             yo, st = O.layer_forward(rnd(x[p]), lgs[r], experts, cfg, positions=p,
                                      kept_override=kept_over[r])
@@ -217,8 +220,22 @@ def test_layer_cases_bf16_vs_oracle_with_gpu_logits(golden, ledgers):
             np.testing.assert_array_equal(dec.kept.cpu().numpy(), st.routing.kept, err_msg=c)
             y[p], yw[p] = outs[r].float().cpu().numpy(), yo
             dx[p], dxw[p] = res.input_grads[r].float().cpu().numpy(), g[0]
+            # weight gradients summed over ranks (dispatcher.py:492-499)
+            dwg_w += g[2]
+            for e in range(E):
+                dw1_w[e] += g[3][e]
+                dw2_w[e] += g[4][e]
         assert O.rel_err(y, yw) < BF16_TOL, (c, O.rel_err(y, yw))
         assert O.rel_err(dx, dxw) < BF16_TOL, (c, O.rel_err(dx, dxw))
+        assert O.rel_err(res.w_g_grad.cpu().numpy(), dwg_w) < BF16_TOL, c
+        ep, etp = meta[3], meta[4]
+        local = E // ep
+        for e in range(E):
+            ei, le = e // local, e % local
+            g1 = torch.cat([res.expert_grads[(ei, tt)][0][le] for tt in range(etp)], dim=1).cpu().numpy()
+            g2 = torch.cat([res.expert_grads[(ei, tt)][1][le] for tt in range(etp)], dim=0).cpu().numpy()
+            assert O.rel_err(g1, dw1_w[e]) < BF16_TOL, (c, e, O.rel_err(g1, dw1_w[e]))
+            assert O.rel_err(g2, dw2_w[e]) < BF16_TOL, (c, e, O.rel_err(g2, dw2_w[e]))
 
 
 
