@@ -250,11 +250,7 @@ static int launch(const void* x, int64_t T, int64_t H, const void* w, Args a, cu
   a.nkb = (int)ceil_div(H, BK);
   a.stages = std::max(2, std::min(8, (196 * 1024) / STAGE));
   const int smem = 1024 + a.stages * STAGE + 16 * a.stages + 64;
-  static bool attr_set = false;  // idempotent; races only repeat the same call
-  if (!attr_set) {
-    cudaFuncSetAttribute(router_tc_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    attr_set = true;
-  }
+  if (int e = ensure_max_smem(router_tc_kernel<EP>, 232448, "router_fwd_tc")) return e;
   router_tc_kernel<EP><<<(unsigned)ceil_div(T, BM), 256, smem, st>>>(mx, mw, a);
   B200MOE_CHECK_LAUNCH("router_fwd_tc");
   if (EP > 32)
@@ -440,11 +436,7 @@ static int launch_wgrad(const void* x, const void* dz_parts, int64_t T, int64_t 
     set_error("router_wgrad_tc: workspace too small");
     return B200MOE_EINVAL;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(router_wgrad_tc_kernel<EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    attr_set = true;
-  }
+  if (int e = ensure_max_smem(router_wgrad_tc_kernel<EPW>, 232448, "router_wgrad_tc")) return e;
   router_wgrad_tc_kernel<EPW><<<dim3((unsigned)mt, (unsigned)split), 256, smem, st>>>(mx, md, a);
   const int64_t HE = H * E;
   wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(HE, 256), 148 * 8), 256, 0, st>>>(

@@ -3,6 +3,10 @@
 #pragma once
 #include <cuda.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 
 namespace b200moe {
@@ -151,6 +155,25 @@ static int make_map(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, u
               (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2);
     return B200MOE_EINVAL;
   }
+  return B200MOE_OK;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device: set it once for
+// every (kernel, device) pair (ranks of a LocalWorld share the process).
+template <typename Kernel>
+static int ensure_max_smem(Kernel kern, int bytes, const char* name) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(key)) return B200MOE_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    set_error("%s: cannot set %d B of dynamic shared memory", name, bytes);
+    return B200MOE_ELAUNCH;
+  }
+  done.insert(key);
   return B200MOE_OK;
 }
 
