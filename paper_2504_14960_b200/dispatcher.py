@@ -312,6 +312,17 @@ def exchange_plan(counts: np.ndarray, ep_pos: int, L_: int, etp_recv: Optional[n
 # waiting for that early point of the step only (the GEMMs stay queued).
 ST_NONFINITE, ST_PEER_ABORT, ST_OVERSIZE = 1, 2, 4
 _STATUS: Dict[tuple, tuple] = {}
+_SIDE: Dict[tuple, torch.cuda.Stream] = {}
+_SIDE_SHARED = os.environ.get("B200MOE_SHARED_SIDE", "1") != "0"
+
+
+def _side_stream(device, main) -> "torch.cuda.Stream":
+    """One side stream per compute stream (ranks of a LocalWorld that share a
+    GPU each have their own)."""
+    key = (str(device), main.cuda_stream)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
 
 
 def _status_slot(device, rank: int):
@@ -409,6 +420,40 @@ class RankLayer:
         dx, dw1, dw2 = X.ffn_backward(u, sv["x"], sv["s_pre"], sv["s_h"], sv["s_goff"], 1, None,
                                       self.shared_pk, T)
         return dx, (dw1, dw2)
+
+    # With the peer exchange the shared expert's GEMMs run on a side stream
+    # while the compute stream waits in the cross-GPU barrier after the routed
+    # GEMMs (that wait is the other GPUs' skew and their last scatter stores):
+    # the side work is released by an event recorded right after the routed
+    # GEMMs, so it never takes SMs from them, and the combine waits for it.
+    # B200MOE_SHARED_SIDE=0 runs it in line on the compute stream.
+    def _on_side(self, fn, *args):
+        main = torch.cuda.current_stream()
+        side = _side_stream(self.device, main)
+        go = torch.cuda.Event()
+        go.record(main)
+        side.wait_event(go)
+        with torch.cuda.stream(side):
+            out = fn(*args)
+            done = torch.cuda.Event()
+            done.record(side)
+        return out, done, main
+
+    def _shared_forward_side(self, x, saved):
+        if self.shared_pk is None or not _SIDE_SHARED:
+            return self._shared_forward(x, saved), None
+        y, done, main = self._on_side(self._shared_forward, x, saved)
+        for t in (y, saved["s_pre"], saved["s_h"]):  # made on the side stream, used on the main one
+            t.record_stream(main)
+        return y, done
+
+    def _shared_backward_side(self, u, sv):
+        if self.shared_pk is None or not _SIDE_SHARED:
+            return None
+        (dx, grads), done, main = self._on_side(self._shared_backward, u, sv)
+        for t in (dx,) + tuple(grads):
+            t.record_stream(main)
+        return dx, grads, done
 
     # ---------------------------------------------------------------- fwd
     def forward(self, ctx: Optional[RankContext], x: torch.Tensor, positions: torch.Tensor) -> Tuple[torch.Tensor, dict]:
@@ -719,8 +764,10 @@ class RankLayer:
         self._mark_status()
         pre, h, _ = X.ffn_forward(px.region("xr"), st["goff"], self.L, None, self.pk, px.cap,
                                   y_scatter=px.scatter("yret"))
-        y_sh = self._shared_forward(x, saved)
+        y_sh, sh_done = self._shared_forward_side(x, saved)
         px.barrier()  # every expert output row (ETP: every partial) is back in yret
+        if sh_done is not None:
+            torch.cuda.current_stream().wait_event(sh_done)
         if oversize:
             out = torch.zeros_like(x)
             saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row, y=None)
@@ -737,6 +784,7 @@ class RankLayer:
         _, dw1p, dw2p = X.ffn_backward(px.region("dyr"), px.region("xr"), sv["pre"], sv["h"],
                                        st["goff"], self.L, None, self.pk, px.cap,
                                        dx_scatter=px.scatter("dxret"))
+        sv["shared_side"] = self._shared_backward_side(u, sv)
         px.barrier()  # every input-gradient row (ETP: every partial) is back in dxret
         return px.returned("dxret"), dgates, dw1p, dw2p
 
@@ -812,7 +860,12 @@ class RankLayer:
                           p.renormalize_topk, want_parts=wg_tc)
         if wg_tc:
             dz, dz_parts = dz
-        dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
+        side = sv.pop("shared_side", None)
+        if side is not None:
+            dx_sh, sv["shared_grads"], done = side
+            torch.cuda.current_stream().wait_event(done)
+        else:
+            dx_sh, sv["shared_grads"] = self._shared_backward(u, sv)
         if E <= 8:
             # router term dz . W_g^T fused into the combine (W_g^T slice held in
             # registers, csrc/dispatch.cu combine_router_kernel for bf16)

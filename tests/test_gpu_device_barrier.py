@@ -146,3 +146,23 @@ def test_push_mode_must_agree(monkeypatch):
     monkeypatch.setattr(B.dispatcher.os.environ, "get", per_rank_env)
     with pytest.raises(ProtocolError, match="PUSH_DEDUP"):
         B.moe_forward(blocks, weights, topo, params, B.LocalWorld(2), dtype=torch.bfloat16)
+
+
+def test_shared_expert_side_stream_is_exact(monkeypatch):
+    """The shared expert's GEMMs on the side stream (overlapping the barrier
+    waits after the routed GEMMs) give exactly the in-line results, with the
+    device barrier and ranks on their own streams."""
+    H, F, E, k, S, seed = 128, 256, 16, 4, 384, 4
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
+    shared = B.init_shared_expert(H, S, seed)
+    blocks, ups = _blocks((256, 192), H, seed)
+    got = {}
+    for side in (False, True):
+        monkeypatch.setattr(B.dispatcher, "_SIDE_SHARED", side)
+        got[side] = _run(B.LocalWorld(2, device_barrier=True), topo, params, weights, blocks, ups,
+                         shared=shared)
+    _same(got[False], got[True])
+    for a, b in zip(got[False][2].shared_grads, got[True][2].shared_grads):
+        torch.testing.assert_close(a, b, rtol=0, atol=0)
