@@ -147,6 +147,17 @@ B200MOE_API size_t b200moe_router_wgrad_ws(int64_t T, int64_t H, int E);
 B200MOE_API int b200moe_router_wgrad(const void* x, int x_dtype, const float* dz, int64_t T, int64_t H, int E,
                          float* dw_g, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Full-sequence capacity over the TP x CP group (router.py:209-269).  The
+ * group's pairs, all-gathered into fixed member slots, sorted on the device in
+ * admission order: seg_sorted[N] = (pos / seq_len) * E + expert (INT64_MAX for
+ * empty slots, sorted ascending; ties in priority order), order[N] = slot of
+ * each sorted pair.  kept_slot[slot] = rank inside its segment < cap.
+ * pos_by_pos (nullable): all pairs' positions sorted ascending; a position
+ * shared by more than k pairs (two tokens) sets bit 3 of *status. */
+B200MOE_API int b200moe_fullseq_capacity(const int64_t* seg_sorted, const int64_t* order, int64_t N,
+                                         int64_t cap, uint8_t* kept_slot, const int64_t* pos_by_pos, int k,
+                                         int32_t* status, void* stream);
+
 /* load statistics (router.py:279-301): counts[e] = kept pairs routed to e,
  * top1[e] = tokens whose best expert is e, score_sum[e] = sum over tokens of
  * scores[t, e] / sum_e' scores[t, e'] (fp64; scores may be NULL).  kept may

@@ -56,6 +56,7 @@ _SIGS = {
     "b200moe_capacity_by_gate": [P, P, P, P, I64, I32, I32, I64, P, P],
     "b200moe_router_bwd": [P, P, P, P, I64, I32, I32, I32, I32, P, P, P],
     "b200moe_router_parts_cols": [I32],
+    "b200moe_fullseq_capacity": [P, P, I64, I64, P, P, I32, P, P],
     "b200moe_router_wgrad_tc_ws": [I64, I64, I32],
     "b200moe_router_wgrad_tc": [P, P, I64, I64, I32, P, P, SZ, P],
     "b200moe_router_wgrad_ws": [I64, I64, I32],

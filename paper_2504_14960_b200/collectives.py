@@ -471,6 +471,12 @@ class RankContext:
             recvs: List[Tuple[int, torch.Tensor]]) -> None:
         raise NotImplementedError
 
+    def all_gather_fixed(self, group: Group, t: torch.Tensor) -> torch.Tensor:
+        """[len(group), *t.shape]: every member's equally-shaped tensor in
+        group order, on this rank's device -- no sizes cross the host, so the
+        stream never waits for the host (NCCL all_gather_into_tensor)."""
+        raise NotImplementedError
+
     def a2a_single(self, group: Group, send: torch.Tensor, send_splits: Sequence[int],
                    recv: torch.Tensor, recv_splits: Sequence[int], async_op: bool = False):
         """Rows [sum(send_splits[:j]), +send_splits[j]) of ``send`` go to
@@ -528,6 +534,15 @@ class LocalRankContext(RankContext):
             return {r: None for r in g}
 
         self.world._rendezvous(self.rank, group, payload, compute)
+
+    def all_gather_fixed(self, group, t):
+        def compute(g, payloads):
+            shapes = {tuple(payloads[r].shape) for r in g}
+            if len(shapes) != 1:
+                raise ProtocolError(f"all_gather_fixed: shapes differ across the group: {shapes}")
+            return {r: torch.stack([payloads[q].to(payloads[r].device) for q in g]) for r in g}
+
+        return self.world._rendezvous(self.rank, group, t.contiguous(), compute)
 
     def _all_reduce(self, group, values, op):
         def compute(g, payloads):
@@ -629,6 +644,16 @@ class NcclRankContext(RankContext):
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+
+    def all_gather_fixed(self, group, t):
+        _check_group(self.rank, group)
+        t = t.contiguous()
+        out = torch.empty((len(group),) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        if len(group) == 1:
+            out[0].copy_(t)
+        else:
+            self.world.dist.all_gather_into_tensor(out.view(-1), t.view(-1), group=self.world.pg(group))
+        return out
 
     def a2a_single(self, group, send, send_splits, recv, recv_splits, async_op=False):
         from . import _lib

@@ -24,6 +24,8 @@ int router_fwd_tc_np(int);
 int router_fwd_tc(const void*, int64_t, int64_t, const void*, int, int, int, int, float*, float*,
                   int32_t*, float*, double*, int32_t*, cudaStream_t);
 size_t plan_ws_bytes(int64_t, int);
+int fullseq_capacity(const int64_t*, const int64_t*, int64_t, int64_t, uint8_t*, const int64_t*, int,
+                     int32_t*, cudaStream_t);
 int dispatch_plan(const int32_t*, const float*, const uint8_t*, const int32_t*, int64_t, int, int,
                   int64_t, int, void*, uint8_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*,
                   int64_t*, float*, cudaStream_t);
@@ -205,6 +207,15 @@ int b200moe_router_bwd(const float* dgates, const float* scores, const int32_t* 
   REQUIRE(dgates && scores && topk_idx && gates && dz, "router_bwd: null pointer");
   return router_bwd(dgates, scores, topk_idx, gates, T, E, k, gate_fn, renorm, dz, dz_parts, epw, nb,
                     S(stream));
+}
+
+int b200moe_fullseq_capacity(const int64_t* seg_sorted, const int64_t* order, int64_t N, int64_t cap,
+                             uint8_t* kept_slot, const int64_t* pos_by_pos, int k, int32_t* status,
+                             void* stream) {
+  REQUIRE(N >= 0 && cap >= 0 && k >= 1, "fullseq_capacity: bad args");
+  if (N == 0) return B200MOE_OK;
+  REQUIRE(seg_sorted && order && kept_slot, "fullseq_capacity: null pointer");
+  return fullseq_capacity(seg_sorted, order, N, cap, kept_slot, pos_by_pos, k, status, S(stream));
 }
 
 int b200moe_router_parts_cols(int E) {

@@ -513,6 +513,55 @@ __global__ void __launch_bounds__(256) capacity_by_gate_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// full-sequence capacity                          (router.py:209-269)
+// ---------------------------------------------------------------------------
+// The (sequence x expert, position) keys of every pair of the TP x CP group
+// arrive all-gathered in fixed member slots (padding = INT64_MAX) and sorted
+// on the device in admission order: by segment seg = (pos / seq_len) * E + e,
+// then (probability priority) by gate descending, then by position.  A pair
+// is kept iff its rank inside its segment is below cap -- the rank is its
+// index minus the segment's first index, found by binary search in the
+// sorted segment array (no scan, no host round trip).  Flags are written
+// back to the pairs' original slots.  pos_by_pos (every pair's position,
+// sorted) detects duplicate token positions across shards: a token's k pairs
+// share a position, so position i equal to position i - k means two tokens
+// (status bit 3).
+__global__ void __launch_bounds__(256) fullseq_capacity_kernel(
+    const int64_t* __restrict__ seg_sorted, const int64_t* __restrict__ order, int64_t N, int64_t cap,
+    uint8_t* __restrict__ kept_slot, const int64_t* __restrict__ pos_by_pos, int k,
+    int32_t* __restrict__ status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int64_t sg = seg_sorted[i];
+  const int64_t slot = order[i];
+  if (sg == INT64_MAX) {
+    kept_slot[slot] = 0;
+  } else {
+    int64_t lo = 0, hi = i;  // first index with seg_sorted[idx] == sg
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (seg_sorted[mid] < sg) lo = mid + 1;
+      else hi = mid;
+    }
+    kept_slot[slot] = (i - lo) < cap ? 1 : 0;
+  }
+  if (pos_by_pos && status && i >= k) {
+    const int64_t p = pos_by_pos[i];
+    if (p != INT64_MAX && p == pos_by_pos[i - k]) atomicOr(status, 8);
+  }
+}
+
+int fullseq_capacity(const int64_t* seg_sorted, const int64_t* order, int64_t N, int64_t cap,
+                     uint8_t* kept_slot, const int64_t* pos_by_pos, int k, int32_t* status,
+                     cudaStream_t st) {
+  if (N == 0) return B200MOE_OK;
+  fullseq_capacity_kernel<<<(unsigned)ceil_div(N, 256), 256, 0, st>>>(seg_sorted, order, N, cap, kept_slot,
+                                                                      pos_by_pos, k, status);
+  B200MOE_CHECK_LAUNCH("fullseq_capacity");
+  return B200MOE_OK;
+}
+
+// ---------------------------------------------------------------------------
 // router backward                                  (dispatcher.py:470-488)
 // ---------------------------------------------------------------------------
 // an fp32 value as three bf16 parts hi + mid + lo == v exactly (8 + 8 + 8

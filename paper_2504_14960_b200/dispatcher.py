@@ -310,10 +310,12 @@ def exchange_plan(counts: np.ndarray, ep_pos: int, L_: int, etp_recv: Optional[n
 # exchange kernels set them, the word is copied to pinned host memory right
 # after the router / the dispatch barrier, and moe_forward raises after
 # waiting for that early point of the step only (the GEMMs stay queued).
-ST_NONFINITE, ST_PEER_ABORT, ST_OVERSIZE = 1, 2, 4
+ST_NONFINITE, ST_PEER_ABORT, ST_OVERSIZE, ST_DUPLICATE = 1, 2, 4, 8
 _STATUS: Dict[tuple, tuple] = {}
 _SIDE: Dict[tuple, torch.cuda.Stream] = {}
-_SIDE_SHARED = os.environ.get("B200MOE_SHARED_SIDE", "1") != "0"
+# measured neutral at 4 GPUs (C4: 36.4 vs 36.0 ms/step): the barrier wait it
+# fills is the slowest GPU's skew, which the slowest GPU itself cannot hide
+_SIDE_SHARED = os.environ.get("B200MOE_SHARED_SIDE", "0") == "1"
 
 
 def _side_stream(device, main) -> "torch.cuda.Stream":
@@ -339,6 +341,8 @@ def _status_slot(device, rank: int):
 def _raise_status(bits: int, what: str = "") -> None:
     if bits & ST_NONFINITE:
         raise NumericError(f"token block contains non-finite values{what}")
+    if bits & ST_DUPLICATE:
+        raise ProtocolError(f"full-sequence gather: duplicate token positions across shards{what}")
     if bits & ST_OVERSIZE:
         raise ValidationError(f"token block exceeds the peer buffers{what}: pass peer_tokens >= the "
                               "largest block on first use", constraint="peer-capacity")
@@ -426,7 +430,7 @@ class RankLayer:
     # GEMMs (that wait is the other GPUs' skew and their last scatter stores):
     # the side work is released by an event recorded right after the routed
     # GEMMs, so it never takes SMs from them, and the combine waits for it.
-    # B200MOE_SHARED_SIDE=0 runs it in line on the compute stream.
+    # Opt-in (B200MOE_SHARED_SIDE=1): measured neutral, see _SIDE_SHARED.
     def _on_side(self, fn, *args):
         main = torch.cuda.current_stream()
         side = _side_stream(self.device, main)
@@ -499,7 +503,8 @@ class RankLayer:
         if not p.dropless:
             if p.drop_mode == DROP_FULLSEQUENCE:
                 _, dec = gather_full_sequence_decision(ctx, self.g.seq, dec, self.seq_len, E, p,
-                                                      check=self.check)
+                                                      slots=self._fullseq_slots(ctx, T),
+                                                      status=self.status, want_global=False)
             else:
                 dec.kept = kept_mask(dec, T, E, p).bool()
         kept_in = None if p.dropless else dec.kept.to(torch.uint8).contiguous()
@@ -569,6 +574,17 @@ class RankLayer:
                 ctx.account(self.g.etp, None)
             ctx.account(self.g.etp, "reduce_scatter_v", H, lambda: dplan.recv_counts.sum())
         ctx.account(self.g.ep, "all_to_all_v", H, lambda: dplan.recv_counts.sum(1))
+
+    def _fullseq_slots(self, ctx, T: int) -> int:
+        """Tokens per member of the full-sequence gather: the sequence group's
+        largest block, agreed once (like the peer buffers); a later, larger
+        block needs ``peer_tokens`` on first use."""
+        cache = ctx.world.__dict__.setdefault("_fullseq_slots", {})
+        key = (ctx.rank, self.g.seq)
+        if key not in cache:
+            mine = max(T, int(self.peer_tokens or 0))
+            cache[key] = max(int(v) for v in ctx.meta(self.g.seq, mine).values())
+        return cache[key]
 
     # ------------------------------------------------------- EP / ETP exchange
     # Rows are permuted straight into the padded per-global-expert layout,
@@ -938,6 +954,9 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
     of that call (or ``peer_tokens`` if larger); layers whose forward and
     backward interleave need distinct ``peer_tag`` values (their own buffers).
     """
+    pending = world.__dict__.pop("_b200moe_pending", None)
+    if pending is not None:  # a previous step whose backward never ran
+        _check_step(pending, block=True)
     groups = _validate(blocks, topology, params, seq_len)
     if hasattr(world, "setup_groups"):
         world.setup_groups([groups.moe["EP"], groups.moe["ETP"], groups.moe["EDP"],
@@ -968,28 +987,48 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
     for r in results:
         outputs.append(None if r is None else r[0])
         context.per_rank.append(None if r is None else r[1])
-    # failures the device flagged during the step (non-finite inputs, an
-    # oversized block, a failed peer): the wait ends at the router / dispatch
-    # barrier of this step, the rest of the step stays queued on the GPU
-    layers = [(r, sv["layer"]) for r, sv in enumerate(context.per_rank) if sv is not None]
-    for r, layer in layers:
-        layer.status_event and layer.status_event.synchronize()
-    bits = {r: int(layer.status_host[0]) if layer.status_event is not None else 0 for r, layer in layers}
-    for mask in (ST_NONFINITE, ST_OVERSIZE, ST_PEER_ABORT):  # the root cause first
-        for r in sorted(bits):
-            if bits[r] & mask:
-                if mask == ST_NONFINITE:
-                    raise nonfinite_error(context.per_rank[r]["x"], params, f" (rank {r})")
-                _raise_status(mask, f" (rank {r})")
     for sv in context.per_rank:
         if sv is not None:
             sv["decision"] = sv["dec"]
+    # failures the device flagged during the step (non-finite inputs, an
+    # oversized block, a failed peer, duplicate positions) are raised here if
+    # the step's status copy has already landed, otherwise at the next
+    # natural synchronisation point -- the start of moe_backward for this
+    # context, or the next moe_forward on this world -- so the host never
+    # stalls the stream it feeds
+    if not _check_step(context, block=False):
+        world.__dict__["_b200moe_pending"] = context
     return outputs, context
+
+
+def _check_step(context: ForwardContext, block: bool) -> bool:
+    """Raise the root cause of a step the device flagged; False when
+    ``block`` is off and a status copy is still in flight."""
+    if context.__dict__.get("_checked"):
+        return True
+    layers = [(r, sv["layer"]) for r, sv in enumerate(context.per_rank) if sv is not None]
+    events = [layer.status_event for _, layer in layers if layer.status_event is not None]
+    if not block and not all(ev.query() for ev in events):
+        return False
+    for ev in events:
+        ev.synchronize()
+    context.__dict__["_checked"] = True
+    bits = {r: int(layer.status_host[0]) if layer.status_event is not None else 0 for r, layer in layers}
+    for mask in (ST_NONFINITE, ST_DUPLICATE, ST_OVERSIZE, ST_PEER_ABORT):  # the root cause first
+        for r in sorted(bits):
+            if bits[r] & mask:
+                if mask == ST_NONFINITE:
+                    raise nonfinite_error(context.per_rank[r]["x"], context.params, f" (rank {r})")
+                _raise_status(mask, f" (rank {r})")
+    return True
 
 
 def moe_backward(upstream, context: ForwardContext, workers: Optional[int] = None) -> BackwardResult:
     """Gradients of sum over ranks of <upstream, output> (dispatcher.py:387-510)."""
     topology = context.topology
+    _check_step(context, block=True)  # by now long complete: the forward's dispatch barrier
+    if context.world.__dict__.get("_b200moe_pending") is context:
+        del context.world.__dict__["_b200moe_pending"]
     if len(upstream) != topology.world_size:
         raise ValidationError(f"{len(upstream)} upstream blocks for world_size {topology.world_size}",
                               constraint="upstream==world")

@@ -442,3 +442,16 @@ def act_bwd(dh, pre, act: int, group_off, G: int, F: int, out=None):
     L.call("b200moe_act_bwd", L.ptr(dh), L.ptr(pre), L.dtype_code(pre.dtype), act,
            L.ptr(group_off), G, rows, F, L.ptr(out), _sp())
     return out
+
+
+def fullseq_capacity(seg_sorted: torch.Tensor, order: torch.Tensor, cap: int, k: int,
+                     pos_by_pos: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None):
+    """Kept flags (uint8, original slot order) of a full-sequence capacity pass
+    over device-sorted pair keys (router.py:209-269); see b200moe.h."""
+    N = seg_sorted.numel()
+    _cuda(seg_sorted, "seg_sorted", torch.int64)
+    _cuda(order, "order", torch.int64)
+    kept = torch.empty((N,), dtype=torch.uint8, device=seg_sorted.device)
+    L.call("b200moe_fullseq_capacity", L.ptr(seg_sorted), L.ptr(order), N, int(cap), L.ptr(kept),
+           L.ptr(pos_by_pos), k, L.ptr(status), _sp())
+    return kept

@@ -304,67 +304,83 @@ def apply_capacity(decision: RoutingDecision, l_scope: int, num_experts: int,
 
 
 def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: int,
-                                  num_experts: int, params: GatingParams, check: bool = True
-                                  ) -> Tuple[RoutingDecision, RoutingDecision]:
+                                  num_experts: int, params: GatingParams, check: bool = True,
+                                  slots: Optional[int] = None, status: Optional[torch.Tensor] = None,
+                                  want_global: bool = True
+                                  ) -> Tuple[Optional[RoutingDecision], RoutingDecision]:
     """Capacity per full sequence across the ranks sharding it (router.py:209-269).
 
-    The (position, slot, expert, gate) pairs of the group are all-gathered on
-    the device (the size exchange is the one host synchronisation), sorted by
-    position, and every sequence's experts become a block of E virtual
-    experts, so ONE capacity pass of the plan kernels applies the
-    per-sequence capacity to all sequences at once; the flags of this rank's
-    pairs are mapped back through the gather permutation.  ``check``
-    validates unique positions (one more sync)."""
-    from .collectives import VarBuffer
-
+    Device-native: every member's pairs travel as int64 keys -- segment
+    (sequence x expert) and position, plus the float64 gate under probability
+    priority -- through a fixed-size all-gather (``slots`` tokens per member,
+    padded; no sizes cross the host), are sorted on the device into admission
+    order (stable sorts: position, [gate descending,] segment), and one
+    kernel (b200moe_fullseq_capacity) gives every pair its rank inside its
+    segment, keeps it iff rank < cap, and writes the flags back to the pairs'
+    slots.  Nothing in the layer path synchronises with the host; the
+    duplicate-position check (router.py:245-246) is a status bit (``status``,
+    raised by moe_forward) -- or, standalone with ``check``, a host read.
+    ``slots`` defaults to the group's largest block, agreed with one host
+    exchange.  The global decision (union of the group's pairs in position
+    order) is built only when ``want_global``."""
     n, k = local.experts.shape
     E = num_experts
+    group = tuple(group)
+    me = group.index(ctx.rank)
     dev = local.experts.device
-    pos = local.positions.to(dev, torch.int64)
-    rows = torch.stack([
-        pos.repeat_interleave(k).double(),
-        torch.arange(k, device=dev).repeat(n).double(),
-        local.experts.reshape(-1).double(),
-        (local.gates_f64 if local.gates_f64 is not None else local.gates.double()).reshape(-1),
-    ], dim=1)
-    buf, counts = ctx.all_gather_v(tuple(group), VarBuffer.from_rows(rows))
-    g = buf.rows()
-    if g.shape[0] % k:
-        raise ProtocolError(f"full-sequence gather: {g.shape[0]} pairs is not a multiple of k={k}; "
-                            "shard lengths are inconsistent")
-    N = g.shape[0] // k
-    gk = g.reshape(N, k, 4)
-    order = torch.argsort(gk[:, 0, 0].to(torch.int64), stable=True)
-    gk = gk[order]
-    gpos = gk[:, 0, 0].to(torch.int64)
-    if check and N > 1 and bool((gpos[1:] == gpos[:-1]).any()):
-        raise ProtocolError("full-sequence gather: duplicate token positions across shards")
-    experts = gk[:, :, 2].to(torch.int32).contiguous()
-    g64 = gk[:, :, 3].contiguous()
-    global_dec = RoutingDecision(experts, g64.float(), torch.ones_like(experts, dtype=torch.bool),
-                                 gpos, None, g64)
-    # compact sequence index of every token (positions are sorted)
-    sid = gpos // seq_len
-    new_seq = torch.ones_like(sid)
-    if N > 1:
-        new_seq[1:] = (sid[1:] != sid[:-1]).to(sid.dtype)
-    cid = torch.cumsum(new_seq, 0) - 1
-    n_seq = int(cid[-1]) + 1 if N else 0
-    if n_seq * E > 4096:
-        raise ValidationError(f"full-sequence capacity: {n_seq} sequences x {E} experts in one "
-                              "group exceeds 4096", constraint="full-seq-virtual-experts")
-    vdec = RoutingDecision((cid[:, None].to(torch.int32) * E + experts).contiguous(), global_dec.gates,
-                           global_dec.kept, gpos, None, g64)
+    if slots is None:
+        slots = max(int(v) for v in ctx.meta(group, n).values())
+    if n > slots:
+        raise ValidationError(f"token block of {n} rows exceeds the {slots} full-sequence gather slots",
+                              constraint="fullseq-slots")
+    S = slots * k
+    pos_h = local.positions
+    if pos_h.is_cuda:
+        pos = pos_h.to(torch.int64)
+    else:
+        pos = pos_h.to(torch.int64).pin_memory().to(dev, non_blocking=True)
+    pad = torch.iinfo(torch.int64).max
+    seg = torch.full((S,), pad, dtype=torch.int64, device=dev)
+    ppos = torch.full((S,), pad, dtype=torch.int64, device=dev)
+    if n:
+        seg[:n * k] = ((pos // seq_len)[:, None] * E + local.experts.to(torch.int64)).reshape(-1)
+        ppos[:n * k] = pos.repeat_interleave(k)
+    # the reference's wire record: (pos, slot, expert, gate) rows of width 4
+    ctx.account(group, "all_gather_v", 4, n * k)
+    all_seg = ctx.all_gather_fixed(group, seg).view(-1)
+    all_pos = ctx.all_gather_fixed(group, ppos).view(-1)
+    by_pos = torch.sort(all_pos, stable=True).indices
+    order = by_pos
+    prob = params.drop_priority == PRIORITY_PROBABILITY
+    g64 = None
+    if prob or want_global:
+        g = local.gates_f64 if local.gates_f64 is not None else local.gates.double()
+        gp = torch.full((S,), float("-inf"), dtype=torch.float64, device=dev)
+        if n:
+            gp[:n * k] = g.reshape(-1)
+        g64 = ctx.all_gather_fixed(group, gp).view(-1)
+    if prob:
+        order = order[torch.sort(g64[order], descending=True, stable=True).indices]
+    order = order[torch.sort(all_seg[order], stable=True).indices]
     cap = capacity_limit(params.capacity_factor, seq_len, E)
-    kept = kept_mask(vdec, seq_len, max(n_seq, 1) * E, params, cap=cap, sorted_positions=True).bool()
-    global_dec.kept = kept
-    # map back: this rank's pairs sit at rows [off, off + n) of the gathered table
-    me = tuple(group).index(ctx.rank)
-    off = int(np.asarray(counts[:me]).sum()) // k
-    inv = torch.empty_like(order)
-    inv[order] = torch.arange(N, device=dev)
+    own_status = status if status is not None else torch.zeros((1,), dtype=torch.int32, device=dev)
+    kept_slot = K.fullseq_capacity(all_seg[order].contiguous(), order.contiguous(), cap, k,
+                                   pos_by_pos=all_pos[by_pos].contiguous(), status=own_status)
+    if status is None and check and int(own_status.item()) & 8:
+        raise ProtocolError("full-sequence gather: duplicate token positions across shards")
     out = local.copy()
-    out.kept = kept[inv[off:off + n]]
+    out.kept = kept_slot.view(len(group), S)[me, :n * k].view(n, k).bool()
+    global_dec = None
+    if want_global:
+        # the group's pairs in position order (sizes read on the host: API use only)
+        valid = all_pos[by_pos] != pad
+        idx = by_pos[valid]
+        # a token's k pairs share its position and sit in slot order (t*k + s),
+        # so the stable position sort keeps them adjacent and best-first
+        tok = idx.view(-1, k)
+        gg = g64[tok]
+        global_dec = RoutingDecision((all_seg[tok] % E).to(torch.int32).contiguous(), gg.float(),
+                                     kept_slot[tok].bool(), all_pos[tok[:, 0]].cpu(), None, gg.contiguous())
     return global_dec, out
 
 

@@ -131,8 +131,9 @@ def test_peer_buffers_reused_before_backward_fail_loudly():
         B.moe_backward(ups, ctx_a)
     # a later, larger token block than the buffers were sized for
     big, _ = _blocks((128, 64), H, 2)
-    with pytest.raises(ValidationError, match="peer buffers"):
-        B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
+    with pytest.raises(ValidationError, match="peer buffers"):  # from moe_forward or, deferred, moe_backward
+        _, ctx_big = B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
+        B.moe_backward(_blocks((128, 64), H, 3)[1], ctx_big)
 
 
 def test_peer_tags_and_headroom():
