@@ -28,6 +28,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MoE-layer fwd+bwd tokens/s"
+# experiments only: B200MOE_E2E_CHECK=0 times the e2e leg without input validation
+E2E_CHECK = os.environ.get("B200MOE_E2E_CHECK", "1") != "0"
 UNIT = "tokens/s"
 
 # BASELINE.json configs[1..4] (configs[0] is the CPU-oracle case); per-GPU
@@ -598,7 +600,8 @@ def main():
             # the API's default path: inputs validated (router.py:141-144) through
             # the device status word, read after the router/dispatch barrier
             outs, fctx = B.moe_forward(blocks, wmap, topo, params, api_world, dtype=torch.bfloat16,
-                                       shared_weights=shared, pad_to_capacity=c["pad"])
+                                       shared_weights=shared, pad_to_capacity=c["pad"],
+                                       check_finite_inputs=E2E_CHECK)
             stager.download(outs[rank], yh)  # overlaps the backward
             state["x_ev"] = None if last else stager.upload(xh, xd[(i + 1) % 2])
             stager.consume(u_ev)

@@ -1174,6 +1174,9 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
   p.debug_nostore = (ns && ns[0] >= '1' && ns[0] <= '3') ? ns[0] - '0' : 0;
   p.panel_m = choose_panel(a, p.tile_m);
+  // experiments: B200MOE_PANEL_M=n forces the raster panel height (m-tiles)
+  const char* pm = getenv("B200MOE_PANEL_M");
+  if (pm && atoi(pm) > 0) p.panel_m = atoi(pm);
 
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                          const Params);

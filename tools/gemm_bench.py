@@ -31,6 +31,7 @@ def main():
                          "'B200MOE_STORE_HINT=0,B200MOE_STORE_HINT=1'")
     ap.add_argument("--routed", action="store_true", help="uneven groups from a real routing")
     ap.add_argument("--splitk", type=int, default=4, help="K slices of the split-K dgrad1 variant")
+    ap.add_argument("--only", default="", help="run only the GEMMs whose name contains this")
     ap.add_argument("--wait-prof", action="store_true",
                     help="library built with -DB200MOE_WAIT_PROF: print per-role barrier wait shares")
     a = ap.parse_args()
@@ -95,6 +96,8 @@ def main():
             dpre, x, dw1, grouped_dim=1, G=E, M=N1, N=H, K=0, a_sm=1, a_sk=N1, b_sg=0, b_sk=H,
             b_sn=1, c_sg=N1 * H, ldc=H, group_off=goff, max_rows=R)),
     ]
+    if a.only:
+        runs = [r for r in runs if a.only in r[0]]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     variants = [v for v in a.variants.split(",") if v] or [""]
 
