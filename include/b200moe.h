@@ -311,8 +311,9 @@ B200MOE_API int b200moe_ep_barrier(const uint64_t* peer_base, int64_t flag_off, 
  * (me, le) in EP index d's receive buffers -- the same on its etp members),
  * goff[L+1] / gcount[L] (this rank's GEMM groups: one per local expert,
  * senders contiguous in member order, the group padded to align rows).
- * Marker rows count as empty and set bit 1 of *status (nullable).
- * Traps if a layout exceeds cap_rows. */
+ * Marker rows count as empty and set bit 1 of *status (nullable).  A layout
+ * that exceeds cap_rows sets bit 4 (this rank's groups become empty) or,
+ * without a status word, traps. */
 B200MOE_API int b200moe_ep_layout(const int32_t* cnt_local, int me, int ep, int etp, int L, int align,
                                   int64_t cap_rows, int32_t* seg_off, int32_t* goff, int32_t* gcount,
                                   int32_t* status, void* stream);

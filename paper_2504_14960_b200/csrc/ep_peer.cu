@@ -94,7 +94,8 @@ __global__ void ep_counts_push_kernel(const int32_t* __restrict__ counts, int me
 // expert, no per-sender padding.
 // seg_off[d*L + le] = first row of (me, le) in EP index d's receive buffers;
 // goff[le] / gcount[le] = group start / real rows in this rank's buffer,
-// goff[L] = end.  A layout beyond cap_rows (the buffer size) traps.
+// goff[L] = end.  A layout beyond cap_rows (the buffer size) fails the step
+// (status bit 4) or, without a status word, traps.
 __global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int me, int ep, int etp, int L,
                                  int align, int64_t cap_rows, int32_t* __restrict__ seg_off,
                                  int32_t* __restrict__ goff, int32_t* __restrict__ gcount,
@@ -124,9 +125,21 @@ __global__ void ep_layout_kernel(const int32_t* __restrict__ cnt, int me, int ep
     run += (tot + align - 1) / align * align;
   }
   if (run > cap_rows) {
-    printf("b200moe ep_layout: EP index %d receive layout needs %lld rows > capacity %lld\n", d,
-           (long long)run, (long long)cap_rows);
-    __trap();
+    // this step's routing does not fit EP index d's receive buffers: every
+    // member sees the same counts, so all of them fail the step (status bit
+    // 4; no pushes) and this rank's groups shrink to nothing (no GEMM reads
+    // past the buffer); without a status word there is no safe way on
+    if (!status) {
+      printf("b200moe ep_layout: EP index %d receive layout needs %lld rows > capacity %lld\n", d,
+             (long long)run, (long long)cap_rows);
+      __trap();
+    }
+    atomicOr(status, 16);
+    if (mine) {
+      for (int le = 0; le <= L; ++le) goff[le] = 0;
+      for (int le = 0; le < L; ++le) gcount[le] = 0;
+    }
+    return;
   }
   if (mine) goff[L] = (int32_t)run;
 }

@@ -73,6 +73,7 @@ struct Params {
   // ([32 gate | 32 up] per 64) and are stored de-interleaved ([gate | up])
   int64_t glu_f;
   int store_hint;  // L2 evict_first policy on the epilogue's bulk stores
+  int kstagger;    // K walk of a tile starts at (n-tile * kstagger) mod nkb (0: off)
 };
 
 // packed SwiGLU row -> [gate | up] row (rows come in 32-row halves)
@@ -325,6 +326,7 @@ struct Tile {
   int64_t kbeg;       // first K coordinate (grouped-K: absolute row)
   int nkb;            // number of BK blocks
   int bidx;           // weight/expert index for B (grouped-M)
+  int krot;           // first BK block of the tile's K walk (rotated, wraps)
 };
 
 // Panel rasterisation inside a group: panels of `pm` m-tiles x all n-tiles,
@@ -383,6 +385,11 @@ __device__ __forceinline__ Tile decode(const Params& p, const int32_t* prefix, i
     r.nkb = (int)((g1 - g0 + BK - 1) / BK);
     r.bidx = 0;
   }
+  // the tiles of one m-panel share A's K slabs; staggering their K walks by
+  // output column block keeps them from requesting the same slab at the same
+  // instant (a row's result depends only on its column block's order, so
+  // outputs stay independent of the row layout)
+  r.krot = (p.kstagger && r.nkb > 0) ? (int)(((r.n0 / BN) * p.kstagger) % r.nkb) : 0;
   return r;
 }
 
@@ -586,7 +593,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t fb = full_bar + 8 * stage;
           if (crank == 0) mbar_expect_tx(fb, C::STAGE * CG);
           const uint32_t fb_tma = CG == 2 ? (fb & PEER_BIT_MASK) : fb;
-          const int kc = (int)(tl.kbeg + (int64_t)kb * BK);
+          const int kbr = kb + tl.krot < tl.nkb ? kb + tl.krot : kb + tl.krot - tl.nkb;
+          const int kc = (int)(tl.kbeg + (int64_t)kbr * BK);
           const uint32_t a_dst = sA + stage * C::A_BYTES;
           const uint32_t b_dst = sB + stage * C::B_BYTES;
           if (!A_MN) {
@@ -1174,6 +1182,8 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
   p.debug_nostore = (ns && ns[0] >= '1' && ns[0] <= '3') ? ns[0] - '0' : 0;
   p.panel_m = choose_panel(a, p.tile_m);
+  const char* ks = getenv("B200MOE_KSTAGGER");
+  p.kstagger = ks ? atoi(ks) : 0;
   // experiments: B200MOE_PANEL_M=n forces the raster panel height (m-tiles)
   const char* pm = getenv("B200MOE_PANEL_M");
   if (pm && atoi(pm) > 0) p.panel_m = atoi(pm);

@@ -310,7 +310,7 @@ def exchange_plan(counts: np.ndarray, ep_pos: int, L_: int, etp_recv: Optional[n
 # exchange kernels set them, the word is copied to pinned host memory right
 # after the router / the dispatch barrier, and moe_forward raises after
 # waiting for that early point of the step only (the GEMMs stay queued).
-ST_NONFINITE, ST_PEER_ABORT, ST_OVERSIZE, ST_DUPLICATE = 1, 2, 4, 8
+ST_NONFINITE, ST_PEER_ABORT, ST_OVERSIZE, ST_DUPLICATE, ST_RECV_OVERFLOW = 1, 2, 4, 8, 16
 _STATUS: Dict[tuple, tuple] = {}
 _SIDE: Dict[tuple, torch.cuda.Stream] = {}
 # measured neutral at 4 GPUs (C4: 36.4 vs 36.0 ms/step): the barrier wait it
@@ -346,6 +346,9 @@ def _raise_status(bits: int, what: str = "") -> None:
     if bits & ST_OVERSIZE:
         raise ValidationError(f"token block exceeds the peer buffers{what}: pass peer_tokens >= the "
                               "largest block on first use", constraint="peer-capacity")
+    if bits & ST_RECV_OVERFLOW:
+        raise ProtocolError(f"this step's routing overflows the peer receive buffers{what}: raise "
+                            "peer_capacity (None = worst case) or rebalance the router")
     if bits & ST_PEER_ABORT:
         raise ProtocolError(f"a member of the expert-parallel exchange failed this step{what}")
 
@@ -356,7 +359,8 @@ class RankLayer:
     def __init__(self, params: GatingParams, weights: X.ExpertWeights, topology: ParallelTopology,
                  groups: LayerGroups, rank: int, dtype, device, seq_len=None, check=False,
                  shared: Optional[X.ExpertWeights] = None, pad_to_capacity: bool = False,
-                 exchange: Optional[str] = None, peer_tokens: Optional[int] = None, peer_tag=0):
+                 exchange: Optional[str] = None, peer_tokens: Optional[int] = None, peer_tag=0,
+                 peer_capacity: Optional[float] = None):
         self.shared_pk = None if shared is None else shared.packed(dtype, device)
         # pad-to-capacity (BASELINE C3): every expert segment holds exactly
         # round_up(cap, ALIGN) rows, so all exchange sizes are static and the
@@ -391,6 +395,7 @@ class RankLayer:
         # return direction is the tensor-core GEMM's scatter epilogue), or
         # NCCL (B200MOE_EP_EXCHANGE=nccl, and the fp32 parity mode)
         self.peer_tokens = peer_tokens
+        self.peer_capacity = peer_capacity
         self.peer_tag = peer_tag
         want = exchange or os.environ.get("B200MOE_EP_EXCHANGE", "peer")
         if want not in ("peer", "nccl"):
@@ -754,7 +759,7 @@ class RankLayer:
             if len({bool(v[1]) for v in got.values()}) != 1:
                 raise ProtocolError("B200MOE_PUSH_DEDUP differs between the members of the exchange "
                                     f"{xch}: {[bool(got[r][1]) for r in xch]}")
-            cap = PX.capacity_rows(len(xch), T_max, self.k, self.L, ALIGN)
+            cap = PX.capacity_rows(len(xch), T_max, self.k, self.L, ALIGN, self.peer_capacity)
             ret = T_max * self.k + self.E * (ALIGN - 1)  # this rank's padded pair layout
             if self.pad_to_capacity and not self.params.dropless:
                 seg = (capacity_limit(self.params.capacity_factor, T_max, self.E) + ALIGN - 1) // ALIGN
@@ -941,7 +946,7 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
                 seq_len: Optional[int] = None, workers: Optional[int] = None, *, dtype=None,
                 check_finite_inputs: bool = True, shared_weights: Optional[X.ExpertWeights] = None,
                 pad_to_capacity: bool = False, exchange: Optional[str] = None,
-                peer_tokens: Optional[int] = None, peer_tag=0):
+                peer_tokens: Optional[int] = None, peer_tag=0, peer_capacity: Optional[float] = None):
     """Run the MoE layer forward on every rank of ``world`` (dispatcher.py:246-384).
 
     ``world`` is a LocalWorld (all ranks in this process) or an NcclWorld
@@ -953,6 +958,10 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
     The peer buffers are allocated on first use for the largest token block
     of that call (or ``peer_tokens`` if larger); layers whose forward and
     backward interleave need distinct ``peer_tag`` values (their own buffers).
+    The receive buffers hold the worst case (every sender's tokens routed to
+    one rank) unless ``peer_capacity`` = f sizes them for f times the
+    balanced load; a step whose routing overflows them then raises
+    ``ProtocolError`` on every rank (no rank traps).
     """
     pending = world.__dict__.pop("_b200moe_pending", None)
     if pending is not None:  # a previous step whose backward never ran
@@ -976,7 +985,7 @@ def moe_forward(blocks, weights_map, topology: ParallelTopology, params: GatingP
                           pad_to_capacity=pad_to_capacity, exchange=exchange,
                           peer_tokens=max([int(peer_tokens or 0)] + [b_.values.shape[0] for b_ in blocks
                                                                      if b_ is not None]),
-                          peer_tag=peer_tag)
+                          peer_tag=peer_tag, peer_capacity=peer_capacity)
         out, saved = layer.forward(ctx, b.values, b.positions)
         saved["layer"] = layer
         return out, saved
@@ -1014,7 +1023,7 @@ def _check_step(context: ForwardContext, block: bool) -> bool:
         ev.synchronize()
     context.__dict__["_checked"] = True
     bits = {r: int(layer.status_host[0]) if layer.status_event is not None else 0 for r, layer in layers}
-    for mask in (ST_NONFINITE, ST_DUPLICATE, ST_OVERSIZE, ST_PEER_ABORT):  # the root cause first
+    for mask in (ST_NONFINITE, ST_DUPLICATE, ST_OVERSIZE, ST_RECV_OVERFLOW, ST_PEER_ABORT):  # root cause first
         for r in sorted(bits):
             if bits[r] & mask:
                 if mask == ST_NONFINITE:

@@ -14,6 +14,8 @@ group; the grouped GEMMs read the group offsets from device memory.
 """
 from __future__ import annotations
 
+import warnings
+
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -199,12 +201,24 @@ def init_expert_weights(num_experts: int, hidden: int, ffn: int, etp_size: int, 
 
 
 # --------------------------------------------------------------- grouped FFN
+_SIMT_WARNED = set()
+
+
 def _gemm(A, B, C, **kw):
-    """Grouped GEMM dispatch: tcgen05 for bf16 when available, SIMT otherwise."""
+    """Grouped GEMM dispatch: tcgen05 for bf16 when available, SIMT otherwise
+    (fp32 parity mode, or bf16 shapes the tensor-core kernel rejects -- the
+    latter is a ~20x slower path, so it warns once per shape)."""
     from . import gemm_tc
 
-    if A.dtype == torch.bfloat16 and gemm_tc.available() and gemm_tc.supports(**kw):
-        return gemm_tc.gemm(A, B, C, **kw)
+    if A.dtype == torch.bfloat16:
+        if gemm_tc.available() and gemm_tc.supports(**kw):
+            return gemm_tc.gemm(A, B, C, **kw)
+        key = (kw.get("N"), kw.get("K"), kw.get("M"), kw.get("grouped_dim"))
+        if key not in _SIMT_WARNED:
+            _SIMT_WARNED.add(key)
+            warnings.warn(f"b200moe: bf16 GEMM N={key[0]} K={key[1]} M={key[2]} is not supported by the "
+                          "tcgen05 kernel (H and the FFN shard must be multiples of 8, SwiGLU of 32); "
+                          "running the CUDA-core SIMT GEMM", RuntimeWarning, stacklevel=3)
     return K.gemm_simt(A, B, C, **kw)
 
 

@@ -31,7 +31,8 @@ synchronize -- the same kernels run on both.
 """
 from __future__ import annotations
 
-from typing import Dict, Tuple
+import math
+from typing import Dict, Optional, Tuple
 
 import numpy as np
 
@@ -49,10 +50,14 @@ def _up(n: int, a: int) -> int:
     return (n + a - 1) // a * a
 
 
-def capacity_rows(ep: int, T_max: int, k: int, L_: int, align: int) -> int:
+def capacity_rows(ep: int, T_max: int, k: int, L_: int, align: int, factor: Optional[float] = None) -> int:
     """Receive rows a rank can need: every sender routes each of its tokens
-    to at most min(k, L) of this rank's experts, plus one pad per expert."""
-    return ep * T_max * min(k, L_) + L_ * (align - 1)
+    to at most min(k, L) of this rank's experts, plus one pad per expert.
+    ``factor`` f sizes for f times the balanced load (T_max * k rows) instead,
+    capped at that worst case; an overflowing step fails cleanly (status)."""
+    worst = ep * T_max * min(k, L_)
+    rows = worst if factor is None else min(worst, int(math.ceil(factor * T_max * k)))
+    return rows + L_ * (align - 1)
 
 
 def wire_rows(send_counts, topology) -> int:
