@@ -216,9 +216,9 @@ def _gemm(A, B, C, **kw):
         key = (kw.get("N"), kw.get("K"), kw.get("M"), kw.get("grouped_dim"))
         if key not in _SIMT_WARNED:
             _SIMT_WARNED.add(key)
-            warnings.warn(f"b200moe: bf16 GEMM N={key[0]} K={key[1]} M={key[2]} is not supported by the "
-                          "tcgen05 kernel (H and the FFN shard must be multiples of 8, SwiGLU of 32); "
-                          "running the CUDA-core SIMT GEMM", RuntimeWarning, stacklevel=3)
+            warnings.warn(f"b200moe: bf16 GEMM N={key[0]} K={key[1]} M={key[2]} falls outside the tcgen05 "
+                          "kernel's supported shapes (gemm_tc.supports; INTEGRATION.md §1); running the "
+                          "CUDA-core SIMT GEMM", RuntimeWarning, stacklevel=3)
     return K.gemm_simt(A, B, C, **kw)
 
 

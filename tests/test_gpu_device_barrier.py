@@ -185,28 +185,39 @@ def test_smaller_receive_buffers_and_clean_overflow():
     """peer_capacity sizes the receive buffers for f x the balanced load
     instead of the worst case; a step whose routing overflows them fails on
     every rank with ProtocolError (no trap) and the next step runs."""
-    H, F, E, k, seed = 128, 256, 8, 2, 6
+    H, F, E, k, T, seed = 128, 256, 8, 2, 256, 6
     topo = B.ParallelTopology(world_size=2, ep=2)
-    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k)
     weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
-    blocks, ups = _blocks((256, 256), H, seed)
-    ref = _run(B.LocalWorld(2), topo, params, weights, blocks, ups)
+    # feature 0 steers the routing: +1 -> experts 0, 1 (rank 0); -1 -> 4, 5 (rank 1)
+    wg = np.zeros((H, E))
+    wg[0, 0], wg[0, 1], wg[0, 4], wg[0, 5] = 2.0, 1.0, -2.0, -1.0
+    params = B.GatingParams(w_g=wg, k=k)
+    rng = np.random.default_rng(seed)
+
+    def blocks_with(signs):
+        out = []
+        for r, sgn in enumerate(signs):
+            x = rng.standard_normal((T, H)) * 0.1
+            x[:, 0] = sgn
+            out.append(B.TokenBlock(torch.as_tensor(x, dtype=torch.float32).to("cuda", torch.bfloat16),
+                                    np.arange(r * T, (r + 1) * T)))
+        return out
+
+    ups = [torch.randn((T, H), device="cuda").to(torch.bfloat16) for _ in range(2)]
+    split = blocks_with((1.0, -1.0))  # 512 rows to each rank
+    skew = blocks_with((1.0, 1.0))  # 1024 rows to rank 0
+    ref = _run(B.LocalWorld(2), topo, params, weights, split, ups)
     for barrier in (False, True):
         world = B.LocalWorld(2, device_barrier=barrier)
-        outs, ctx = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16,
-                                  peer_capacity=1.5)
+        outs, ctx = B.moe_forward(split, weights, topo, params, world, dtype=torch.bfloat16, peer_capacity=1.0)
         res = B.moe_backward(ups, ctx)
         torch.cuda.synchronize()
-        assert ctx.per_rank[0]["peer"].cap < 2 * 256 * 2  # smaller than the worst case
+        from paper_2504_14960_b200.peer import capacity_rows
+
+        cap = ctx.per_rank[0]["peer"].cap
+        assert cap == capacity_rows(2, T, k, E // 2, 128, 1.0) < capacity_rows(2, T, k, E // 2, 128)
         _same(ref, (outs, ctx, res))
-        # every token to experts 0 and 1 (both on rank 0): 2 x 256 x 2 rows > 1.5 x 256 x 2
-        wg = -np.ones((H, E)) / H
-        wg[:, 0], wg[:, 1] = 2.0 / H, 1.0 / H
-        skew = B.GatingParams(w_g=wg, k=k)
-        pos = [torch.as_tensor(np.abs(np.random.default_rng(r).standard_normal((256, H))) + 0.1)
-               .to("cuda", torch.bfloat16) for r in range(2)]
-        sblocks = [B.TokenBlock(pos[r], np.arange(r * 256, (r + 1) * 256)) for r in range(2)]
         with pytest.raises(ProtocolError, match="overflows the peer receive buffers"):
-            _, c2 = B.moe_forward(sblocks, weights, topo, skew, world, dtype=torch.bfloat16)
+            _, c2 = B.moe_forward(skew, weights, topo, params, world, dtype=torch.bfloat16)
             B.moe_backward(ups, c2)
-        _same(ref, _run(world, topo, params, weights, blocks, ups))
+        _same(ref, _run(world, topo, params, weights, split, ups))
