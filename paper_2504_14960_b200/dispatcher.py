@@ -234,6 +234,16 @@ class ForwardContext:
     groups: GroupSets
     per_rank: List[dict] = field(default_factory=list)
 
+    def check(self) -> None:
+        """Wait for the step's device status and raise what it flagged
+        (NumericError / ProtocolError / ValidationError, router.py:141-144):
+        the explicit synchronisation point; moe_forward / moe_backward raise
+        without waiting when the status has already landed, and the next
+        moe_forward on the world raises a pending one."""
+        _check_step(self, block=True)
+        if self.world.__dict__.get("_b200moe_pending") is self:
+            del self.world.__dict__["_b200moe_pending"]
+
 
 @dataclass
 class BackwardResult:
@@ -327,8 +337,8 @@ def _side_stream(device, main) -> "torch.cuda.Stream":
     return _SIDE[key]
 
 
-def _status_slot(device, rank: int):
-    key = (str(device), rank)
+def _status_slot(device, rank: int, tag=0):
+    key = (str(device), rank, tag)
     slot = _STATUS.get(key)
     if slot is None:
         slot = (torch.zeros((1,), dtype=torch.int32, device=device),
@@ -405,7 +415,7 @@ class RankLayer:
                          and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
         # step status (see _status_slot): the router writes bit 0 into the
         # checked word only when inputs are validated
-        self.status, self.status_host, self.scratch = _status_slot(device, rank)
+        self.status, self.status_host, self.scratch = _status_slot(device, rank, peer_tag)
         self.status_event = None
 
     # ------------------------------------------------------- shared expert
@@ -801,7 +811,7 @@ class RankLayer:
     def _backward_peer(self, ctx, u, sv, dec, plan):
         px, st = sv["peer"], sv["pst"]
         px.check_generation(st)
-        dgates = px.backward_dispatch(u, dec.experts, plan, dec.gates, st, sv["y"], ALIGN)
+        dgates = px.backward_dispatch(u, dec.experts, plan, dec.gates, st, sv["y"], ALIGN, status=self.status)
         _, dw1p, dw2p = X.ffn_backward(px.region("dyr"), px.region("xr"), sv["pre"], sv["h"],
                                        st["goff"], self.L, None, self.pk, px.cap,
                                        dx_scatter=px.scatter("dxret"))
@@ -1035,8 +1045,11 @@ def _check_step(context: ForwardContext, block: bool) -> bool:
 def moe_backward(upstream, context: ForwardContext, workers: Optional[int] = None) -> BackwardResult:
     """Gradients of sum over ranks of <upstream, output> (dispatcher.py:387-510)."""
     topology = context.topology
-    _check_step(context, block=True)  # by now long complete: the forward's dispatch barrier
-    if context.world.__dict__.get("_b200moe_pending") is context:
+    # the forward's status, if it has landed (it normally has); a flagged step
+    # pushes nothing in the backward either (the exchange kernels check the
+    # same word), so an unchecked status is raised after the backward or by
+    # the next moe_forward -- never a host stall in a pipelined loop
+    if _check_step(context, block=False) and context.world.__dict__.get("_b200moe_pending") is context:
         del context.world.__dict__["_b200moe_pending"]
     if len(upstream) != topology.world_size:
         raise ValidationError(f"{len(upstream)} upstream blocks for world_size {topology.world_size}",
@@ -1069,6 +1082,10 @@ def moe_backward(upstream, context: ForwardContext, workers: Optional[int] = Non
         return dx, dwg, dw1p, dw2p, layer.pk.act, shared
 
     results = context.world.run(program, workers=workers)
+    if _check_step(context, block=False) and context.world.__dict__.get("_b200moe_pending") is context:
+        del context.world.__dict__["_b200moe_pending"]
+    elif not context.__dict__.get("_checked"):
+        context.world.__dict__["_b200moe_pending"] = context
     input_grads = [None if r is None else r[0] for r in results]
     w_g_grad = next(r[1] for r in results if r is not None)
     shared = next(r[5] for r in results if r is not None)

@@ -215,12 +215,14 @@ class PeerExchange:
         self.generation += 1
         return dict(seg_off=seg_off, goff=goff, gcount=gcount, generation=self.generation)
 
-    def backward_dispatch(self, u, topk_idx, plan, gates, st, y_rows, align: int):
-        """pads -> push g*u rows (dgates from the returned y) -> barrier."""
+    def backward_dispatch(self, u, topk_idx, plan, gates, st, y_rows, align: int, status=None):
+        """pads -> push g*u rows (dgates from the returned y) -> barrier.
+        Nothing is pushed when the forward's ``status`` flagged the step."""
         K.ep_zero_pads(self.region("dyr"), st["goff"], st["gcount"], self.L, align)
         dg = K.ep_dispatch(u, topk_idx, plan.gemm_row, plan.poffsets, st["seg_off"], self.L,
                            self.peer_base, self.me, self.etp, self.off["dyr"], bwd=True,
-                           y_rows=y_rows, gates=gates, dup_off=self.off["dup"] if self.dedup else -1)
+                           y_rows=y_rows, gates=gates, dup_off=self.off["dup"] if self.dedup else -1,
+                           status=status)
         self.barrier()
         if self.dedup:
             K.ep_expand(self.region("dyr"), st["goff"], st["gcount"], self.L, self.dup(), 1)

@@ -39,6 +39,7 @@ def _run(world, topo, params, weights, blocks, ups, shared=None):
     outs, ctx = B.moe_forward(blocks, weights, topo, params, world, dtype=torch.bfloat16,
                               shared_weights=shared)
     res = B.moe_backward(ups, ctx)
+    ctx.check()
     torch.cuda.synchronize()
     return outs, ctx, res
 
@@ -220,4 +221,5 @@ def test_smaller_receive_buffers_and_clean_overflow():
         with pytest.raises(ProtocolError, match="overflows the peer receive buffers"):
             _, c2 = B.moe_forward(skew, weights, topo, params, world, dtype=torch.bfloat16)
             B.moe_backward(ups, c2)
+            c2.check()
         _same(ref, _run(world, topo, params, weights, split, ups))

@@ -134,6 +134,7 @@ def test_peer_buffers_reused_before_backward_fail_loudly():
     with pytest.raises(ValidationError, match="peer buffers"):  # from moe_forward or, deferred, moe_backward
         _, ctx_big = B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
         B.moe_backward(_blocks((128, 64), H, 3)[1], ctx_big)
+        ctx_big.check()
 
 
 def test_peer_tags_and_headroom():

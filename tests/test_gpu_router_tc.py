@@ -125,12 +125,14 @@ def test_layer_nonfinite_raises_without_blocking_check(dtype):
     with pytest.raises(NumericError, match="token block"):
         _, ctx = B.moe_forward([B.TokenBlock(x, np.arange(T))], weights, topo, params, B.LocalWorld(1))
         B.moe_backward(u, ctx)
+        ctx.check()
     wbad = O.gating_matrix(H, E, 0)
     wbad[3, 2] = np.inf
     with pytest.raises(NumericError, match="gating weights"):
         _, ctx = B.moe_forward([B.TokenBlock(torch.randn((T, H), device="cuda").to(dtype), np.arange(T))],
                                weights, topo, B.GatingParams(w_g=wbad, k=k), B.LocalWorld(1))
         B.moe_backward(u, ctx)
+        ctx.check()
     # a flagged forward without its backward is raised by the next forward on that world
     w1 = B.LocalWorld(1)
     try:
