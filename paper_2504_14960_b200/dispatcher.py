@@ -354,8 +354,9 @@ def _raise_status(bits: int, what: str = "") -> None:
     if bits & ST_DUPLICATE:
         raise ProtocolError(f"full-sequence gather: duplicate token positions across shards{what}")
     if bits & ST_OVERSIZE:
-        raise ValidationError(f"token block exceeds the peer buffers{what}: pass peer_tokens >= the "
-                              "largest block on first use", constraint="peer-capacity")
+        raise ValidationError(f"token block exceeds the peer buffers / full-sequence gather slots sized on "
+                              f"first use{what}: pass peer_tokens >= the largest block on first use",
+                              constraint="peer-capacity")
     if bits & ST_RECV_OVERFLOW:
         raise ProtocolError(f"this step's routing overflows the peer receive buffers{what}: raise "
                             "peer_capacity (None = worst case) or rebalance the router")
@@ -788,7 +789,7 @@ class RankLayer:
         if oversize:
             # the block does not fit the peers' buffers: take part in the
             # step's protocol without tokens and fail it everywhere (status)
-            self.status.fill_(ST_OVERSIZE)
+            self.status.bitwise_or_(ST_OVERSIZE)
             st = px.forward_dispatch(x[:0], dec.experts[:0], plan, ALIGN, status=self.status)
         else:
             st = px.forward_dispatch(x, dec.experts, plan, ALIGN, status=self.status)

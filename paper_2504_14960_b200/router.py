@@ -330,9 +330,14 @@ def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: i
     dev = local.experts.device
     if slots is None:
         slots = max(int(v) for v in ctx.meta(group, n).values())
-    if n > slots:
-        raise ValidationError(f"token block of {n} rows exceeds the {slots} full-sequence gather slots",
-                              constraint="fullseq-slots")
+    oversize = n > slots
+    if oversize:
+        if status is None:
+            raise ValidationError(f"token block of {n} rows exceeds the {slots} full-sequence gather slots",
+                                  constraint="fullseq-slots")
+        # the layer path: take part in the group's gather with no pairs and
+        # fail the step through the status word (bit 2) on every rank
+        status.bitwise_or_(4)
     S = slots * k
     pos_h = local.positions
     if pos_h.is_cuda:
@@ -342,7 +347,7 @@ def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: i
     pad = torch.iinfo(torch.int64).max
     seg = torch.full((S,), pad, dtype=torch.int64, device=dev)
     ppos = torch.full((S,), pad, dtype=torch.int64, device=dev)
-    if n:
+    if n and not oversize:
         seg[:n * k] = ((pos // seq_len)[:, None] * E + local.experts.to(torch.int64)).reshape(-1)
         ppos[:n * k] = pos.repeat_interleave(k)
     # the reference's wire record: (pos, slot, expert, gate) rows of width 4
@@ -356,7 +361,7 @@ def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: i
     if prob or want_global:
         g = local.gates_f64 if local.gates_f64 is not None else local.gates.double()
         gp = torch.full((S,), float("-inf"), dtype=torch.float64, device=dev)
-        if n:
+        if n and not oversize:
             gp[:n * k] = g.reshape(-1)
         g64 = ctx.all_gather_fixed(group, gp).view(-1)
     if prob:
@@ -369,7 +374,10 @@ def gather_full_sequence_decision(ctx, group, local: RoutingDecision, seq_len: i
     if status is None and check and int(own_status.item()) & 8:
         raise ProtocolError("full-sequence gather: duplicate token positions across shards")
     out = local.copy()
-    out.kept = kept_slot.view(len(group), S)[me, :n * k].view(n, k).bool()
+    if oversize:
+        out.kept = torch.zeros((n, k), dtype=torch.bool, device=dev)
+    else:
+        out.kept = kept_slot.view(len(group), S)[me, :n * k].view(n, k).bool()
     global_dec = None
     if want_global:
         # the group's pairs in position order (sizes read on the host: API use only)

@@ -139,3 +139,27 @@ def test_c5_like_full_sequence_layer_vs_oracle(exchange):
     recs = [rec for rec in ctx.world.ledger if rec.row_width == 4]
     assert len(recs) == 1 and recs[0].group == (0, 1, 2, 3)
     assert recs[0].elements_sent == tuple(4 * k * b.values.shape[0] * 3 for b in blocks)
+
+
+def test_full_sequence_oversized_block_fails_every_rank():
+    """A block larger than the gather slots agreed on first use fails the step
+    on every rank through the status word (no rank leaves the collective)."""
+    E, k, H, F, seq_len, seed = 8, 2, 64, 128, 256, 2
+    topo = B.ParallelTopology(world_size=2, tp=2, ep=2)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=1.0,
+                            drop_mode="fullsequence")
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
+    world = B.LocalWorld(2)
+    _, blocks = B.fabricate_token_blocks(topo, seq_len, topo.dp, H, seed, dtype=torch.bfloat16)
+    _, ups = B.fabricate_upstream(topo, seq_len, topo.dp, H, seed, dtype=torch.bfloat16)
+    _, c = B.moe_forward(blocks, weights, topo, params, world, seq_len=seq_len)
+    B.moe_backward(ups, c)
+    c.check()
+    _, big = B.fabricate_token_blocks(topo, 2 * seq_len, topo.dp, H, seed, dtype=torch.bfloat16)
+    _, bigu = B.fabricate_upstream(topo, 2 * seq_len, topo.dp, H, seed, dtype=torch.bfloat16)
+    from paper_2504_14960_b200.errors import ValidationError
+
+    with pytest.raises(ValidationError, match="first use"):
+        _, c2 = B.moe_forward(big, weights, topo, params, world, seq_len=2 * seq_len)
+        B.moe_backward(bigu, c2)
+        c2.check()

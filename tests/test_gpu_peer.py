@@ -131,7 +131,7 @@ def test_peer_buffers_reused_before_backward_fail_loudly():
         B.moe_backward(ups, ctx_a)
     # a later, larger token block than the buffers were sized for
     big, _ = _blocks((128, 64), H, 2)
-    with pytest.raises(ValidationError, match="peer buffers"):  # from moe_forward or, deferred, moe_backward
+    with pytest.raises(ValidationError, match="peer buffers"):  # from moe_forward, moe_backward or check()
         _, ctx_big = B.moe_forward(big, weights, topo, params, world, dtype=torch.bfloat16)
         B.moe_backward(_blocks((128, 64), H, 3)[1], ctx_big)
         ctx_big.check()
