@@ -397,3 +397,39 @@ def test_load_stats_kernel_vs_oracle(E, k, n, gate):
     if n:
         assert abs(got.imbalance - want[1]) < 1e-12
         assert abs(got.aux_loss - want[2]) < 1e-6 * max(1.0, abs(want[2]))
+
+
+@pytest.mark.parametrize("gate_fn,renorm,priority", [("softmax", True, "probability"), ("sigmoid", False, "probability"),
+                                                     ("sigmoid", True, "position")])
+def test_bf16_layer_gating_variants_vs_oracle(gate_fn, renorm, priority):
+    """bf16 layer through the fused tensor-core router (router_tc.cu) with the
+    gating variants the golden layer cases do not cover: renormalised gates,
+    sigmoid, probability-priority dropping (router.py:146-153, 195).  Kept
+    masks equal the oracle's on the GPU logits; outputs and gradients within
+    the bf16 tolerance."""
+    E, k, H, F, T, seed = 8, 2, 512, 1024, 2048, 4
+    topo = B.ParallelTopology(world_size=1)
+    wg = O.gating_matrix(H, E, seed)
+    params = B.GatingParams(w_g=wg, k=k, gate_fn=gate_fn, renormalize_topk=renorm, capacity_factor=1.0,
+                            drop_priority=priority)
+    weights = B.init_expert_weights(E, H, F, 1, seed, activation="swiglu")
+    x = O.token_rows(T, H, seed, 2)
+    u = O.token_rows(T, H, seed, 3)
+    xb, ub = t(x, torch.bfloat16), t(u, torch.bfloat16)
+    outs, ctx = B.moe_forward([B.TokenBlock(xb, np.arange(T))], weights, topo, params, B.LocalWorld(1))
+    res = B.moe_backward([ub], ctx)
+    ctx.check()
+    lg = ctx.per_rank[0]["logits"].cpu().numpy().astype(np.float64)
+    w0 = weights[(0, 0)]
+    experts = [O.Expert(np.asarray(a), np.asarray(b), "swiglu") for a, b in zip(w0.w1, w0.w2)]
+    cfg = O.LayerConfig(k=k, gate_fn=gate_fn, renormalize=renorm, capacity_factor=1.0, drop_priority=priority)
+    xin = xb.float().cpu().numpy().astype(np.float64)
+    uin = ub.float().cpu().numpy().astype(np.float64)
+    y, st = O.layer_forward(xin, lg, experts, cfg)
+    g = O.layer_backward(uin, st, experts, cfg, w_g=wg)
+    dec = ctx.per_rank[0]["decision"]
+    np.testing.assert_array_equal(dec.experts.cpu().numpy(), st.routing.experts)
+    np.testing.assert_array_equal(dec.kept.cpu().numpy(), st.routing.kept)
+    assert O.rel_err(outs[0].float().cpu().numpy(), y) < BF16_TOL
+    assert O.rel_err(res.input_grads[0].float().cpu().numpy(), g[0]) < BF16_TOL
+    assert O.rel_err(res.w_g_grad.cpu().numpy(), g[2]) < BF16_TOL
