@@ -340,6 +340,31 @@ B200MOE_API int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, 
                                     int64_t origin_off, int64_t dup_off, const void* y_rows,
                                     const float* gates, float* dgates, int bwd, const int32_t* status,
                                     void* stream);
+/* b200moe_ep_dispatch split in two for overlapping the exchange with the
+ * first expert GEMM: part 1 performs only the stores into this rank's own
+ * buffers (the rows its experts take from itself), part 2 only those into
+ * the other members' (NVLink); part 0 = both (b200moe_ep_dispatch).  Each
+ * pair's dgate (backward) is written by exactly one part: part 1 for pairs
+ * routed to this rank's EP index, part 2 for the rest.  Part 2 launches one
+ * small block per SM whose register budget fits beside a resident
+ * b200moe_gemm_tc CTA, so it runs concurrently with a GEMM on another
+ * stream. */
+B200MOE_API int b200moe_ep_dispatch_part(const void* x, int64_t T, int64_t H, int k, int L,
+                                         const int32_t* topk_idx, const int32_t* gemm_row,
+                                         const int32_t* poff, const int32_t* seg_off,
+                                         const uint64_t* peer_base, int me, int etp, int64_t dst_off,
+                                         int64_t origin_off, int64_t dup_off, const void* y_rows,
+                                         const float* gates, float* dgates, int bwd, int part,
+                                         const int32_t* status, void* stream);
+/* GEMM groups of the split first GEMM, from the layout of b200moe_ep_layout:
+ * per local expert, the rows this rank sent itself (available before the
+ * barrier) and the rest (two groups: before and after them, pads included).
+ * split (int32, 8L + 2) = loc_off[L+1] | loc_end[L] | rem_off[2L+1] |
+ * rem_end[2L] | rem_exp[2L] -- b200moe_gemm_tc group_off / group_end /
+ * group_expert arrays; loc_off[L] = rem_off[2L] = goff[L]. */
+B200MOE_API int b200moe_ep_split_groups(const int32_t* cnt_local, int me, int ep, int etp, int L,
+                                        const int32_t* seg_off, const int32_t* goff, const int32_t* gcount,
+                                        int32_t* split, void* stream);
 /* Receiver side of the deduplicated push (dispatcher.py:317-323's regroup
  * has no counterpart: the reference moves every pair): over the real rows
  * goff[g] .. goff[g] + gcount[g] of the bf16 [rows, H] receive buffer, with

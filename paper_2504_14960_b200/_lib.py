@@ -78,6 +78,9 @@ _SIGS = {
     "b200moe_ep_reduce_parts": [P, I32, I64, I64, P, P],
     "b200moe_ep_zero_pads": [P, I64, P, P, I32, I32, P, P],
     "b200moe_ep_dispatch": [P, I64, I64, I32, I32, P, P, P, P, P, I32, I32, I64, I64, I64, P, P, P, I32, P, P],
+    "b200moe_ep_dispatch_part": [P, I64, I64, I32, I32, P, P, P, P, P, I32, I32, I64, I64, I64, P, P, P, I32,
+                                 I32, P, P],
+    "b200moe_ep_split_groups": [P, I32, I32, I32, I32, P, P, P, P, P],
     "b200moe_ep_expand": [P, I64, P, P, I32, P, I32, P],
 }
 _RESTYPES = {
@@ -195,12 +198,12 @@ class Profile:
 PROFILE = Profile()
 
 
-def call(name: str, *args) -> None:
+def call(name: str, *args, tag: Optional[str] = None) -> None:
     lib = load()
     e0 = PROFILE.begin() if PROFILE.on and name not in _NO_LAUNCH else None
     check(getattr(lib, name)(*args), name)
     if e0 is not None:
-        PROFILE.end(name.replace("b200moe_", ""), e0)
+        PROFILE.end(tag or name.replace("b200moe_", ""), e0)
     if name not in _NO_LAUNCH:
         n = _LAUNCHES.get(name, 1)
         if name in ("b200moe_permute", "b200moe_permute_bwd") and args[-5]:

@@ -54,7 +54,9 @@ int ep_reduce_parts(const void*, int, int64_t, int64_t, void*, cudaStream_t);
 int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
                 const int32_t*, const int32_t*, const uint64_t*, int, int, int64_t, int64_t, int64_t,
-                const void*, const float*, float*, int, const int32_t*, cudaStream_t);
+                const void*, const float*, float*, int, int, const int32_t*, cudaStream_t);
+int ep_split_groups(const int32_t*, int, int, int, int, const int32_t*, const int32_t*, const int32_t*,
+                    int32_t*, cudaStream_t);
 int ep_expand(void*, int64_t, const int32_t*, const int32_t*, int, const void*, int, cudaStream_t);
 int split_bf16x3(const float*, int64_t, int, void*, void*, cudaStream_t);
 size_t router_stats_ws_bytes(int64_t, int);
@@ -344,18 +346,36 @@ int b200moe_ep_zero_pads(void* buf, int64_t H, const int32_t* goff, const int32_
   return ep_zero_pads(buf, H, goff, gcount, G, align, origin, S(stream));
 }
 
+int b200moe_ep_dispatch_part(const void* x, int64_t T, int64_t H, int k, int L, const int32_t* topk_idx,
+                             const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
+                             const uint64_t* peer_base, int me, int etp, int64_t dst_off,
+                             int64_t origin_off, int64_t dup_off, const void* y_rows, const float* gates,
+                             float* dgates, int bwd, int part, const int32_t* status, void* stream) {
+  REQUIRE(H % 8 == 0 && k >= 1 && L >= 1 && me >= 0 && etp >= 1 && etp <= 32 && part >= 0 && part <= 2,
+          "ep_dispatch: H %% 8, k >= 1, me >= 0, 1 <= etp <= 32, part in [0, 2] required");
+  if (T == 0) return B200MOE_OK;
+  REQUIRE(x && topk_idx && gemm_row && poff && seg_off && peer_base, "ep_dispatch: null pointer");
+  REQUIRE(!bwd || (gates && dgates && y_rows), "ep_dispatch: backward needs gates, dgates, y_rows");
+  return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, etp, dst_off,
+                     origin_off, dup_off, y_rows, gates, dgates, bwd, part, status, S(stream));
+}
+
 int b200moe_ep_dispatch(const void* x, int64_t T, int64_t H, int k, int L, const int32_t* topk_idx,
                         const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
                         const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
                         int64_t dup_off, const void* y_rows, const float* gates, float* dgates, int bwd,
                         const int32_t* status, void* stream) {
-  REQUIRE(H % 8 == 0 && k >= 1 && L >= 1 && me >= 0 && etp >= 1 && etp <= 32,
-          "ep_dispatch: H %% 8, k >= 1, me >= 0, 1 <= etp <= 32 required");
-  if (T == 0) return B200MOE_OK;
-  REQUIRE(x && topk_idx && gemm_row && poff && seg_off && peer_base, "ep_dispatch: null pointer");
-  REQUIRE(!bwd || (gates && dgates && y_rows), "ep_dispatch: backward needs gates, dgates, y_rows");
-  return ep_dispatch(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, etp, dst_off,
-                     origin_off, dup_off, y_rows, gates, dgates, bwd, status, S(stream));
+  return b200moe_ep_dispatch_part(x, T, H, k, L, topk_idx, gemm_row, poff, seg_off, peer_base, me, etp,
+                                  dst_off, origin_off, dup_off, y_rows, gates, dgates, bwd, 0, status,
+                                  stream);
+}
+
+int b200moe_ep_split_groups(const int32_t* cnt_local, int me, int ep, int etp, int L, const int32_t* seg_off,
+                            const int32_t* goff, const int32_t* gcount, int32_t* split, void* stream) {
+  REQUIRE(cnt_local && seg_off && goff && gcount && split && ep >= 1 && etp >= 1 && ep * etp <= 32 &&
+              L >= 1 && me >= 0 && me < ep * etp,
+          "ep_split_groups: bad args");
+  return ep_split_groups(cnt_local, me, ep, etp, L, seg_off, goff, gcount, split, S(stream));
 }
 
 int b200moe_ep_expand(void* buf, int64_t H, const int32_t* goff, const int32_t* gcount, int G,

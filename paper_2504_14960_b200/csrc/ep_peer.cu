@@ -176,36 +176,41 @@ __global__ void ep_zero_pads_kernel(__nv_bfloat16* __restrict__ buf, int64_t H,
 //             (leader row, gate) -> phase 1 writes bf16(gate * raw) into the
 //             duplicates, phase 2 scales the raw leaders in place.
 // Each row ends up with exactly the value the undeduplicated push stores.
+//
+// Split push (part != 0), for overlapping the exchange with the first GEMM:
+// part 1 performs only the stores into this rank's own buffers (the rows its
+// own experts take from itself: origin, dup entries, data), part 2 only the
+// stores into the other members' buffers.  Each pair's dgate (backward) is
+// written by exactly one part: part 1 for pairs routed to this rank's EP
+// index, part 2 for the rest.  part 0 = everything (one launch).
 template <int KMAX, bool BWD>
-__global__ void __launch_bounds__(256) ep_dispatch_kernel(
-    const __nv_bfloat16* __restrict__ x, int64_t Tn, int64_t H, int k, int L,
+__device__ __forceinline__ void dispatch_token(
+    int64_t t, int lane, int64_t H, int k, int L, const __nv_bfloat16* __restrict__ x,
     const int32_t* __restrict__ topk, const int32_t* __restrict__ gemm_row,
     const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
-    const uint64_t* __restrict__ peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
-    int64_t dup_off, const __nv_bfloat16* __restrict__ y_rows, const float* __restrict__ gates,
-    float* __restrict__ dgates, const int32_t* __restrict__ status) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= Tn) return;
-  if (status && *status != 0) return;  // failed step: nothing is pushed (see counts_push)
-  __nv_bfloat16* dst[KMAX];
-  const __nv_bfloat16* ysrc[KMAX];
+    const uint64_t* __restrict__ peer_base, int me, int etp, int part, int64_t dst_off,
+    int64_t origin_off, int64_t dup_off, const __nv_bfloat16* __restrict__ y_rows,
+    const float* __restrict__ gates, float* __restrict__ dgates) {
+  const int self_mem = (me / etp) * etp;  // first member of this rank's EP index
+  // which members of a pair's destination EP index this part stores to
+  auto keep = [&](int mm) { return part == 0 || ((part == 1) == (mm == me)); };
   int mem[KMAX];
-  int32_t rrs[KMAX];
+  int32_t rrs[KMAX], grs[KMAX];
   int64_t roff[KMAX];
   float g[KMAX], dot[KMAX];
-  bool push[KMAX], scale[KMAX];
+  bool push[KMAX], scale[KMAX], wdg[KMAX];
+  bool work = false;
 #pragma unroll
   for (int s = 0; s < KMAX; ++s) {
-    dst[s] = nullptr;
     mem[s] = -1;
     rrs[s] = -1;
+    grs[s] = 0;
     roff[s] = 0;
-    ysrc[s] = nullptr;
     g[s] = 1.f;
     dot[s] = 0.f;
     push[s] = false;
     scale[s] = BWD;
+    wdg[s] = false;
     if (s >= k) continue;
     const int32_t gr = gemm_row[t * k + s];
     if (gr < 0) continue;
@@ -214,25 +219,35 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     const int32_t rr = seg_off[d * L + le] + (gr - poff[e]);
     mem[s] = d * etp;  // the ETP members of EP index d all get the row
     rrs[s] = rr;
+    grs[s] = gr;
     roff[s] = dst_off + (int64_t)rr * H * 2;
-    dst[s] = reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s]] + roff[s]);
     push[s] = true;
+    bool any = false;
+    for (int m = 0; m < etp; ++m) any |= keep(mem[s] + m);
     if (BWD) {
-      ysrc[s] = y_rows + (int64_t)gr * H;
       g[s] = gates[t * k + s];
-    } else if (lane < etp) {
+      wdg[s] = part == 0 || ((part == 1) == (mem[s] == self_mem));
+      any |= wdg[s];
+    } else if (lane < etp && keep(mem[s] + lane)) {
       int2* o = reinterpret_cast<int2*>(peer_base[mem[s] + lane] + origin_off) + rr;
       *o = make_int2(me, gr);
     }
+    work |= any;
+  }
+  if (!work) {  // warp-uniform: nothing of this token belongs to this part
+    if (BWD && part != 2 && lane == 0)
+      for (int s = 0; s < k && s < KMAX; ++s)
+        if (mem[s] < 0) dgates[t * k + s] = 0.f;  // dropped pairs
+    return;
   }
   if (dup_off >= 0) {
-    const int self_mem = (me / etp) * etp;  // rows for this rank's own EP index stay per pair:
-                                            // a local store is cheaper than a later copy
 #pragma unroll
     for (int s = 0; s < KMAX; ++s) {
       if (mem[s] < 0) continue;
-      if (mem[s] == self_mem) {
-        if (lane < etp) reinterpret_cast<int2*>(peer_base[mem[s] + lane] + dup_off)[rrs[s]] = make_int2(-1, 0);
+      if (mem[s] == self_mem) {  // rows for this rank's own EP index stay per pair (the
+                                 // local store; ETP siblings get their own copy)
+        if (lane < etp && keep(mem[s] + lane))
+          reinterpret_cast<int2*>(peer_base[mem[s] + lane] + dup_off)[rrs[s]] = make_int2(-1, 0);
         continue;
       }
       int lead = s, ndup = 0;
@@ -251,7 +266,8 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       } else {
         entry = make_int2(-1, 0);
       }
-      if (lane < etp) reinterpret_cast<int2*>(peer_base[mem[s] + lane] + dup_off)[rrs[s]] = entry;
+      if (lane < etp && keep(mem[s] + lane))
+        reinterpret_cast<int2*>(peer_base[mem[s] + lane] + dup_off)[rrs[s]] = entry;
     }
   }
   // U column chunks per iteration keep several 16 B loads in flight per lane
@@ -267,7 +283,7 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       if (BWD) {
 #pragma unroll
         for (int s = 0; s < KMAX; ++s)
-          if (dst[s] && c < H) y[u][s].raw = ld_nc_v4(ysrc[s] + c);
+          if (wdg[s] && c < H) y[u][s].raw = ld_nc_v4(y_rows + (int64_t)grs[s] * H + c);
       }
     }
 #pragma unroll
@@ -276,25 +292,24 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       if (c >= H) break;
 #pragma unroll
       for (int s = 0; s < KMAX; ++s) {
-        if (!dst[s]) continue;
+        if (mem[s] < 0) continue;
+        uint4 val;
         if (BWD) {
           Vec16<__nv_bfloat16> o;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float uv = __bfloat162float(v[u].v[i]);
-            dot[s] = fmaf(uv, __bfloat162float(y[BWD ? u : 0][BWD ? s : 0].v[i]), dot[s]);
+            if (wdg[s]) dot[s] = fmaf(uv, __bfloat162float(y[BWD ? u : 0][BWD ? s : 0].v[i]), dot[s]);
             o.v[i] = __float2bfloat16_rn(scale[s] ? uv * g[s] : uv);
           }
-          if (!push[s]) continue;
-          st_v4(dst[s] + c, o.raw);  // NVLink push
-          for (int m = 1; m < etp; ++m)
-            st_v4(reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s] + m] + roff[s]) + c, o.raw);
+          val = o.raw;
         } else {
-          if (!push[s]) continue;
-          st_v4(dst[s] + c, v[u].raw);  // NVLink push
-          for (int m = 1; m < etp; ++m)
-            st_v4(reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s] + m] + roff[s]) + c, v[u].raw);
+          val = v[u].raw;
         }
+        if (!push[s]) continue;
+        for (int m = 0; m < etp; ++m)  // NVLink push (or the local store)
+          if (keep(mem[s] + m))
+            st_v4(reinterpret_cast<__nv_bfloat16*>(peer_base[mem[s] + m] + roff[s]) + c, val);
       }
     }
   }
@@ -303,9 +318,30 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
     for (int s = 0; s < KMAX; ++s) {
       if (s >= k) break;
       const float d = warp_sum(dot[s]);
-      if (lane == 0) dgates[t * k + s] = dst[s] ? d : 0.f;
+      if (lane == 0 && (mem[s] < 0 ? part != 2 : wdg[s])) dgates[t * k + s] = mem[s] >= 0 ? d : 0.f;
     }
   }
+}
+
+// One warp per token, grid-stride.  NT = 256: the one-launch push (the whole
+// GPU).  NT = 128 (forward) / 64 (backward): the overlapped remote push, one
+// block per SM with a register budget (<= 80 / 144 per thread) that fits
+// next to a resident gemm_tc CTA (256 threads x 216 registers of 64 K), so
+// the push runs beside the GEMM instead of waiting for its SMs.
+template <int KMAX, bool BWD, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 1 : (NT == 128 ? 6 : 7)) ep_dispatch_kernel(
+    const __nv_bfloat16* __restrict__ x, int64_t Tn, int64_t H, int k, int L,
+    const int32_t* __restrict__ topk, const int32_t* __restrict__ gemm_row,
+    const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
+    const uint64_t* __restrict__ peer_base, int me, int etp, int part, int64_t dst_off,
+    int64_t origin_off, int64_t dup_off, const __nv_bfloat16* __restrict__ y_rows,
+    const float* __restrict__ gates, float* __restrict__ dgates, const int32_t* __restrict__ status) {
+  if (status && *status != 0) return;  // failed step: nothing is pushed (see counts_push)
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (NT / 32);
+  for (int64_t t = (int64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5); t < Tn; t += nw)
+    dispatch_token<KMAX, BWD>(t, lane, H, k, L, x, topk, gemm_row, poff, seg_off, peer_base, me, etp,
+                              part, dst_off, origin_off, dup_off, y_rows, gates, dgates);
 }
 
 // Receiver side of the deduplicated push, over the real rows of each group
@@ -434,19 +470,109 @@ int ep_dispatch(const void* x, int64_t Tn, int64_t H, int k, int L, const int32_
                 const int32_t* gemm_row, const int32_t* poff, const int32_t* seg_off,
                 const uint64_t* peer_base, int me, int etp, int64_t dst_off, int64_t origin_off,
                 int64_t dup_off, const void* y_rows, const float* gates, float* dgates, int bwd,
-                const int32_t* status, cudaStream_t st) {
-  const unsigned grid = (unsigned)ceil_div(Tn, 8);
+                int part, const int32_t* status, cudaStream_t st) {
+  if (part < 0 || part > 2) {
+    set_error("ep_dispatch: part=%d outside [0, 2]", part);
+    return B200MOE_EINVAL;
+  }
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* yb = static_cast<const __nv_bfloat16*>(y_rows);
-#define DF(KM) ep_dispatch_kernel<KM, false><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates, status)
-#define DB(KM) ep_dispatch_kernel<KM, true><<<grid, 256, 0, st>>>(xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, dst_off, origin_off, dup_off, yb, gates, dgates, status)
+  // part 2 runs beside the first GEMM: one small block per SM (see the kernel)
+  static const int n_sm = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const bool beside = part == 2;
+  // the side push must not hold an SM in a small-shared-memory carveout:
+  // the smem/L1 split only changes on an idle SM, so a push block resident
+  // first would keep the GEMM CTA (~214 KB of shared memory) off that SM
+  // until it drains.  Experiments: B200MOE_PUSH_CARVEOUT=0 skips this.
+  static const bool carve = [] {
+    const char* e = getenv("B200MOE_PUSH_CARVEOUT");
+    if (e && atoi(e) == 0) return false;
+    cudaFuncSetAttribute(ep_dispatch_kernel<1, false, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ep_dispatch_kernel<2, false, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ep_dispatch_kernel<4, false, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ep_dispatch_kernel<8, false, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ep_dispatch_kernel<1, true, 64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ep_dispatch_kernel<2, true, 64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ep_dispatch_kernel<4, true, 64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ep_dispatch_kernel<8, true, 64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)carve;
+  const int nt = beside ? (bwd ? 64 : 128) : 256;
+  // experiments: B200MOE_PUSH_BLOCKS_PER_SM = blocks of the side push per SM
+  static const int beside_blocks = [] {
+    const char* e = getenv("B200MOE_PUSH_BLOCKS_PER_SM");
+    const int v = e ? atoi(e) : 1;
+    return v >= 1 ? v : 1;
+  }();
+  const unsigned grid =
+      (unsigned)std::min<int64_t>(ceil_div(Tn, nt / 32), beside ? (int64_t)n_sm * beside_blocks : INT32_MAX);
+#define DARGS xb, Tn, H, k, L, topk, gemm_row, poff, seg_off, peer_base, me, etp, part, dst_off, origin_off, dup_off, yb, gates, dgates, status
+#define DF(KM)                                                                  \
+  if (beside) ep_dispatch_kernel<KM, false, 128><<<grid, 128, 0, st>>>(DARGS); \
+  else ep_dispatch_kernel<KM, false, 256><<<grid, 256, 0, st>>>(DARGS)
+#define DB(KM)                                                               \
+  if (beside) ep_dispatch_kernel<KM, true, 64><<<grid, 64, 0, st>>>(DARGS); \
+  else ep_dispatch_kernel<KM, true, 256><<<grid, 256, 0, st>>>(DARGS)
   if (Tn > 0) {
     if (bwd) { KSW(k, DB) }
     else { KSW(k, DF) }
   }
 #undef DF
 #undef DB
+#undef DARGS
   B200MOE_CHECK_LAUNCH("ep_dispatch");
+  return B200MOE_OK;
+}
+
+// GEMM groups of the split first GEMM (push overlapped with the GEMM): per
+// local expert le, its group [goff[le], goff[le+1]) of the receive buffer
+// splits into the rows this rank sent itself -- [s, s + c), s = seg_off[d*L
+// + le] for d = this rank's EP index, c its own count -- and the rest
+// (before and after them, pads included).  split (int32, 8L + 2):
+//   [0, L]            loc_off  (loc_off[L] = goff[L], the bound)
+//   [L+1, 2L+1)       loc_end
+//   [2L+1, 4L+2)      rem_off  (2 groups per expert; rem_off[2L] = goff[L])
+//   [4L+2, 6L+2)      rem_end
+//   [6L+2, 8L+2)      rem_exp  (= le)
+// An empty group (the layout failed, or no rows) is [goff[le], goff[le]).
+__global__ void ep_split_groups_kernel(const int32_t* __restrict__ cnt, int me, int ep, int etp, int L,
+                                       const int32_t* __restrict__ seg_off, const int32_t* __restrict__ goff,
+                                       const int32_t* __restrict__ gcount, int32_t* __restrict__ split) {
+  const int E = ep * L, d = me / etp;
+  int32_t* loc_off = split;
+  int32_t* loc_end = split + L + 1;
+  int32_t* rem_off = split + 2 * L + 1;
+  int32_t* rem_end = split + 4 * L + 2;
+  int32_t* rem_exp = split + 6 * L + 2;
+  for (int le = threadIdx.x; le <= L; le += blockDim.x) {
+    if (le == L) {
+      loc_off[L] = goff[L];
+      rem_off[2 * L] = goff[L];
+      continue;
+    }
+    const int32_t g0 = goff[le], g1 = goff[le + 1];
+    const bool live = gcount[le] > 0;
+    const int32_t s = live ? seg_off[d * L + le] : g0;
+    const int32_t c = live ? max(cnt[me * E + d * L + le], 0) : 0;
+    loc_off[le] = s;
+    loc_end[le] = s + c;
+    rem_off[2 * le] = g0;
+    rem_end[2 * le] = s;
+    rem_off[2 * le + 1] = s + c;
+    rem_end[2 * le + 1] = live ? g1 : s + c;
+    rem_exp[2 * le] = rem_exp[2 * le + 1] = le;
+  }
+}
+
+int ep_split_groups(const int32_t* cnt_local, int me, int ep, int etp, int L, const int32_t* seg_off,
+                    const int32_t* goff, const int32_t* gcount, int32_t* split, cudaStream_t st) {
+  ep_split_groups_kernel<<<1, 128, 0, st>>>(cnt_local, me, ep, etp, L, seg_off, goff, gcount, split);
+  B200MOE_CHECK_LAUNCH("ep_split_groups");
   return B200MOE_OK;
 }
 

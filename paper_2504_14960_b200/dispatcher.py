@@ -414,6 +414,13 @@ class RankLayer:
         self.use_peer = (want == "peer" and not self.single and 1 < len(groups.xch) <= 32
                          and dtype == torch.bfloat16 and self.k <= 8 and gemm_tc.available()
                          and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
+        # peer path, B200MOE_PUSH_OVERLAP=1: the NVLink part of each push runs
+        # on a side stream beside the first GEMM over the rank's own rows
+        # (bit-identical).  Off by default: measured, a concurrent push slows
+        # the tensor-core GEMM by about twice its own duration
+        # (tools/push_overlap_probe.py)
+        self.push_overlap = (self.use_peer and X.split_ok(self.pk, dtype)
+                             and os.environ.get("B200MOE_PUSH_OVERLAP", "0") == "1")
         # step status (see _status_slot): the router writes bit 0 into the
         # checked word only when inputs are validated
         self.status, self.status_host, self.scratch = _status_slot(device, rank, peer_tag)
@@ -786,16 +793,24 @@ class RankLayer:
         T = x.shape[0]
         px = self._peer(ctx, T)
         oversize = T > px.tokens
+        ov = self.push_overlap
         if oversize:
             # the block does not fit the peers' buffers: take part in the
             # step's protocol without tokens and fail it everywhere (status)
             self.status.bitwise_or_(ST_OVERSIZE)
-            st = px.forward_dispatch(x[:0], dec.experts[:0], plan, ALIGN, status=self.status)
+            st = px.forward_dispatch(x[:0], dec.experts[:0], plan, ALIGN, status=self.status, overlap=ov)
         else:
-            st = px.forward_dispatch(x, dec.experts, plan, ALIGN, status=self.status)
+            st = px.forward_dispatch(x, dec.experts, plan, ALIGN, status=self.status, overlap=ov)
         self._mark_status()
-        pre, h, _ = X.ffn_forward(px.region("xr"), st["goff"], self.L, None, self.pk, px.cap,
-                                  y_scatter=px.scatter("yret"))
+        if ov:
+            # the NVLink push runs on the exchange stream beside GEMM1 over
+            # this rank's own rows; GEMM1 over the received rows follows the
+            # landing barrier (pre / h identical to one launch)
+            pre, h = X.ffn_forward_split(px.region("xr"), st["goff"], self.L, self.pk, px.cap, st["split"],
+                                         lambda: px.land(st), px.scatter("yret"))
+        else:
+            pre, h, _ = X.ffn_forward(px.region("xr"), st["goff"], self.L, None, self.pk, px.cap,
+                                      y_scatter=px.scatter("yret"))
         y_sh, sh_done = self._shared_forward_side(x, saved)
         px.barrier()  # every expert output row (ETP: every partial) is back in yret
         if sh_done is not None:
@@ -812,10 +827,13 @@ class RankLayer:
     def _backward_peer(self, ctx, u, sv, dec, plan):
         px, st = sv["peer"], sv["pst"]
         px.check_generation(st)
-        dgates = px.backward_dispatch(u, dec.experts, plan, dec.gates, st, sv["y"], ALIGN, status=self.status)
+        ov = self.push_overlap and "split" in st
+        dgates = px.backward_dispatch(u, dec.experts, plan, dec.gates, st, sv["y"], ALIGN, status=self.status,
+                                      overlap=ov)
         _, dw1p, dw2p = X.ffn_backward(px.region("dyr"), px.region("xr"), sv["pre"], sv["h"],
                                        st["goff"], self.L, None, self.pk, px.cap,
-                                       dx_scatter=px.scatter("dxret"))
+                                       dx_scatter=px.scatter("dxret"),
+                                       split=st["split"] if ov else None, land=lambda: px.land(st))
         sv["shared_side"] = self._shared_backward_side(u, sv)
         px.barrier()  # every input-gradient row (ETP: every partial) is back in dxret
         return px.returned("dxret"), dgates, dw1p, dw2p

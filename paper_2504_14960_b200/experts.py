@@ -258,15 +258,48 @@ def ffn_forward(xp: torch.Tensor, goff: torch.Tensor, G: int, gexp: Optional[tor
     return pre, h, y
 
 
+def ffn_forward_split(xp: torch.Tensor, goff: torch.Tensor, G: int, pk: PackedExperts, max_rows: int,
+                      split, land, y_scatter):
+    """ffn_forward with the first GEMM in two launches over the groups of
+    ``split`` (kernels.ep_split_groups): the rows already in place (this
+    rank's own), then -- after ``land()`` makes the stream wait for the rest
+    of the exchange -- the received ones.  Rows are independent in GEMM1, so
+    pre / h are bit-identical to one launch; GEMM2 (scatter epilogue) runs
+    over the whole groups.  bf16 tensor-core path only."""
+    from . import gemm_tc
+
+    R = xp.shape[0]
+    loc_off, loc_end, rem_off, rem_end, rem_exp = split
+    h = torch.empty((R, pk.ffn), dtype=xp.dtype, device=xp.device)
+    pre = torch.empty((R, pk.n1), dtype=xp.dtype, device=xp.device)
+    gemm_tc.ffn1_fused(xp, pk, pre, h, loc_off, G, None, max_rows, loc_end)
+    land()
+    gemm_tc.ffn1_fused(xp, pk, pre, h, rem_off, 2 * G, rem_exp, max_rows, rem_end)
+    H, F = pk.hidden, pk.ffn
+    gemm_tc.gemm(h, pk.w2p, None, grouped_dim=0, G=G, M=0, N=H, K=F, a_sm=F, a_sk=1, b_sg=H * F,
+                 b_sk=1, b_sn=F, c_sg=0, ldc=H, group_off=goff, max_rows=max_rows, scatter=y_scatter)
+    return pre, h
+
+
+def split_ok(pk: PackedExperts, dtype) -> bool:
+    """Whether the split first GEMMs (ffn_forward_split / ffn_backward's
+    ``split``) apply: the fused bf16 tensor-core epilogues."""
+    from . import gemm_tc
+
+    return dtype == torch.bfloat16 and gemm_tc.available() and gemm_tc.fused_act_ok(pk)
+
+
 def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torch.Tensor,
                  goff: torch.Tensor, G: int, gexp: Optional[torch.Tensor], pk: PackedExperts,
                  max_rows: int, want_dx: bool = True, gend: Optional[torch.Tensor] = None,
-                 dx_scatter=None):
+                 dx_scatter=None, split=None, land=None):
     """experts.py:146-172 batched over groups: returns (dxp, dw1p, dw2p) with
     dw*p [G, ...] fp32 per GROUP (callers sum groups sharing an expert);
     dw1p[g] is [N1, H] with SwiGLU rows in [gate | up] order, so dw1p[g].T is
     the reference layout.
-    ``dx_scatter``: as ffn_forward's y_scatter, for the input gradient."""
+    ``dx_scatter``: as ffn_forward's y_scatter, for the input gradient.
+    ``split`` / ``land``: as ffn_forward_split, for the first backward GEMM
+    (the fused activation-derivative dgrad; requires split_ok)."""
     from . import gemm_tc
 
     R = dyp.shape[0]
@@ -275,7 +308,12 @@ def ffn_backward(dyp: torch.Tensor, xp: torch.Tensor, pre: torch.Tensor, h: torc
     dt = dyp.dtype
     dev = dyp.device
     dpre = torch.empty((R, N1), dtype=dt, device=dev)
-    if dt == torch.bfloat16 and gemm_tc.available() and gemm_tc.fused_act_ok(pk):
+    if split is not None:
+        loc_off, loc_end, rem_off, rem_end, rem_exp = split
+        gemm_tc.dgrad2_fused(dyp, pk, pre, dpre, loc_off, G, None, max_rows, loc_end)
+        land()
+        gemm_tc.dgrad2_fused(dyp, pk, pre, dpre, rem_off, 2 * G, rem_exp, max_rows, rem_end)
+    elif dt == torch.bfloat16 and gemm_tc.available() and gemm_tc.fused_act_ok(pk):
         gemm_tc.dgrad2_fused(dyp, pk, pre, dpre, goff, G, gexp, max_rows, gend)
     else:
         dh = torch.empty((R, F), dtype=dt, device=dev)

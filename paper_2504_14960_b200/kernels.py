@@ -403,20 +403,42 @@ def ep_zero_pads(buf: torch.Tensor, goff, gcount, G: int, align: int, origin=Non
 
 def ep_dispatch(x: torch.Tensor, topk_idx, gemm_row, poffsets, seg_off, L_: int, peer_base, me: int,
                 etp: int, dst_off: int, origin_off: int = 0, bwd: bool = False, y_rows=None,
-                gates=None, dup_off: int = -1, status=None):
+                gates=None, dup_off: int = -1, status=None, part: int = 0, dgates=None):
     """Forward: push x rows to the owners' receive buffers and record their
     origin.  Backward: push gates*u rows; returns dgates [T, k] fp32 = <u, y>
     with y the returned expert outputs (``y_rows``, local padded layout).
     ``dup_off >= 0``: one push per (token, EP index), duplicates recorded in
-    the receivers' dup tables (resolved by ``ep_expand``)."""
+    the receivers' dup tables (resolved by ``ep_expand``).
+    ``part`` 1 / 2: only the stores into this rank's own / the other members'
+    buffers (b200moe_ep_dispatch_part); the two parts of a backward share one
+    ``dgates`` tensor (each writes its own pairs)."""
     T, H = x.shape
     k = topk_idx.shape[1]
     _cuda(x, "x", torch.bfloat16)
-    dg = torch.empty((T, k), dtype=torch.float32, device=x.device) if bwd else None
-    L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
-           L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, etp, dst_off, origin_off, dup_off,
-           L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), L.ptr(status), _sp())
+    dg = dgates
+    if bwd and dg is None:
+        dg = torch.empty((T, k), dtype=torch.float32, device=x.device)
+    if part == 0:
+        L.call("b200moe_ep_dispatch", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
+               L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, etp, dst_off, origin_off, dup_off,
+               L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), L.ptr(status), _sp())
+    else:
+        L.call("b200moe_ep_dispatch_part", L.ptr(x), T, H, k, L_, L.ptr(topk_idx), L.ptr(gemm_row),
+               L.ptr(poffsets), L.ptr(seg_off), L.ptr(peer_base), me, etp, dst_off, origin_off, dup_off,
+               L.ptr(y_rows), L.ptr(gates), L.ptr(dg), int(bwd), int(part), L.ptr(status), _sp(),
+               tag="ep_dispatch" if part == 2 else "ep_dispatch_local")
     return dg
+
+
+def ep_split_groups(cnt: torch.Tensor, me: int, ep: int, etp: int, L_: int, seg_off, goff, gcount):
+    """-> (loc_off [L+1], loc_end [L], rem_off [2L+1], rem_end [2L], rem_exp [2L]) int32 views: the
+    groups of the first GEMM split into the rows this rank sent itself and the rest."""
+    split = torch.empty((8 * L_ + 2,), dtype=torch.int32, device=cnt.device)
+    L.call("b200moe_ep_split_groups", L.ptr(cnt), me, ep, etp, L_, L.ptr(seg_off), L.ptr(goff),
+           L.ptr(gcount), L.ptr(split), _sp())
+    n = L_
+    return (split[:n + 1], split[n + 1:2 * n + 1], split[2 * n + 1:4 * n + 2], split[4 * n + 2:6 * n + 2],
+            split[6 * n + 2:8 * n + 2])
 
 
 def ep_expand(buf: torch.Tensor, goff, gcount, G: int, dup: torch.Tensor, phase: int):

@@ -194,40 +194,98 @@ class PeerExchange:
             self.ctx.meta(self.group, None)
 
     # ------------------------------------------------------------ steps
-    def forward_dispatch(self, x, topk_idx, plan, align: int, status=None):
+    def forward_dispatch(self, x, topk_idx, plan, align: int, status=None, overlap: bool = False):
         """counts push -> barrier -> layout -> pads -> dispatch -> barrier.
         Returns the routing state the rest of the step needs.  ``status``
         (device int32[1]): a rank whose step already failed pushes an abort
         marker instead of its counts, every member then skips the pushes and
-        flags the step (bit 1), so all of them finish the barriers and raise."""
+        flags the step (bit 1), so all of them finish the barriers and raise.
+
+        ``overlap``: the push is split (b200moe_ep_dispatch_part): the rows
+        this rank routes to itself are stored on the compute stream, the
+        NVLink part runs on the exchange stream beside the caller's first
+        GEMM over those own rows (``st["split"]``: the GEMM groups of both
+        halves); the caller then calls :meth:`land` before the GEMM over the
+        received rows."""
         K.ep_counts_push(plan.counts, self.me, self.members, self.peer_base, self.cnt_off, status=status)
         self.barrier()
         seg_off, goff, gcount = K.ep_layout(self.counts(), self.me, self.ep, self.etp, self.L, align,
                                             self.cap, status=status)
         K.ep_zero_pads(self.region("xr"), goff, gcount, self.L, align, origin=self.origin())
         dup_off = self.off["dup"] if self.dedup else -1
-        K.ep_dispatch(x, topk_idx, plan.gemm_row, plan.poffsets, seg_off, self.L, self.peer_base,
-                      self.me, self.etp, self.off["xr"], self.off["origin"], dup_off=dup_off,
-                      status=status)
-        self.barrier()
-        if self.dedup:
-            K.ep_expand(self.region("xr"), goff, gcount, self.L, self.dup(), 0)
+        args = (x, topk_idx, plan.gemm_row, plan.poffsets, seg_off, self.L, self.peer_base, self.me,
+                self.etp, self.off["xr"], self.off["origin"])
+        st = dict(seg_off=seg_off, goff=goff, gcount=gcount)
+        if overlap:
+            st["split"] = K.ep_split_groups(self.counts(), self.me, self.ep, self.etp, self.L, seg_off,
+                                            goff, gcount)
+            K.ep_dispatch(*args, dup_off=dup_off, status=status, part=1)
+            self._on_side(lambda: K.ep_dispatch(*args, dup_off=dup_off, status=status, part=2))
+            st["pending"] = ("fwd",)
+        else:
+            K.ep_dispatch(*args, dup_off=dup_off, status=status)
+            self.barrier()
+            if self.dedup:
+                K.ep_expand(self.region("xr"), goff, gcount, self.L, self.dup(), 0)
         self.generation += 1
-        return dict(seg_off=seg_off, goff=goff, gcount=gcount, generation=self.generation)
+        st["generation"] = self.generation
+        return st
 
-    def backward_dispatch(self, u, topk_idx, plan, gates, st, y_rows, align: int, status=None):
+    def backward_dispatch(self, u, topk_idx, plan, gates, st, y_rows, align: int, status=None,
+                          overlap: bool = False):
         """pads -> push g*u rows (dgates from the returned y) -> barrier.
-        Nothing is pushed when the forward's ``status`` flagged the step."""
+        Nothing is pushed when the forward's ``status`` flagged the step.
+        ``overlap``: as forward_dispatch (the caller runs the first backward
+        GEMM over its own rows, then :meth:`land`)."""
         K.ep_zero_pads(self.region("dyr"), st["goff"], st["gcount"], self.L, align)
-        dg = K.ep_dispatch(u, topk_idx, plan.gemm_row, plan.poffsets, st["seg_off"], self.L,
-                           self.peer_base, self.me, self.etp, self.off["dyr"], bwd=True,
-                           y_rows=y_rows, gates=gates, dup_off=self.off["dup"] if self.dedup else -1,
-                           status=status)
+        dup_off = self.off["dup"] if self.dedup else -1
+        args = (u, topk_idx, plan.gemm_row, plan.poffsets, st["seg_off"], self.L, self.peer_base, self.me,
+                self.etp, self.off["dyr"])
+        kw = dict(bwd=True, y_rows=y_rows, gates=gates, dup_off=dup_off, status=status)
+        if overlap:
+            dg = K.ep_dispatch(*args, part=1, **kw)
+            self._on_side(lambda: K.ep_dispatch(*args, part=2, dgates=dg, **kw))
+            st["pending"] = ("bwd",)
+            return dg
+        dg = K.ep_dispatch(*args, **kw)
         self.barrier()
         if self.dedup:
             K.ep_expand(self.region("dyr"), st["goff"], st["gcount"], self.L, self.dup(), 1)
             K.ep_expand(self.region("dyr"), st["goff"], st["gcount"], self.L, self.dup(), 2)
         return dg
+
+    # ------------------------------------------------------------ overlap
+    def _on_side(self, fn):
+        """Run ``fn``'s launches on the exchange stream after everything the
+        compute stream has queued so far."""
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "stream", None) is None:
+            self.stream = torch.cuda.Stream(device=self.device)
+        self.stream.wait_stream(main)
+        with torch.cuda.stream(self.stream):
+            fn()
+
+    def land(self, st):
+        """Finish an overlapped push: barrier (+ dedup expansion) on the
+        exchange stream; the compute stream then waits for it, so every
+        received row is in place for the next GEMM."""
+        kind = st.pop("pending", None)
+        if kind is None:
+            return
+        main = torch.cuda.current_stream(self.device)
+
+        def finish():
+            self.barrier()
+            if self.dedup:
+                if kind[0] == "fwd":
+                    K.ep_expand(self.region("xr"), st["goff"], st["gcount"], self.L, self.dup(), 0)
+                else:
+                    K.ep_expand(self.region("dyr"), st["goff"], st["gcount"], self.L, self.dup(), 1)
+                    K.ep_expand(self.region("dyr"), st["goff"], st["gcount"], self.L, self.dup(), 2)
+
+        with torch.cuda.stream(self.stream):
+            finish()
+        main.wait_stream(self.stream)
 
     def check_generation(self, st):
         if st["generation"] != self.generation:

@@ -223,3 +223,54 @@ def test_smaller_receive_buffers_and_clean_overflow():
             B.moe_backward(ups, c2)
             c2.check()
         _same(ref, _run(world, topo, params, weights, split, ups))
+
+
+@pytest.mark.parametrize("world,ep,etp,E,k,sizes,cf,dedup", CASES)
+@pytest.mark.parametrize("device_barrier", [False, True])
+def test_overlapped_push_bit_identical(world, ep, etp, E, k, sizes, cf, dedup, device_barrier, monkeypatch):
+    """The push split into its local stores and an NVLink part on the
+    exchange stream beside GEMM1 over the rank's own rows (the default) gives
+    exactly the results of the push completing before one GEMM1 launch."""
+    monkeypatch.setenv("B200MOE_PUSH_DEDUP", dedup)
+    H, F, seed = 128, 256, 11
+    topo = B.ParallelTopology(world_size=world, ep=ep, etp=etp, tp=etp)
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=cf)
+    weights = B.init_expert_weights(E, H, F, etp, seed, ep_size=ep, activation="swiglu")
+    blocks, ups = _blocks(sizes, H, seed)
+    got = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("B200MOE_PUSH_OVERLAP", flag)
+        w = B.LocalWorld(world, device_barrier=device_barrier)
+        got[flag] = _run(w, topo, params, weights, blocks, ups)
+        layer_px = got[flag][1].per_rank[0]["peer"]
+        assert ("split" in got[flag][1].per_rank[0]["pst"]) == (flag == "1")
+        assert layer_px.device_barrier == device_barrier
+        if flag == "1":  # a second step on the same buffers and streams
+            _same(got["0"], _run(w, topo, params, weights, blocks, ups))
+    _same(got["0"], got["1"])
+
+
+def test_overlapped_push_all_local_and_all_remote(monkeypatch):
+    """Edge split groups: every token of rank 0 routed to its own experts
+    (empty remote part of its push) and every token of rank 1 routed away
+    (empty local part), through the router, with the device barrier."""
+    H, F, E, k, seed = 128, 256, 8, 2, 4
+    topo = B.ParallelTopology(world_size=2, ep=2)
+    wg = np.zeros((H, E))
+    wg[0, :4] = 4.0   # feature 0 large -> experts 0..3 (rank 0)
+    wg[0, 4:] = -4.0  # feature 0 very negative -> experts 4..7 (rank 1)
+    wg[1:, :] = O.gating_matrix(H - 1, E, seed) * 0.01
+    params = B.GatingParams(w_g=wg, k=k)
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=2, activation="swiglu")
+    blocks, ups = _blocks((192, 160), H, seed)
+    blocks[0].values[:, 0] = 30.0   # rank 0's tokens -> rank 0's experts
+    blocks[1].values[:, 0] = 30.0   # rank 1's tokens -> rank 0's experts too
+    got = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("B200MOE_PUSH_OVERLAP", flag)
+        got[flag] = _run(B.LocalWorld(2, device_barrier=True), topo, params, weights, blocks, ups)
+    dec0 = got["1"][1].per_rank[0]["decision"]
+    assert bool((dec0.experts < 4).all())
+    dec1 = got["1"][1].per_rank[1]["decision"]
+    assert bool((dec1.experts < 4).all())
+    _same(got["0"], got["1"])
