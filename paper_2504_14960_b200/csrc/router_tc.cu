@@ -47,6 +47,8 @@ __host__ __device__ constexpr uint32_t idesc_n(int n) {
 struct Args {
   int64_t T;
   int E, k, gate_fn, renorm, nkb, stages;
+  int bm;    // tokens per CTA tile (multiple of 8, <= 128): the grid covers every SM
+  int ksub;  // 64-column K blocks per pipeline stage (stages = smem slots / ksub)
   float* logits;
   float* scores;
   int32_t* idx;
@@ -143,7 +145,10 @@ __global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant
   const uint32_t full_bar = bars, empty_bar = bars + 8 * S, done_bar = bars + 16 * S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE + 16 * S + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM;
+  const int64_t m0 = (int64_t)blockIdx.x * a.bm;
+  // the TMA box is bm rows (the rest of the 128-row A tile is never read
+  // back: the MMA's extra accumulator rows are ignored by the epilogue)
+  const uint32_t a_tx = (uint32_t)a.bm * BK * 2;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -171,18 +176,27 @@ __global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant
   // not stream the same 8 KB-strided column block of x at the same time (the
   // DRAM partitions stay evenly loaded); the fp32 sum order is fixed per CTA
   const int kb_rot = (int)((blockIdx.x * 7u) % (unsigned)a.nkb);
+  // a pipeline stage holds KS consecutive 64-column K blocks (KS smem slots,
+  // one barrier pair): each x row is then read as KS x 128 contiguous bytes
+  // per stage instead of 128 B -- DRAM page locality for the 8 KB-strided rows
+  const int KS = a.ksub, G = S / KS, nst = (a.nkb + KS - 1) / KS;
   if (warp == 0) {
     if (lane == 0) {
-      int stage = 0;
+      int g = 0;
       uint32_t phase = 0;
-      for (int i = 0; i < a.nkb; ++i) {
-        const int kb = i + kb_rot < a.nkb ? i + kb_rot : i + kb_rot - a.nkb;
-        mbar_wait(empty_bar + 8 * stage, phase ^ 1);
-        mbar_expect_tx(full_bar + 8 * stage, STAGE);
-        tma_load_3d(&map_x, sA + stage * A_BYTES, full_bar + 8 * stage, kb * BK, m0, 0);
-        tma_load_3d(&map_w, sB + stage * B_BYTES, full_bar + 8 * stage, kb * BK, 0, 0);
-        if (++stage == S) {
-          stage = 0;
+      for (int i = 0; i < nst; ++i) {
+        const int nsub = min(KS, a.nkb - i * KS);
+        mbar_wait(empty_bar + 8 * g, phase ^ 1);
+        mbar_expect_tx(full_bar + 8 * g, (uint32_t)nsub * (a_tx + B_BYTES));
+        for (int sub = 0; sub < nsub; ++sub) {
+          const int kk = i * KS + sub;
+          const int kb = kk + kb_rot < a.nkb ? kk + kb_rot : kk + kb_rot - a.nkb;
+          const int slot = g * KS + sub;
+          tma_load_3d(&map_x, sA + slot * A_BYTES, full_bar + 8 * g, kb * BK, (int)m0, 0);
+          tma_load_3d(&map_w, sB + slot * B_BYTES, full_bar + 8 * g, kb * BK, 0, 0);
+        }
+        if (++g == G) {
+          g = 0;
           phase ^= 1;
         }
       }
@@ -190,19 +204,23 @@ __global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_n(NP);
-      int stage = 0;
+      int g = 0;
       uint32_t phase = 0;
-      for (int i = 0; i < a.nkb; ++i) {
-        mbar_wait(full_bar + 8 * stage, phase);
+      for (int i = 0; i < nst; ++i) {
+        const int nsub = min(KS, a.nkb - i * KS);
+        mbar_wait(full_bar + 8 * g, phase);
         tc_fence_after();
-        const uint32_t a_s = sA + stage * A_BYTES, b_s = sB + stage * B_BYTES;
+        for (int sub = 0; sub < nsub; ++sub) {
+          const int slot = g * KS + sub;
+          const uint32_t a_s = sA + slot * A_BYTES, b_s = sB + slot * B_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          tc_mma(tmem, smem_desc(a_s + k * 32, 16, 1024), smem_desc(b_s + k * 32, 16, 1024), idesc,
-                 (i | k) != 0);
-        tc_commit(empty_bar + 8 * stage);
-        if (++stage == S) {
-          stage = 0;
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma(tmem, smem_desc(a_s + k * 32, 16, 1024), smem_desc(b_s + k * 32, 16, 1024), idesc,
+                   (i | sub | k) != 0);
+        }
+        tc_commit(empty_bar + 8 * g);
+        if (++g == G) {
+          g = 0;
           phase ^= 1;
         }
       }
@@ -227,8 +245,9 @@ __global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant
         else if (col < 3 * EP) lg[col % EP] += __uint_as_float(v[j]);
       }
     }
-    const int64_t t = (int64_t)m0 + 32 * q + lane;
-    if (t < a.T) epilogue_row<EP>(a, t, lg);
+    const int r = 32 * q + lane;
+    const int64_t t = m0 + r;
+    if (r < a.bm && t < a.T) epilogue_row<EP>(a, t, lg);
   }
   tc_fence_before();
   __syncthreads();
@@ -242,16 +261,35 @@ template <int EP>
 static int launch(const void* x, int64_t T, int64_t H, const void* w, Args a, cudaStream_t st) {
   constexpr int NP = np_of(EP);
   constexpr int STAGE = BM * BK * 2 + NP * BK * 2;
+  // tile height: the fewest rows (multiple of 8) that spread T over every SM
+  // in one wave (one CTA per SM: x is streamed once by all of them), e.g.
+  // T = 16384 -> 112-row tiles on 147 SMs instead of 128-row tiles on 128.
+  // B200MOE_ROUTER_BM overrides (experiments).
+  static const int bm_env = [] {
+    const char* e = getenv("B200MOE_ROUTER_BM");
+    return e ? atoi(e) : 0;
+  }();
+  int bm = (int)std::min<int64_t>(BM, std::max<int64_t>(8, ceil_div(ceil_div(T, num_sms()), 8) * 8));
+  if (bm_env >= 8 && bm_env <= BM && bm_env % 8 == 0) bm = bm_env;
+  a.bm = bm;
   CUtensorMap mx, mw;
-  int rc = make_map(&mx, x, (uint64_t)H, (uint64_t)T, 1, (uint64_t)H, (uint64_t)H * T, BM);
+  int rc = make_map(&mx, x, (uint64_t)H, (uint64_t)T, 1, (uint64_t)H, (uint64_t)H * T, (uint32_t)bm);
   if (rc) return rc;
   rc = make_map(&mw, w, (uint64_t)H, (uint64_t)NP, 1, (uint64_t)H, (uint64_t)H * NP, NP);
   if (rc) return rc;
   a.nkb = (int)ceil_div(H, BK);
-  a.stages = std::max(2, std::min(8, (196 * 1024) / STAGE));
+  a.stages = std::max(2, std::min(8, (196 * 1024) / STAGE));  // smem slots of one K block
+  static const int ks_env = [] {
+    const char* e = getenv("B200MOE_ROUTER_KSUB");
+    return e ? atoi(e) : 0;
+  }();
+  // measured neutral (C2: 30.1-31.2 us for ksub 1 / 2 / 4, 128- or 112-row
+  // tiles alike): the kernel's ~30 us is not DRAM-locality or SM-count bound
+  a.ksub = ks_env >= 1 ? std::min(ks_env, a.stages / 2) : 1;
+  a.stages = a.stages / a.ksub * a.ksub;
   const int smem = 1024 + a.stages * STAGE + 16 * a.stages + 64;
   if (int e = ensure_max_smem(router_tc_kernel<EP>, 232448, "router_fwd_tc")) return e;
-  router_tc_kernel<EP><<<(unsigned)ceil_div(T, BM), 256, smem, st>>>(mx, mw, a);
+  router_tc_kernel<EP><<<(unsigned)ceil_div(T, bm), 256, smem, st>>>(mx, mw, a);
   B200MOE_CHECK_LAUNCH("router_fwd_tc");
   if (EP > 32)
     return router_topk(a.logits, T, a.E, a.k, a.gate_fn, a.renorm, a.scores, a.idx, a.gates, a.gates64,
@@ -486,7 +524,7 @@ int router_fwd_tc(const void* x, int64_t T, int64_t H, const void* w_parts, int 
                   int renorm, float* logits, float* scores, int32_t* idx, float* gates, double* gates64,
                   int32_t* status, cudaStream_t st) {
   if (T == 0) return B200MOE_OK;
-  rtc::Args a{T, E, k, gate_fn, renorm, 0, 0, logits, scores, idx, gates, gates64, status};
+  rtc::Args a{T, E, k, gate_fn, renorm, 0, 0, rtc::BM, 1, logits, scores, idx, gates, gates64, status};
   if (E <= 8) return rtc::launch<8>(x, T, H, w_parts, a, st);
   if (E <= 16) return rtc::launch<16>(x, T, H, w_parts, a, st);
   if (E <= 32) return rtc::launch<32>(x, T, H, w_parts, a, st);
