@@ -62,6 +62,7 @@ struct Params {
   int64_t ldpre;
   int panel_m;     // raster panel height in m-tiles
   int tile_m;      // rows per tile: 128 (1 CTA) or 256 (CTA pair)
+  int debug_ops;      // energy experiments only: 1 = operand loads from one L2-hot block, 2 = none
   int debug_nostore;  // perf experiments only: 1 = no epilogue global traffic, 2 = no bulk
                       // stores, 3 = SwiGLU backward without its pre loads
   int use_tma;        // output tensor maps are valid (TMA-store epilogue)
@@ -582,8 +583,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       (void)w_empty;
       for (int t = cid; t < total; t += ncl) {
         const Tile tl = decode(p, prefix, t);
-        const int m0 = (int)tl.m0 + BM * (int)crank;
-        const int n0 = (int)tl.n0 + C::B_CTA * (int)crank;
+        const int m0 = (p.debug_ops == 1 ? 0 : (int)tl.m0) + BM * (int)crank;
+        const int n0 = (p.debug_ops == 1 ? 0 : (int)tl.n0) + C::B_CTA * (int)crank;
         for (int kb = 0; kb < tl.nkb; ++kb) {
           {
             WP_T0();
@@ -591,13 +592,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             WP_ADD(w_empty);
           }
           const uint32_t fb = full_bar + 8 * stage;
-          if (crank == 0) mbar_expect_tx(fb, C::STAGE * CG);
+          if (p.debug_ops == 2) {  // energy experiment: no operand loads at all
+            if (crank == 0) mbar_arrive(fb);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          // energy experiment 3: the pair's second CTA skips its A load (half
+          // of A's L2 reads, as a 2-pair multicast of A would give)
+          const bool skip_a = p.debug_ops == 3 && crank == 1;
+          if (crank == 0) mbar_expect_tx(fb, C::STAGE * CG - (p.debug_ops == 3 && CG == 2 ? C::A_BYTES : 0));
           const uint32_t fb_tma = CG == 2 ? (fb & PEER_BIT_MASK) : fb;
           const int kbr = kb + tl.krot < tl.nkb ? kb + tl.krot : kb + tl.krot - tl.nkb;
-          const int kc = (int)(tl.kbeg + (int64_t)kbr * BK);
+          // energy experiment 1: every load reads the first K block of the
+          // CTA's first tile rows (L2-resident, no DRAM traffic)
+          const int kc = p.debug_ops == 1 ? 0 : (int)(tl.kbeg + (int64_t)kbr * BK);
           const uint32_t a_dst = sA + stage * C::A_BYTES;
           const uint32_t b_dst = sB + stage * C::B_BYTES;
-          if (!A_MN) {
+          if (skip_a) {
+          } else if (!A_MN) {
             // A [rows, K] K-major: box {64 K, 128 rows}
             tma_load<CG>(&map_a, a_dst, fb_tma, kc, m0, 0);
           } else {
@@ -1179,6 +1194,8 @@ int gemm_tc(const b200moe_tc_gemm_args* a, cudaStream_t st) {
   const char* sh = getenv("B200MOE_STORE_HINT");
   p.store_hint = (sh && sh[0] == '0') ? 0 : 1;
   p.tile_m = BM * cg;
+  const char* dops = getenv("B200MOE_DEBUG_OPS");
+  p.debug_ops = (dops && dops[0] >= '1' && dops[0] <= '3') ? dops[0] - '0' : 0;
   const char* ns = getenv("B200MOE_DEBUG_NOSTORE");
   p.debug_nostore = (ns && ns[0] >= '1' && ns[0] <= '3') ? ns[0] - '0' : 0;
   p.panel_m = choose_panel(a, p.tile_m);
