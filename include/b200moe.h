@@ -209,6 +209,17 @@ B200MOE_API int b200moe_combine(const void* rows, int dtype, int64_t T, int64_t 
                     const int32_t* pair_row, const float* gates, const float* dz,
                     const float* w_gT, int E, void* out, int out_dtype, int accumulate,
                     void* stream);
+/* b200moe_combine (bf16) over ETP partial rows: rows r of the combine are
+ * bf16(sum over p = 0..nparts-1 ascending, fp32, of parts[p * part_stride +
+ * r * H ..]) -- the ETP reduce-scatter fold (dispatcher.py:349-361,
+ * collectives.py:386-388; b200moe_ep_reduce_parts) fused into the
+ * combine's row loads.  rows_out (nullable, [rows, H] bf16, forward only)
+ * receives every reduced pair row (the forward's saved y_perm,
+ * dispatcher.py:374).  With dz (backward): E <= 8, no gates. */
+B200MOE_API int b200moe_combine_parts(const void* parts, int nparts, int64_t part_stride, void* rows_out,
+                                      int64_t T, int64_t H, int k, const int32_t* pair_row,
+                                      const float* gates, const float* dz, const float* w_gT, int E,
+                                      void* out, int accumulate, void* stream);
 
 /* ------------------------------------------------------------ expert GEMM */
 

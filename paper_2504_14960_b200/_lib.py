@@ -81,6 +81,7 @@ _SIGS = {
     "b200moe_ep_dispatch_part": [P, I64, I64, I32, I32, P, P, P, P, P, I32, I32, I64, I64, I64, P, P, P, I32,
                                  I32, P, P],
     "b200moe_ep_split_groups": [P, I32, I32, I32, I32, P, P, P, P, P],
+    "b200moe_combine_parts": [P, I32, I64, P, I64, I64, I32, P, P, P, P, I32, P, I32, P],
     "b200moe_ep_expand": [P, I64, P, P, I32, P, I32, P],
 }
 _RESTYPES = {

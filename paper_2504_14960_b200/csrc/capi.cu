@@ -55,6 +55,8 @@ int ep_zero_pads(void*, int64_t, const int32_t*, const int32_t*, int, int, int32
 int ep_dispatch(const void*, int64_t, int64_t, int, int, const int32_t*, const int32_t*,
                 const int32_t*, const int32_t*, const uint64_t*, int, int, int64_t, int64_t, int64_t,
                 const void*, const float*, float*, int, int, const int32_t*, cudaStream_t);
+int combine_parts(const void*, int, int64_t, void*, int64_t, int64_t, int, const int32_t*, const float*,
+                  const float*, const float*, int, void*, int, cudaStream_t);
 int ep_split_groups(const int32_t*, int, int, int, int, const int32_t*, const int32_t*, const int32_t*,
                     int32_t*, cudaStream_t);
 int ep_expand(void*, int64_t, const int32_t*, const int32_t*, int, const void*, int, cudaStream_t);
@@ -286,6 +288,19 @@ int b200moe_combine(const void* rows, int dtype, int64_t T, int64_t H, int k,
   if (T > 0) REQUIRE(rows && pair_row && out, "combine: null pointer");
   return combine(rows, dtype, T, H, k, pair_row, gates, dz, w_gT, E, out, out_dtype, accumulate,
                  S(stream));
+}
+
+int b200moe_combine_parts(const void* parts, int nparts, int64_t part_stride, void* rows_out, int64_t T,
+                          int64_t H, int k, const int32_t* pair_row, const float* gates, const float* dz,
+                          const float* w_gT, int E, void* out, int accumulate, void* stream) {
+  REQUIRE(nparts >= 1 && nparts <= 32 && part_stride >= 0 && H % 8 == 0 && k >= 1 && k <= 8 && T >= 0,
+          "combine_parts: 1 <= nparts <= 32, H %% 8 == 0, 1 <= k <= 8 required");
+  REQUIRE(!dz || (w_gT && E >= 1 && E <= 8 && !gates), "combine_parts: dz needs w_gT, E <= 8 and no gates");
+  REQUIRE(!rows_out || !dz, "combine_parts: rows_out only without dz");
+  if (T > 0) REQUIRE(parts && pair_row && out, "combine_parts: null pointer");
+  if (T == 0) return B200MOE_OK;
+  return combine_parts(parts, nparts, part_stride, rows_out, T, H, k, pair_row, gates, dz, w_gT, E, out,
+                       accumulate, S(stream));
 }
 
 int b200moe_gemm_simt(const b200moe_gemm_args* a, void* stream) {

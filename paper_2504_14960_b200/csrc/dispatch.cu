@@ -130,6 +130,28 @@ __global__ void __launch_bounds__(256) permute_bwd_kernel(
 }
 
 // ------------------------------------------------------------------ combine
+// bf16(sum over p ascending of parts[p][r][h..h+8)) in fp32, part 0 already
+// loaded -- the ETP reduce-scatter fold (ep_peer.cu ep_reduce_parts) fused
+// into the combines' row loads
+template <typename T>
+__device__ __forceinline__ Vec16<T> reduce_parts_row(const T* __restrict__ rows, int32_t r, int64_t H,
+                                                     int64_t h, int nparts, int64_t pstride, Vec16<T> p0) {
+  static_assert(sizeof(T) == 2, "bf16 rows");
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = to_f32(p0.v[j]);
+  for (int p = 1; p < nparts; ++p) {
+    Vec16<T> q;
+    q.raw = ld_nc_v4(rows + p * pstride + (int64_t)r * H + h);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += to_f32(q.v[j]);
+  }
+  Vec16<T> o;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o.v[j] = from_f32<T>(acc[j]);
+  return o;
+}
+
 // TPW tokens per warp so the optional router term (dz[t] @ w_g^T, w_g^T given
 // as [E, H]) reuses each w_g^T chunk across the warp's tokens.
 template <typename Tin, typename Tout, int KMAX, int TPW>
@@ -309,7 +331,7 @@ template <int KMAX, int EP, int UT>
 __global__ void __launch_bounds__(256, 2) combine_router_kernel(
     const __nv_bfloat16* __restrict__ rows, int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_row,
     const float* __restrict__ dz, const float* __restrict__ wgT, int E, __nv_bfloat16* __restrict__ out,
-    int accumulate, int64_t chunk) {
+    int accumulate, int64_t chunk, int nparts, int64_t pstride) {
   const int64_t h0 = (int64_t)blockIdx.y * CR_COLS + threadIdx.x * 8;
   if (h0 >= H) return;
   float w[EP][8];
@@ -337,6 +359,18 @@ __global__ void __launch_bounds__(256, 2) combine_router_kernel(
         has[u][s] = r >= 0;
         if (r >= 0) v[u][s].raw = ld_nc_v4(rows + (int64_t)r * H + h0);
       }
+    if (nparts > 1) {
+      // ETP partial rows (one block per member, pstride apart): the row is
+      // bf16(sum over members ascending, fp32) -- ep_reduce_parts' value
+#pragma unroll
+      for (int u = 0; u < UT; ++u)
+#pragma unroll
+        for (int s = 0; s < KMAX; ++s) {
+          if (!has[u][s]) continue;
+          const int32_t r = __ldg(pair_row + (t + u) * k + s);
+          v[u][s] = reduce_parts_row(rows, r, H, h0, nparts, pstride, v[u][s]);
+        }
+    }
 #pragma unroll
     for (int u = 0; u < UT; ++u) {
       if (t + u >= te) break;
@@ -376,7 +410,8 @@ __global__ void __launch_bounds__(256, 2) combine_router_kernel(
 template <typename Tin, typename Tout, int KMAX, int UNR>
 __global__ void __launch_bounds__(256) combine_gather_kernel(
     const Tin* __restrict__ rows, int64_t Tn, int64_t H, int k, const int32_t* __restrict__ pair_row,
-    const float* __restrict__ gates, Tout* __restrict__ out, int accumulate) {
+    const float* __restrict__ gates, Tout* __restrict__ out, int accumulate, int nparts, int64_t pstride,
+    Tin* __restrict__ rows_out) {
   static_assert(sizeof(Tin) == 2, "bf16 rows");
   constexpr int V = 8;
   const int lane = threadIdx.x & 31;
@@ -397,6 +432,18 @@ __global__ void __launch_bounds__(256) combine_gather_kernel(
 #pragma unroll
       for (int s = 0; s < KMAX; ++s)
         if (r[s] >= 0 && h < H) v[u][s].raw = ld_nc_v4(rows + (int64_t)r[s] * H + h);
+    }
+    if (nparts > 1) {  // ETP partial rows: reduce (ep_reduce_parts' value), keep the row for later
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t h = h0 + (int64_t)u * 32 * V;
+#pragma unroll
+        for (int s = 0; s < KMAX; ++s)
+          if (r[s] >= 0 && h < H) {
+            v[u][s] = reduce_parts_row(rows, r[s], H, h, nparts, pstride, v[u][s]);
+            if (rows_out) st_v4(rows_out + (int64_t)r[s] * H + h, v[u][s].raw);
+          }
+      }
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -515,7 +562,8 @@ int permute_bwd(const void* u, int dt, int64_t Tn, int64_t H, int k, const int32
 template <typename Tin, typename Tout>
 static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const int32_t* pr,
                           const float* gates, const float* dz, const float* wgT, int E, Tout* out,
-                          int acc, cudaStream_t st) {
+                          int acc, cudaStream_t st, int nparts = 1, int64_t pstride = 0,
+                          Tin* rows_out = nullptr) {
   constexpr int TPW = 4;
   const unsigned grid = (unsigned)ceil_div(ceil_div(Tn, TPW), 8);
   bool done = false;
@@ -526,8 +574,8 @@ static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const i
       dim3 g2((unsigned)ceil_div(Tn, chunk), (unsigned)ceil_div(H, CR_COLS));
       auto* ob = reinterpret_cast<__nv_bfloat16*>(out);
       auto* rb = reinterpret_cast<const __nv_bfloat16*>(rows);
-#define CR(KM) if (E <= 4) combine_router_kernel<KM, 4, 2><<<g2, 256, 0, st>>>(rb, Tn, H, k, pr, dz, wgT, E, ob, acc, chunk); \
-               else combine_router_kernel<KM, 8, 2><<<g2, 256, 0, st>>>(rb, Tn, H, k, pr, dz, wgT, E, ob, acc, chunk)
+#define CR(KM) if (E <= 4) combine_router_kernel<KM, 4, 2><<<g2, 256, 0, st>>>(rb, Tn, H, k, pr, dz, wgT, E, ob, acc, chunk, nparts, pstride); \
+               else combine_router_kernel<KM, 8, 2><<<g2, 256, 0, st>>>(rb, Tn, H, k, pr, dz, wgT, E, ob, acc, chunk, nparts, pstride)
       KDISPATCH(k, CR)
 #undef CR
       done = true;
@@ -536,11 +584,15 @@ static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const i
   if constexpr (sizeof(Tin) == 2) {
     if (!done && !dz && H % 8 == 0) {
       const unsigned g1 = (unsigned)ceil_div(Tn, 8);
-#define CG1(KM) combine_gather_kernel<Tin, Tout, KM, (KM <= 2 ? 4 : (KM <= 4 ? 2 : 1))><<<g1, 256, 0, st>>>(rows, Tn, H, k, pr, gates, out, acc)
+#define CG1(KM) combine_gather_kernel<Tin, Tout, KM, (KM <= 2 ? 4 : (KM <= 4 ? 2 : 1))><<<g1, 256, 0, st>>>(rows, Tn, H, k, pr, gates, out, acc, nparts, pstride, rows_out)
       if (Tn > 0) { KDISPATCH(k, CG1) }
 #undef CG1
       done = true;
     }
+  }
+  if (!done && nparts > 1) {
+    set_error("combine: ETP partial rows need bf16 rows, H %% 8 == 0 and (with dz) E <= 8, k <= 8");
+    return B200MOE_EUNSUPPORTED;
   }
   if (done) {
   } else if (H % 8 == 0) {
@@ -554,6 +606,14 @@ static int launch_combine(const Tin* rows, int64_t Tn, int64_t H, int k, const i
   }
   B200MOE_CHECK_LAUNCH("combine");
   return B200MOE_OK;
+}
+
+int combine_parts(const void* rows, int nparts, int64_t pstride, void* rows_out, int64_t Tn, int64_t H, int k,
+                  const int32_t* pr, const float* gates, const float* dz, const float* wgT, int E, void* out,
+                  int acc, cudaStream_t st) {
+  return launch_combine(static_cast<const __nv_bfloat16*>(rows), Tn, H, k, pr, gates, dz, wgT, E,
+                        static_cast<__nv_bfloat16*>(out), acc, st, nparts, pstride,
+                        static_cast<__nv_bfloat16*>(rows_out));
 }
 
 int combine(const void* rows, int dt, int64_t Tn, int64_t H, int k, const int32_t* pr,

@@ -261,15 +261,18 @@ template <int EP>
 static int launch(const void* x, int64_t T, int64_t H, const void* w, Args a, cudaStream_t st) {
   constexpr int NP = np_of(EP);
   constexpr int STAGE = BM * BK * 2 + NP * BK * 2;
-  // tile height: the fewest rows (multiple of 8) that spread T over every SM
-  // in one wave (one CTA per SM: x is streamed once by all of them), e.g.
-  // T = 16384 -> 112-row tiles on 147 SMs instead of 128-row tiles on 128.
-  // B200MOE_ROUTER_BM overrides (experiments).
+  // tile height 128.  Experiments: B200MOE_ROUTER_BM=n (multiple of 8), or
+  // 0 = the fewest rows that spread T over every SM in one wave (112 at
+  // T = 16384: measured no faster, and a T-dependent tiling would make a
+  // token's K-walk rotation -- hence its fp32 logit -- depend on how the
+  // tokens are split over ranks; with 128-row tiles and 64 K blocks it does
+  // not: tests/test_gpu_fullsize.py, EP1 == EP2 bit for bit)
   static const int bm_env = [] {
     const char* e = getenv("B200MOE_ROUTER_BM");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : -1;
   }();
-  int bm = (int)std::min<int64_t>(BM, std::max<int64_t>(8, ceil_div(ceil_div(T, num_sms()), 8) * 8));
+  int bm = BM;
+  if (bm_env == 0) bm = (int)std::min<int64_t>(BM, std::max<int64_t>(8, ceil_div(ceil_div(T, num_sms()), 8) * 8));
   if (bm_env >= 8 && bm_env <= BM && bm_env % 8 == 0) bm = bm_env;
   a.bm = bm;
   CUtensorMap mx, mw;

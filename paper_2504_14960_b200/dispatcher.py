@@ -819,8 +819,15 @@ class RankLayer:
             out = torch.zeros_like(x)
             saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row, y=None)
             return out, saved
-        y = px.returned("yret")
-        out = K.combine(y, plan.gemm_row, T, gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
+        if px.etp == 1:
+            y = px.region("yret")[0]
+            out = K.combine(y, plan.gemm_row, T, gates=dec.gates, out=y_sh, accumulate=y_sh is not None)
+        else:
+            # ETP: the members' partial rows are folded inside the combine,
+            # which also keeps the reduced rows (y_perm) for the backward
+            y = torch.empty((px.ret_rows, px.H), dtype=x.dtype, device=x.device)
+            out = K.combine(px.region("yret"), plan.gemm_row, T, gates=dec.gates, out=y_sh,
+                            accumulate=y_sh is not None, rows_out=y)
         saved.update(peer=px, pst=st, pre=pre, h=h, pair_row=plan.gemm_row, y=y)
         return out, saved
 
@@ -836,7 +843,9 @@ class RankLayer:
                                        split=st["split"] if ov else None, land=lambda: px.land(st))
         sv["shared_side"] = self._shared_backward_side(u, sv)
         px.barrier()  # every input-gradient row (ETP: every partial) is back in dxret
-        return px.returned("dxret"), dgates, dw1p, dw2p
+        # ETP: the partial rows [etp, rows, H] are folded by the combine
+        rows = px.region("dxret")[0] if px.etp == 1 else px.region("dxret")
+        return rows, dgates, dw1p, dw2p
 
     def _forward_exchange(self, ctx, x, dec, plan, saved):
         T, H = x.shape

@@ -274,7 +274,28 @@ def permute_bwd(u: torch.Tensor, pair_row: torch.Tensor, gates: torch.Tensor,
 
 
 def combine(rows: torch.Tensor, pair_row: torch.Tensor, T: int, gates=None, dz=None, w_gT=None,
-            out: Optional[torch.Tensor] = None, out_dtype=None, accumulate: bool = False):
+            out: Optional[torch.Tensor] = None, out_dtype=None, accumulate: bool = False,
+            rows_out: Optional[torch.Tensor] = None):
+    """``rows`` [R, H], or [P, R, H] ETP partial rows (summed in fp32 in
+    member order inside the combine, b200moe_combine_parts; ``rows_out``
+    then receives the reduced pair rows)."""
+    if rows.dim() == 3:
+        P_, R, H = rows.shape
+        k = pair_row.shape[1]
+        fused = (rows.dtype == torch.bfloat16 and H % 8 == 0 and k <= 8 and (dz is None or dz.shape[1] <= 8)
+                 and (out is None or out.dtype == torch.bfloat16) and out_dtype in (None, torch.bfloat16))
+        if not fused:
+            red = ep_reduce_parts(rows)
+            if rows_out is not None:
+                rows_out.copy_(red)
+            return combine(red, pair_row, T, gates=gates, dz=dz, w_gT=w_gT, out=out, out_dtype=out_dtype,
+                           accumulate=accumulate)
+        if out is None:
+            out = torch.empty((T, H), dtype=rows.dtype, device=rows.device)
+        E = 0 if dz is None else dz.shape[1]
+        L.call("b200moe_combine_parts", L.ptr(rows), P_, R * H, L.ptr(rows_out), T, H, k, L.ptr(pair_row),
+               L.ptr(gates), L.ptr(dz), L.ptr(w_gT), E, L.ptr(out), int(accumulate), _sp())
+        return out
     H = rows.shape[1]
     k = pair_row.shape[1]
     if out is None:

@@ -286,3 +286,33 @@ def test_deduplicated_push_is_exact(world, ep, etp, E, k, monkeypatch):
         for a, b in zip(r0.expert_grads[key][0] + r0.expert_grads[key][1],
                         r1.expert_grads[key][0] + r1.expert_grads[key][1]):
             torch.testing.assert_close(b, a, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("nparts,k,E,H,dz,acc", [(2, 2, 8, 4096, False, False), (2, 2, 8, 4096, True, False),
+                                                 (3, 4, 8, 256, True, True), (2, 8, 64, 512, False, True),
+                                                 (4, 1, 4, 136, True, False)])
+def test_combine_parts_equals_reduce_then_combine(nparts, k, E, H, dz, acc):
+    """ETP partial rows folded inside the combine (b200moe_combine_parts) give
+    exactly ep_reduce_parts followed by the plain combine; the forward's
+    materialised rows equal the reduced rows."""
+    from paper_2504_14960_b200 import kernels as K
+
+    g = torch.Generator(device="cuda").manual_seed(nparts * 100 + k)
+    T, R = 300, 300 * k + 40
+    parts = torch.randn((nparts, R, H), generator=g, device="cuda").to(torch.bfloat16)
+    pair_row = torch.randperm(R, generator=g, device="cuda")[:T * k].to(torch.int32).reshape(T, k).contiguous()
+    pair_row[5, 0] = -1  # a dropped pair
+    gates = None if dz else torch.rand((T, k), generator=g, device="cuda")
+    dzt = torch.randn((T, E), generator=g, device="cuda") if dz else None
+    wgT = torch.randn((E, H), generator=g, device="cuda") * 0.05 if dz else None
+    base = torch.randn((T, H), generator=g, device="cuda").to(torch.bfloat16)
+    red = K.ep_reduce_parts(parts)
+    want = K.combine(red, pair_row, T, gates=gates, dz=dzt, w_gT=wgT, out=base.clone() if acc else None,
+                     accumulate=acc)
+    rows_out = None if dz else torch.zeros((R, H), dtype=torch.bfloat16, device="cuda")
+    got = K.combine(parts, pair_row, T, gates=gates, dz=dzt, w_gT=wgT, out=base.clone() if acc else None,
+                    accumulate=acc, rows_out=rows_out)
+    torch.testing.assert_close(got, want, rtol=0, atol=0)
+    if rows_out is not None:
+        used = pair_row[pair_row >= 0].long()
+        torch.testing.assert_close(rows_out[used], red[used], rtol=0, atol=0)
