@@ -468,17 +468,33 @@ def main():
             res = B.moe_backward(ups, fctx)
             stager.download(res.input_grads[rank], dxh)  # overlaps the next forward
 
+        def fresh_cache():
+            # each leg starts from an empty caching allocator: blocks cached by
+            # the other leg's tensor lifetimes (copy streams, per-call layers)
+            # otherwise fragment the cache and the next leg's steps pay
+            # cudaFree/cudaMalloc device syncs (C4 at 1 GPU: ~9 ms per step)
+            barrier()
+            torch.cuda.empty_cache()
+
         def run_e2e(n):
             """n pipelined API steps after one untimed one; ms for the n."""
+            fresh_cache()
             e2e_step(0, True)
             stager.drain()
             barrier()
+            m0 = torch.cuda.memory_stats()
             t0 = time.perf_counter()
             for i in range(n):
                 e2e_step(i, i == n - 1)
             stager.drain()  # every step's copies complete inside the timed region
             barrier()
-            return (time.perf_counter() - t0) * 1e3
+            t1 = time.perf_counter()
+            if os.environ.get("B200MOE_BENCH_DEBUG") == "1":
+                m1 = torch.cuda.memory_stats()
+                print("e2e allocator:", {key: m1.get(key, 0) - m0.get(key, 0) for key in
+                                         ("num_device_alloc", "num_device_free", "num_alloc_retries",
+                                          "num_sync_all_streams")}, file=sys.stderr, flush=True)
+            return (t1 - t0) * 1e3
 
         for i in range(2):
             e2e_step(i, i == 1)
@@ -497,7 +513,9 @@ def main():
     halves = [a.steps // 2, a.steps - a.steps // 2] if run_e2e is not None else [a.steps]
     t_wall0 = time.time()
     for hi, n_half in enumerate(halves):
-        if hi:
+        if hi or run_e2e is not None:
+            if run_e2e is not None:
+                fresh_cache()
             step()  # untimed: the resident-input path's buffers back in the allocator's cache
             barrier()
         _lib.reset_launch_count()
