@@ -104,6 +104,10 @@ def main():
         return b
 
     def api(i, last):
+        if os.environ.get("ALLOC_STATS") == "1" and rank == 0:
+            st_ = torch.cuda.memory_stats()
+            print("alloc", {k_: st_.get(k_, 0) for k_ in ("num_device_alloc", "num_device_free",
+                                                          "num_alloc_retries")}, flush=True)
         outs, fctx = B.moe_forward(blocks_of(x), wmap, topo, params, nw, dtype=torch.bfloat16,
                                    check_finite_inputs=False)
         B.moe_backward(ups_of(u), fctx)
@@ -147,24 +151,33 @@ def main():
                      ("api+copies pipelined", api_pipelined)):
         if name.split()[-1] not in which:
             continue
-        if os.environ.get("GAPS") == "1" and world == 1:
+        if os.environ.get("GAPS") == "1":
+            # every rank runs the profiled steps (collectives); rank 0 reports
+            import contextlib
+
             from torch.profiler import ProfilerActivity, profile
 
             for i in range(2):
                 fn(i, False)
-            torch.cuda.synchronize()
-            with profile(activities=[ProfilerActivity.CUDA]) as prof:
-                for i in range(2):
-                    fn(i, i == 1)
+            sync()
+            cm = profile(activities=[ProfilerActivity.CUDA]) if rank == 0 else contextlib.nullcontext()
+            with cm as prof:
+                for i in range(3):
+                    fn(i, i == 2)
                 if hasattr(fn, "drain"):
                     fn.drain()
                 torch.cuda.synchronize()
+            if rank != 0:
+                ms, host = timed(fn)
+                continue
             ev = sorted((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
                         if e.device_type.name == "CUDA")
-            gaps, end = [], None
+            gaps, end, prev = [], None, ""
             for s_, e_, n_ in ev:
                 if end is not None and s_ - end > 50:
-                    gaps.append((s_ - end, n_[:60]))
+                    gaps.append((s_ - end, n_[:60] + "  (after " + prev[:40] + ")"))
+                if end is None or e_ >= end:
+                    prev = n_
                 end = e_ if end is None else max(end, e_)
             busy = sum(e_ - s_ for s_, e_, _ in ev)
             print(f"{name}: span {(ev[-1][1] - ev[0][0]) / 1e3:.2f} ms, kernel sum {busy / 1e3:.2f} ms, "
@@ -179,6 +192,17 @@ def main():
                 c[1] += e_ - s_
             for key, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1])[:12]:
                 print(f"   {c:4d} {t / 1e3:8.3f} ms  {key}", flush=True)
+        if os.environ.get("PYPROF") == "1" and name == "api":  # every rank runs it (collectives)
+            import cProfile
+            import pstats
+
+            timed(fn)  # first-use setup (exchange buffers, imports) outside the profile
+            pr = cProfile.Profile()
+            pr.enable()
+            timed(fn)
+            pr.disable()
+            if rank == 0:
+                pstats.Stats(pr).sort_stats("tottime").print_stats(22)
         ms, host = timed(fn)
         if rank == 0:
             print(f"{name:22s} {ms:8.2f} ms/step (wall, max over ranks)  {host:8.2f} ms/step host enqueue  "
