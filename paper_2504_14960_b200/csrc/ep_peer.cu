@@ -271,7 +271,7 @@ __device__ __forceinline__ void dispatch_token(
     }
   }
   // U column chunks per iteration keep several 16 B loads in flight per lane
-  constexpr int U = KMAX >= 4 ? 2 : 4;
+  constexpr int U = (BWD && KMAX >= 8) ? 1 : (KMAX >= 4 ? 2 : 4);
   const __nv_bfloat16* src = x + t * H;
   for (int64_t c0 = (int64_t)lane * 8; c0 < H; c0 += 256 * U) {
     Vec16<__nv_bfloat16> v[U];
@@ -329,7 +329,7 @@ __device__ __forceinline__ void dispatch_token(
 // next to a resident gemm_tc CTA (256 threads x 216 registers of 64 K), so
 // the push runs beside the GEMM instead of waiting for its SMs.
 template <int KMAX, bool BWD, int NT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 1 : (NT == 128 ? 6 : 7)) ep_dispatch_kernel(
+__global__ void __launch_bounds__(NT, NT == 256 ? (BWD && KMAX >= 4 ? 2 : 1) : (NT == 128 ? 6 : 7)) ep_dispatch_kernel(
     const __nv_bfloat16* __restrict__ x, int64_t Tn, int64_t H, int k, int L,
     const int32_t* __restrict__ topk, const int32_t* __restrict__ gemm_row,
     const int32_t* __restrict__ poff, const int32_t* __restrict__ seg_off,
