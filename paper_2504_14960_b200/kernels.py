@@ -6,6 +6,7 @@ torch caching allocator, and never synchronises.  There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Optional, Tuple
 
 import torch
@@ -13,7 +14,12 @@ import torch
 from . import _lib as L
 from .errors import ValidationError
 
-GEMM_ALIGN = 128  # rows per expert segment in the padded (GEMM) layout
+# rows per expert segment in the padded (GEMM) layout: a multiple of the
+# GEMM's 64-row K block (the weight-gradient GEMMs walk each expert's rows as
+# K); B200MOE_GEMM_ALIGN overrides (experiments; 64 or 128)
+GEMM_ALIGN = int(os.environ.get("B200MOE_GEMM_ALIGN", "128"))
+if GEMM_ALIGN not in (64, 128, 256):
+    raise ValidationError(f"B200MOE_GEMM_ALIGN={GEMM_ALIGN} must be 64, 128 or 256", constraint="gemm-align")
 
 
 def _cuda(t: torch.Tensor, name: str, dtype=None) -> torch.Tensor:

@@ -216,7 +216,9 @@ def test_smaller_receive_buffers_and_clean_overflow():
         from paper_2504_14960_b200.peer import capacity_rows
 
         cap = ctx.per_rank[0]["peer"].cap
-        assert cap == capacity_rows(2, T, k, E // 2, 128, 1.0) < capacity_rows(2, T, k, E // 2, 128)
+        from paper_2504_14960_b200.kernels import GEMM_ALIGN
+
+        assert cap == capacity_rows(2, T, k, E // 2, GEMM_ALIGN, 1.0) < capacity_rows(2, T, k, E // 2, GEMM_ALIGN)
         _same(ref, (outs, ctx, res))
         with pytest.raises(ProtocolError, match="overflows the peer receive buffers"):
             _, c2 = B.moe_forward(skew, weights, topo, params, world, dtype=torch.bfloat16)
