@@ -35,10 +35,12 @@ def cases(world):
     if world == 2:
         return [(1, 1, 2, 1, None, "subsequence", "swiglu", 8, 2), (2, 1, 1, 2, None, "subsequence", "relu", 8, 2),
                 (1, 2, 2, 1, 1.0, "fullsequence", "gelu", 8, 2), (2, 1, 2, 1, 1.0, "subsequence", "swiglu", 8, 2),
+                (1, 1, 2, 1, None, "subsequence", "swiglu", 2, 2),  # one expert per rank (C2 at EP8)
                 (1, 1, 2, 1, None, "subsequence", "swiglu", 16, 4)]
     return [(1, 1, world, 1, None, "subsequence", "swiglu", 8, 2), (2, 1, 2, 2, 1.0, "subsequence", "relu", 8, 2),
             (2, 2, 2, 2, 1.0, "fullsequence", "gelu", 8, 2),
             (1, 2, world // 2, 2, None, "subsequence", "swiglu", 8, 2),
+            (1, 1, world, 1, None, "subsequence", "swiglu", world, 2),  # one expert per rank
             (1, 1, world, 1, None, "subsequence", "swiglu", 16, 4)]
 
 
