@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256) combine_gather_kernel(
       for (int s = 0; s < KMAX; ++s)
         if (r[s] >= 0 && h < H) v[u][s].raw = ld_nc_v4(rows + (int64_t)r[s] * H + h);
     }
-    if (nparts > 1) {  // ETP partial rows: reduce (ep_reduce_parts' value), keep the row for later
+    if (nparts > 1 || rows_out) {  // ETP partial rows: reduce (ep_reduce_parts' value), keep the row
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         const int64_t h = h0 + (int64_t)u * 32 * V;

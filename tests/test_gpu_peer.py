@@ -288,7 +288,8 @@ def test_deduplicated_push_is_exact(world, ep, etp, E, k, monkeypatch):
             torch.testing.assert_close(b, a, rtol=0, atol=0)
 
 
-@pytest.mark.parametrize("nparts,k,E,H,dz,acc", [(2, 2, 8, 4096, False, False), (2, 2, 8, 4096, True, False),
+@pytest.mark.parametrize("nparts,k,E,H,dz,acc", [(1, 2, 8, 256, False, False), (2, 2, 8, 4096, False, False),
+                                                 (2, 2, 8, 4096, True, False),
                                                  (3, 4, 8, 256, True, True), (2, 8, 64, 512, False, True),
                                                  (4, 1, 4, 136, True, False)])
 def test_combine_parts_equals_reduce_then_combine(nparts, k, E, H, dz, acc):
