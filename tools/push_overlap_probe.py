@@ -100,6 +100,32 @@ def main():
     out["gemm + push2 (push first)"] = run(gemm, lambda: push(2))
     out["gemm + push0 (push first)"] = run(gemm, lambda: push(0))
     out["gemm + push2 (gemm first)"] = run(gemm, lambda: push(2), gemm_first=True)
+
+    # the fair comparison: one region from a common idle start to both done
+    def region(kind):
+        res = []
+        for _ in range(a.reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if kind == "serial":
+                push(0)
+                gemm()
+            else:
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    push(2)
+                gemm()
+                torch.cuda.current_stream().wait_stream(side)
+            e1.record()
+            torch.cuda.synchronize()
+            res.append(e0.elapsed_time(e1))
+        res.sort()
+        return res[len(res) // 2], 0.0
+
+    out["serial push0 -> gemm (region)"] = region("serial")
+    out["push2 beside gemm (region)"] = region("overlap")
     if rank == 0:
         bpsm = os.environ.get("B200MOE_PUSH_BLOCKS_PER_SM", "1") + " carve " + \
             os.environ.get("B200MOE_PUSH_CARVEOUT", "1")
