@@ -429,9 +429,8 @@ class RankLayer:
                          and self.pk.hidden % 8 == 0 and self.pk.ffn % 8 == 0)
         # peer path, B200MOE_PUSH_OVERLAP=1: the NVLink part of each push runs
         # on a side stream beside the first GEMM over the rank's own rows
-        # (bit-identical).  Off by default: measured, a concurrent push slows
-        # the tensor-core GEMM by about twice its own duration
-        # (tools/push_overlap_probe.py)
+        # (bit-identical).  Off by default: measured neutral to negative in the
+        # layer at 4 GPUs (-4 to +2 % across C2-C5)
         self.push_overlap = (self.use_peer and X.split_ok(self.pk, dtype)
                              and os.environ.get("B200MOE_PUSH_OVERLAP", "0") == "1")
         # step status (see _status_slot): the router writes bit 0 into the
