@@ -79,6 +79,13 @@ def main():
                          grouped_dim=0, G=E, M=0, N=H, K=ks, a_sm=N1, a_sk=1, b_sg=N1 * H, b_sk=H,
                          b_sn=1, c_sg=0, ldc=H, group_off=goff, max_rows=R, accumulate=s > 0)
 
+    _w1t = {}
+
+    def w1t():
+        if "t" not in _w1t:
+            _w1t["t"] = pk.w1p.transpose(1, 2).contiguous()
+        return _w1t["t"]
+
     runs = [
         ("fwd1 swiglu", 2 * fl_small, lambda: gemm_tc.ffn1_fused(x, pk, pre, h, goff, E, None, R)),
         ("fwd2 store", fl_small, lambda: gemm_tc.gemm(
@@ -89,6 +96,10 @@ def main():
             dpre, pk.w1p, dx, grouped_dim=0, G=E, M=0, N=H, K=N1, a_sm=N1, a_sk=1, b_sg=N1 * H,
             b_sk=H, b_sn=1, c_sg=0, ldc=H, group_off=goff, max_rows=R)),
         ("dgrad1 splitK", 2 * fl_small, lambda: dgrad1_split(a.splitk)),
+        # experiment: W1 as a K-major B operand (a transposed copy [E, H, N1])
+        ("dgrad1 kmajorB", 2 * fl_small, lambda: gemm_tc.gemm(
+            dpre, w1t(), dx, grouped_dim=0, G=E, M=0, N=H, K=N1, a_sm=N1, a_sk=1, b_sg=N1 * H,
+            b_sk=1, b_sn=N1, c_sg=0, ldc=H, group_off=goff, max_rows=R)),
         ("wgrad2 f32", fl_small, lambda: gemm_tc.gemm(
             dy, h, dw2, grouped_dim=1, G=E, M=H, N=F, K=0, a_sm=1, a_sk=H, b_sg=0, b_sk=F, b_sn=1,
             c_sg=H * F, ldc=F, group_off=goff, max_rows=R)),
