@@ -64,6 +64,7 @@ CASES = [
     (4, 2, 2, 8, 2, (192, 64, 128, 256), 1.0, "0"),  # EP x ETP with dropping (C3-like)
     (4, 2, 2, 16, 4, (128, 128, 96, 64), None, "1"),  # dedup with ETP siblings
     (8, 8, 1, 8, 2, (96, 128, 64, 160, 32, 128, 96, 64), None, "0"),  # C2 at EP8: one expert per rank
+    (2, 2, 1, 16, 4, (0, 256), None, "1"),  # a rank with an empty token block
 ]
 
 
