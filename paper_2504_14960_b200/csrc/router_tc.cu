@@ -49,6 +49,7 @@ struct Args {
   int E, k, gate_fn, renorm, nkb, stages;
   int bm;    // tokens per CTA tile (multiple of 8, <= 128): the grid covers every SM
   int ksub;  // 64-column K blocks per pipeline stage (stages = smem slots / ksub)
+  int krot;  // K-walk stagger between CTAs (blocks per CTA index; 0 = none)
   float* logits;
   float* scores;
   int32_t* idx;
@@ -172,10 +173,13 @@ __global__ void __launch_bounds__(256, 1) router_tc_kernel(const __grid_constant
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // CTAs start their K walk at staggered offsets so that concurrent tiles do
-  // not stream the same 8 KB-strided column block of x at the same time (the
-  // DRAM partitions stay evenly loaded); the fp32 sum order is fixed per CTA
-  const int kb_rot = (int)((blockIdx.x * 7u) % (unsigned)a.nkb);
+  // Every tile walks K from block 0 (krot = 0, the default): a token's fp32
+  // logit is then the same whatever tile -- i.e. whatever position in
+  // whatever rank's block -- it sits in, so splitting tokens over ranks
+  // changes no routing bit (tests/test_gpu_random_layers.py).  krot > 0
+  // staggers the CTAs' K walks (B200MOE_ROUTER_KROT, experiments: 31.2 vs
+  // 31.7 us at C2, not worth the batch-position dependence).
+  const int kb_rot = (int)((blockIdx.x * (unsigned)a.krot) % (unsigned)a.nkb);
   // a pipeline stage holds KS consecutive 64-column K blocks (KS smem slots,
   // one barrier pair): each x row is then read as KS x 128 contiguous bytes
   // per stage instead of 128 B -- DRAM page locality for the 8 KB-strided rows
@@ -263,10 +267,7 @@ static int launch(const void* x, int64_t T, int64_t H, const void* w, Args a, cu
   constexpr int STAGE = BM * BK * 2 + NP * BK * 2;
   // tile height 128.  Experiments: B200MOE_ROUTER_BM=n (multiple of 8), or
   // 0 = the fewest rows that spread T over every SM in one wave (112 at
-  // T = 16384: measured no faster, and a T-dependent tiling would make a
-  // token's K-walk rotation -- hence its fp32 logit -- depend on how the
-  // tokens are split over ranks; with 128-row tiles and 64 K blocks it does
-  // not: tests/test_gpu_fullsize.py, EP1 == EP2 bit for bit)
+  // T = 16384: measured no faster)
   static const int bm_env = [] {
     const char* e = getenv("B200MOE_ROUTER_BM");
     return e ? atoi(e) : -1;
@@ -290,6 +291,11 @@ static int launch(const void* x, int64_t T, int64_t H, const void* w, Args a, cu
   // tiles alike): the kernel's ~30 us is not DRAM-locality or SM-count bound
   a.ksub = ks_env >= 1 ? std::min(ks_env, a.stages / 2) : 1;
   a.stages = a.stages / a.ksub * a.ksub;
+  static const int krot_env = [] {
+    const char* e = getenv("B200MOE_ROUTER_KROT");
+    return e ? atoi(e) : 0;
+  }();
+  a.krot = krot_env;
   const int smem = 1024 + a.stages * STAGE + 16 * a.stages + 64;
   if (int e = ensure_max_smem(router_tc_kernel<EP>, 232448, "router_fwd_tc")) return e;
   router_tc_kernel<EP><<<(unsigned)ceil_div(T, bm), 256, smem, st>>>(mx, mw, a);
@@ -527,7 +533,7 @@ int router_fwd_tc(const void* x, int64_t T, int64_t H, const void* w_parts, int 
                   int renorm, float* logits, float* scores, int32_t* idx, float* gates, double* gates64,
                   int32_t* status, cudaStream_t st) {
   if (T == 0) return B200MOE_OK;
-  rtc::Args a{T, E, k, gate_fn, renorm, 0, 0, rtc::BM, 1, logits, scores, idx, gates, gates64, status};
+  rtc::Args a{T, E, k, gate_fn, renorm, 0, 0, rtc::BM, 1, 0, logits, scores, idx, gates, gates64, status};
   if (E <= 8) return rtc::launch<8>(x, T, H, w_parts, a, st);
   if (E <= 16) return rtc::launch<16>(x, T, H, w_parts, a, st);
   if (E <= 32) return rtc::launch<32>(x, T, H, w_parts, a, st);

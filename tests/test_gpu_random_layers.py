@@ -1,0 +1,117 @@
+"""GPU: a seeded sweep of random single-rank layer configurations against the
+oracle (bf16 and fp32): expert count, top-k, hidden / FFN widths (including
+ones that send the router and GEMMs down their CUDA-core paths), activation,
+gate function, renormalisation, capacity factor and priority, token count.
+Routing is compared bit for bit given the GPU's logits (dispatcher.py:246-510
+via oracle/moe_oracle.py); outputs and all gradients within the north star's
+tolerance."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import moe_oracle as O  # noqa: E402
+
+import paper_2504_14960_b200 as B  # noqa: E402
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-2}
+
+
+def _config(seed):
+    r = np.random.default_rng(1000 + seed)
+    E = int(r.choice([2, 4, 8, 16, 32, 64]))
+    k = int(r.integers(1, min(8, E) + 1))
+    act = str(r.choice(["relu", "gelu", "swiglu"]))
+    H = int(r.choice([64, 72, 128, 256, 320]))
+    F = int(r.choice([32, 64, 96, 160, 256]))
+    T = int(r.integers(1, 1500))
+    cf = [None, None, 1.0, 1.25, 2.0][int(r.integers(0, 5))]
+    gate = str(r.choice(["softmax", "sigmoid"]))
+    renorm = bool(r.integers(0, 2))
+    prio = str(r.choice(["position", "probability"])) if cf is not None else "position"
+    dtype = torch.bfloat16 if r.integers(0, 4) else torch.float32
+    return E, k, act, H, F, T, cf, gate, renorm, prio, dtype
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_layer_vs_oracle(seed):
+    E, k, act, H, F, T, cf, gate, renorm, prio, dtype = _config(seed)
+    tol = TOL[dtype]
+    wg = O.gating_matrix(H, E, seed) * (4.0 if gate == "sigmoid" else 1.0)
+    params = B.GatingParams(w_g=wg, k=k, gate_fn=gate, renormalize_topk=renorm, capacity_factor=cf,
+                            drop_priority=prio)
+    weights = B.init_expert_weights(E, H, F, 1, seed, activation=act)
+    x = O.token_rows(T, H, seed, 2)
+    u = O.token_rows(T, H, seed, 3)
+    xt = torch.as_tensor(x, dtype=torch.float32).to("cuda", dtype)
+    ut = torch.as_tensor(u, dtype=torch.float32).to("cuda", dtype)
+    outs, ctx = B.moe_forward([B.TokenBlock(xt, np.arange(T))], weights, B.ParallelTopology(world_size=1),
+                              params, B.LocalWorld(1))
+    res = B.moe_backward([ut], ctx)
+    sv = ctx.per_rank[0]
+    lg = sv["logits"].double().cpu().numpy()
+    w0 = weights[(0, 0)]
+    experts = [O.Expert(np.asarray(a), np.asarray(b), act) for a, b in zip(w0.w1, w0.w2)]
+    cfg = O.LayerConfig(k=k, gate_fn=gate, renormalize=renorm, capacity_factor=cf, drop_priority=prio)
+    xin = xt.double().cpu().numpy()
+    uin = ut.double().cpu().numpy()
+    y, st = O.layer_forward(xin, lg, experts, cfg)
+    masks = None
+    if act == "relu":  # relu' as the GPU saw it (pre within rounding of 0 may flip sign)
+        pre = sv["pre"].float().cpu().numpy()
+        poff = sv["plan_dev"].poffsets.cpu().numpy()
+        cnt = sv["plan_dev"].counts.cpu().numpy()
+        masks = {e: pre[poff[e]:poff[e] + cnt[e]] > 0 for e in range(E)}
+    g = O.layer_backward(uin, st, experts, cfg, w_g=wg, relu_masks=masks)
+    dec = sv["decision"]
+    np.testing.assert_array_equal(dec.experts.cpu().numpy(), st.routing.experts)
+    if prio == "position":  # probability priority orders by gate values: tolerance-checked
+        np.testing.assert_array_equal(dec.kept.cpu().numpy(), st.routing.kept)
+    else:
+        assert (dec.kept.cpu().numpy() != st.routing.kept).mean() < 1e-3
+        return
+    assert O.rel_err(outs[0].double().cpu().numpy(), y) < tol, "y"
+    assert O.rel_err(res.input_grads[0].double().cpu().numpy(), g[0]) < tol, "dx"
+    assert O.rel_err(res.w_g_grad.double().cpu().numpy(), g[2]) < tol, "dw_g"
+    for e in range(E):
+        if st.routing.kept[st.routing.experts == e].sum() == 0:
+            continue
+        assert O.rel_err(res.expert_grads[(0, 0)][0][e].double().cpu().numpy(), g[3][e]) < tol, ("dw1", e)
+        assert O.rel_err(res.expert_grads[(0, 0)][1][e].double().cpu().numpy(), g[4][e]) < tol, ("dw2", e)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_ep_split_is_bit_identical(seed):
+    """Factorisation independence (reference tests/test_dispatcher.py:194-217)
+    on random configurations: the same tokens over EP = 2 or 4 emulated ranks
+    (peer exchange, host or device barriers) give the single-rank outputs and
+    input gradients bit for bit (bf16, dropless)."""
+    r = np.random.default_rng(5000 + seed)
+    world = int(r.choice([2, 4]))
+    E = world * int(r.choice([1, 2, 4]))
+    k = int(r.integers(1, min(8, E) + 1))
+    act = str(r.choice(["relu", "gelu", "swiglu"]))
+    H, F = int(r.choice([64, 128, 256])), int(r.choice([64, 128, 192]))
+    sizes = [int(v) for v in r.integers(0, 400, size=world)]
+    T = sum(sizes)
+    wg = O.gating_matrix(H, E, seed)
+    params = B.GatingParams(w_g=wg, k=k)
+    x = torch.as_tensor(O.token_rows(max(T, 1), H, seed, 2)[:T], dtype=torch.float32).to("cuda", torch.bfloat16)
+    u = torch.as_tensor(O.token_rows(max(T, 1), H, seed, 3)[:T], dtype=torch.float32).to("cuda", torch.bfloat16)
+    one = B.init_expert_weights(E, H, F, 1, seed, activation=act)
+    outs1, ctx1 = B.moe_forward([B.TokenBlock(x, np.arange(T))], one, B.ParallelTopology(world_size=1), params,
+                                B.LocalWorld(1))
+    res1 = B.moe_backward([u], ctx1)
+    topo = B.ParallelTopology(world_size=world, ep=world)
+    split = B.init_expert_weights(E, H, F, 1, seed, ep_size=world, activation=act)
+    bounds = np.concatenate(([0], np.cumsum(sizes)))
+    blocks = [B.TokenBlock(x[bounds[i]:bounds[i + 1]].contiguous(), np.arange(bounds[i], bounds[i + 1]))
+              for i in range(world)]
+    ups = [u[bounds[i]:bounds[i + 1]].contiguous() for i in range(world)]
+    outs, ctx = B.moe_forward(blocks, split, topo, params, B.LocalWorld(world, device_barrier=bool(seed % 2)))
+    res = B.moe_backward(ups, ctx)
+    assert all(sv.get("peer") is not None for sv in ctx.per_rank)
+    torch.testing.assert_close(torch.cat(outs), outs1[0], rtol=0, atol=0)
+    torch.testing.assert_close(torch.cat(res.input_grads), res1.input_grads[0], rtol=0, atol=0)
+    assert O.rel_err(res.w_g_grad.double().cpu().numpy(), res1.w_g_grad.double().cpu().numpy()) < 1e-5
