@@ -174,3 +174,53 @@ def test_random_multi_rank_peer_vs_nccl(seed):
                         r1.expert_grads[key][0] + r1.expert_grads[key][1]):
             if float(a.abs().max()) > 0:
                 assert O.rel_err(b.cpu().numpy(), a.cpu().numpy()) < 1e-3
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_full_sequence_meshes_peer_vs_nccl(seed):
+    """Full-sequence dropping (router.py:209-269) on random TP x CP x EP
+    meshes of 2 or 4 emulated ranks: the kept masks of the device-native
+    gather agree between the two exchanges and equal the oracle's capacity
+    pass over each whole sequence given the GPU's routing; outputs agree."""
+    r = np.random.default_rng(13000 + seed)
+    world = int(r.choice([2, 4]))
+    tp = int(r.choice([1, 2])) if world >= 2 else 1
+    cp = int(r.choice([1, 2])) if world // tp >= 2 else 1
+    ep = int(r.choice([d for d in (1, 2, 4) if d <= world and world % d == 0 and d > 1] or [1]))
+    topo = B.ParallelTopology(world_size=world, tp=tp, cp=cp, ep=ep)
+    E = ep * int(r.choice([1, 2, 4]))
+    k = int(r.integers(1, min(4, E) + 1))
+    H, F = int(r.choice([64, 128])), int(r.choice([64, 128]))
+    seq_len = int(r.choice([64, 128, 256])) * tp * cp
+    cf = float(r.choice([1.0, 1.25, 2.0]))
+    params = B.GatingParams(w_g=O.gating_matrix(H, E, seed), k=k, capacity_factor=cf, drop_mode="fullsequence")
+    weights = B.init_expert_weights(E, H, F, 1, seed, ep_size=ep, activation="swiglu")
+    _, blocks = B.fabricate_token_blocks(topo, seq_len, topo.dp, H, seed, dtype=torch.bfloat16)
+    _, ups = B.fabricate_upstream(topo, seq_len, topo.dp, H, seed, dtype=torch.bfloat16)
+    got = {}
+    for xch in ("nccl", "peer"):
+        outs, ctx = B.moe_forward(blocks, weights, topo, params, B.LocalWorld(world), dtype=torch.bfloat16,
+                                  seq_len=seq_len, exchange=xch)
+        got[xch] = (outs, ctx, B.moe_backward(ups, ctx))
+    (o0, c0, _), (o1, c1, _) = got["nccl"], got["peer"]
+    # the oracle's full-sequence capacity over the GPU's own routing
+    cap = O.capacity_limit(cf, seq_len, E)
+    seqs = {}
+    for rank in range(world):
+        dec = c1.per_rank[rank]["decision"]
+        pos = np.asarray(blocks[rank].positions)
+        for i, p in enumerate(pos):
+            seqs.setdefault(int(p) // seq_len, []).append((int(p), rank, i))
+        np.testing.assert_array_equal(c0.per_rank[rank]["decision"].kept.cpu().numpy(), dec.kept.cpu().numpy())
+        torch.testing.assert_close(o1[rank], o0[rank], rtol=0, atol=0)
+    for s_id, toks in seqs.items():
+        toks.sort()
+        used = np.zeros(E, dtype=np.int64)
+        for p, rank, i in toks:
+            dec = c1.per_rank[rank]["decision"]
+            ex = dec.experts[i].cpu().numpy()
+            kept = dec.kept[i].cpu().numpy()
+            for slot in range(k):
+                want = used[ex[slot]] < cap
+                assert bool(kept[slot]) == want, (s_id, p, slot)
+                used[ex[slot]] += int(want)
