@@ -1,3 +1,10 @@
+"""Host synchronisations in the public API's steady state (1 GPU): runs
+moe_forward / moe_backward under torch's sync-debug "warn" mode and prints
+every synchronising call (expected: none -- the status check is an event
+query).
+
+    python tools/sync_probe.py
+"""
 import os, sys, warnings, traceback
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
